@@ -1,0 +1,154 @@
+/*
+ * d4orm_cuda.h — the drop-in C-ABI boundary of the B200 denoise-step path.
+ *
+ * The reference (D4orm, /root/reference/proj) has no FFI: its operator
+ * boundary is the C++ function
+ *     DenoiseResult run_denoising(const JointControls& base, const Scenario&,
+ *                                 const DynamicsModel&, const NoiseSchedule&,
+ *                                 const DenoiserConfig&, double dt)
+ *     (proj/include/d4orm/denoiser.hpp:68-70, proj/src/denoiser.cpp:119-184)
+ * plus the public sub-operators it is built from (denoiser.hpp:44-58,
+ * dynamics.hpp:148-155, reward.hpp:49-51).  Each entry point below replaces one
+ * of them; the C++ drop-in in include/d4orm/*.hpp (same names and signatures as
+ * the reference headers) is a thin layer over these calls that turns status
+ * codes back into the reference's exception types and messages.
+ *
+ * Conventions: plain pointers and sizes, host memory, column-major fp64 exactly
+ * as the reference's Eigen matrices (u: (R*du) x T -> element (k*du+d, t) at
+ * t*R*du + k*du + d).  Every call returns D4ORM_OK or an error code; the
+ * message is available from d4orm_cuda_last_error(ctx).  A context owns one
+ * GPU stream and is used by one host thread at a time (the reference's
+ * run_denoising is re-entrant per call).
+ */
+#ifndef D4ORM_CUDA_H
+#define D4ORM_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  D4ORM_OK = 0,
+  D4ORM_E_INVALID = 1,  /* std::invalid_argument in the reference */
+  D4ORM_E_RUNTIME = 2,  /* std::runtime_error (non-finite state / reward) */
+  D4ORM_E_CUDA = 3,
+  D4ORM_E_NCCL = 4,
+  D4ORM_E_UNSUPPORTED = 5
+};
+
+/* ModelKind (dynamics.hpp:11) + the BASELINE extensions. */
+enum {
+  D4ORM_DIFFDRIVE = 0,
+  D4ORM_HOLO2D = 1,
+  D4ORM_HOLO3D = 2,
+  D4ORM_HOLO2D_VEL = 3,
+  D4ORM_HOLO3D_VEL = 4,
+  D4ORM_UNICYCLE = 5
+};
+
+enum { D4ORM_FROM_SCRATCH = 0, D4ORM_DEFORMATION = 1 };   /* DenoiseMode, denoiser.hpp:14-17 */
+enum { D4ORM_NOISE_PHILOX = 0, D4ORM_NOISE_HOST = 1 };    /* K1 in-HBM Philox | host buffer */
+enum { D4ORM_PREC_F32 = 0, D4ORM_PREC_F64 = 1 };          /* throughput | parity arithmetic */
+
+/* Problem = Scenario (scenario.hpp:17-30) + DynamicsModel (dynamics.hpp:22-34)
+ * + RewardConfig (reward.hpp:13-19) + the rollout dt/horizon. */
+typedef struct {
+  int kind;
+  int dx, du, pdim;       /* must match kind */
+  int robots;             /* R */
+  int horizon;            /* T */
+  double dt;
+  double lower[3], upper[3];
+  const double* starts;   /* dx x R column-major (Scenario::starts) */
+  const double* goals;    /* pdim x R (Scenario::goals) */
+  int n_obstacles;
+  const double* obs_centers; /* pdim x O */
+  const double* obs_radii;   /* O */
+  double w_t, epsilon, robot_radius, goal_tolerance, obstacle_weight;
+  double effort_weight;   /* extension; 0 = reference reward */
+} d4orm_problem;
+
+/* DenoiserConfig (denoiser.hpp:19-27); `batch` is BASELINE's "N samples". */
+typedef struct {
+  int steps;
+  int64_t batch;
+  double lambda;
+  double alpha_bar_final;
+  uint64_t seed;
+  int mode;
+} d4orm_denoiser_config;
+
+/* DenoiseStepRecord (denoiser.hpp:29-34) */
+typedef struct {
+  int step;
+  double best_reward, mean_reward, weight_entropy;
+} d4orm_trace_rec;
+
+/* Host noise provider for D4ORM_NOISE_HOST: fill dst (count x elems fp64,
+ * row = sample m0+j) with the standard normals of denoising step `step`.
+ * Return 0 on success. */
+typedef int (*d4orm_noise_fn)(void* user, int step, int64_t m0, int64_t count, int64_t elems,
+                              double* dst);
+
+typedef struct d4orm_cuda_ctx d4orm_cuda_ctx;
+
+/* ---- lifetime ---------------------------------------------------------- */
+/* One context per (process, GPU).  world > 1 shards the samples across ranks;
+ * nccl_id is the 128-byte ncclUniqueId rank 0 created (d4orm_cuda_nccl_id),
+ * broadcast by the caller.  world == 1: nccl_id may be NULL. */
+int d4orm_cuda_create(int device, int rank, int world, const void* nccl_id, d4orm_cuda_ctx** out);
+int d4orm_cuda_nccl_id(void* out128);
+void d4orm_cuda_destroy(d4orm_cuda_ctx* ctx);
+const char* d4orm_cuda_last_error(const d4orm_cuda_ctx* ctx);
+const char* d4orm_cuda_version(void);
+
+/* ---- configuration ------------------------------------------------------- */
+/* validate_scenario-style checks (scenario.cpp:46-108 subset used by the path)
+ * then upload to HBM. */
+int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* problem);
+int d4orm_cuda_set_options(d4orm_cuda_ctx* ctx, int precision, int noise_source, int use_graphs);
+int d4orm_cuda_set_noise_fn(d4orm_cuda_ctx* ctx, d4orm_noise_fn fn, void* user);
+
+/* ---- the path: run_denoising (denoiser.cpp:119-184) ----------------------- */
+/* base: (R*du) x T; out_variable: (R*du) x T; trace: config->steps records
+ * (may be NULL).  Errors mirror the reference's messages. */
+int d4orm_cuda_run_denoising(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* config,
+                             double* out_variable, d4orm_trace_rec* trace);
+
+/* ---- per-stage entry points (parity) -------------------------------------- */
+/* One denoising step i (loop body denoiser.cpp:152-180) from a given variable;
+ * noise (batch x elems, fp64) or NULL for Philox. Outputs may be NULL. */
+int d4orm_cuda_denoise_step(d4orm_cuda_ctx* ctx, const double* base, const double* variable_in,
+                            const double* noise, int i, const d4orm_denoiser_config* config,
+                            double* variable_out, double* rewards, double* weights, d4orm_trace_rec* rec);
+/* rollout (dynamics.cpp:122-169) + total_reward (reward.cpp:67-130) of `count`
+ * candidate control sequences u (count x (R*du*T)).  states: count x (R*dx)x(T+1),
+ * controls: count x (R*du)x(T+1); counts: count x 2 (conflict, obstacle
+ * robot-steps).  Any output may be NULL. */
+int d4orm_cuda_rollout_fitness(d4orm_cuda_ctx* ctx, const double* u, int64_t count, double* states,
+                               double* controls, double* rewards, int64_t* counts);
+/* score_weights (denoiser.cpp:50-90) + entropy (:24-30). trace4 = {best, mean, entropy}. */
+int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t m, double lambda,
+                             double* weights, double* trace3);
+/* K1: the Philox normals of (seed, step) for samples [m0, m0+count). */
+int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_t m0, int64_t count,
+                            float* out);
+
+/* ---- device-resident benchmarking ----------------------------------------- */
+/* Prepare a device-resident run (base uploaded once), then time `steps`
+ * denoising steps after `warmup` untimed ones, with CUDA events on the
+ * context's stream.  Fills ms_total and, if non-NULL, per-kernel average
+ * milliseconds kernel_ms[5] = {K1 noise, K2+K3 rollout+fitness, K4 weights,
+ * K5 partial, K5 tree} (measured in a separate instrumented pass). */
+int d4orm_cuda_bench_steps(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* config,
+                           int warmup, int steps, double* ms_total, double* kernel_ms);
+/* Number of this library's kernel launches per denoising step (graph nodes). */
+int d4orm_cuda_launches_per_step(const d4orm_cuda_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,80 @@
+"""In-tree build of the sm_100a library ``libd4orm_b200.so`` (and the oracle).
+
+Compiles every ``csrc/*.cu`` and ``csrc/*.cpp`` with nvcc for
+``-gencode arch=compute_100a,code=sm_100a`` in parallel, links one shared
+object next to this file, and (when asked) builds the test-only oracle via
+``oracle/Makefile``.  No PyTorch extension machinery: the product boundary is
+the C-ABI in ``include/d4orm_cuda.h``.
+"""
+from __future__ import annotations
+
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+OBJ = PKG / "build"
+LIB = PKG / "libd4orm_b200.so"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+              f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+
+
+def _nvcc() -> str:
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found: cannot build the sm_100a library")
+
+
+def _newer(src: Path, obj: Path, deps: list[Path]) -> bool:
+    if not obj.exists():
+        return True
+    t = obj.stat().st_mtime
+    return src.stat().st_mtime > t or any(d.stat().st_mtime > t for d in deps)
+
+
+def build(verbose: bool = False, jobs: int | None = None) -> Path:
+    nvcc = _nvcc()
+    OBJ.mkdir(exist_ok=True)
+    headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").rglob("*.h*"))
+    srcs = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
+    cmds = []
+    objs = []
+    for s in srcs:
+        o = OBJ / (s.name + ".o")
+        objs.append(o)
+        if _newer(s, o, headers):
+            lang = [] if s.suffix == ".cu" else ["-x", "cu"] if False else []
+            cmds.append([nvcc, *ARCH, *NVCC_FLAGS, *lang, "-c", str(s), "-o", str(o)])
+
+    def run(cmd):
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if verbose or r.returncode:
+            sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        if r.returncode:
+            raise RuntimeError(f"compile failed: {cmd[-3]}")
+        return r
+
+    with cf.ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
+        list(ex.map(run, cmds))
+    if cmds or not LIB.exists():
+        run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-ldl", "-lcudart"])
+    return LIB
+
+
+def build_oracle() -> None:
+    """Test-only checker: oracle/build/libd4orm_oracle.so and, where
+    /root/reference exists, oracle/_ref/libd4orm_ref.so."""
+    subprocess.run(["make", "-s", "-f", str(ROOT / "oracle" / "Makefile")], check=True)
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))
+    if "--oracle" in sys.argv:
+        build_oracle()

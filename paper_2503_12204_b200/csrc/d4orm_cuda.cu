@@ -1,0 +1,994 @@
+// d4orm_cuda.cu — context, orchestration and C-ABI (include/d4orm_cuda.h).
+//
+// One denoising step (denoiser.cpp:152-180) is five launches on the context's
+// stream, captured once per (problem, config, step) as a CUDA graph:
+//
+//   K1(i-1) Philox noise for the *next* step, on a forked branch (HBM-bound,
+//           overlaps the compute-bound K2+K3 of this step; z is double-buffered)
+//   K2+K3(i) rollout + fitness → reward[m]           (this rank's samples)
+//   [NCCL all-gather of rewards when world > 1]
+//   K4(i)   z-scored softmax weights over all M rewards (every rank, identical)
+//   K5(i)   chunked weighted mean + deterministic tree → variable, mean-scaled
+//           variable for step i-1 [NCCL all-gather of chunk-tree roots]
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/d4orm_cuda.h"
+#include "d4orm_kernels.cuh"
+
+namespace d4k {
+template <typename S, int KIND>
+cudaError_t launch_k23(int tb, int maxw, dim3 grid, size_t smem, cudaStream_t st, const FitParams<S>& p);
+}
+
+namespace {
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+// Only world > 1 needs NCCL; it is resolved at run time so single-GPU use has
+// no NCCL dependency.  Types mirror nccl.h (2.x ABI).
+typedef struct ncclComm* ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclInt8 = 0, ncclFloat32 = 7, ncclFloat64 = 8 };
+enum { ncclSum = 0 };
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool load(std::string* err) {
+    if (h) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) {
+      *err = "NCCL not found (dlopen libnccl.so.2)";
+      return false;
+    }
+    GetUniqueId = (decltype(GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (decltype(CommInitRank))dlsym(h, "ncclCommInitRank");
+    CommDestroy = (decltype(CommDestroy))dlsym(h, "ncclCommDestroy");
+    AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
+    GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !CommDestroy || !AllGather || !GetErrorString) {
+      *err = "NCCL symbols missing";
+      return false;
+    }
+    return true;
+  }
+};
+Nccl g_nccl;
+
+// splitmix64 / mix_seed (rng.hpp:10-23)
+uint64_t splitmix64(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+uint64_t mix_seed(uint64_t a, uint64_t b) { return splitmix64(splitmix64(a) ^ (0x9e3779b97f4a7c15ull + b)); }
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    cudaError_t e = cudaMalloc(&p, sizeof(T) * (count ? count : 1));
+    if (e == cudaSuccess) n = count;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+constexpr int kChunk = 256;   // samples per K5 partial (fixed → GPU-count invariant tree)
+constexpr int kWeightThreads = 1024;
+
+}  // namespace
+
+struct StepGraph {
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct d4orm_cuda_ctx {
+  int device = 0, rank = 0, world = 1;
+  cudaStream_t s_main = nullptr, s_noise = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
+  std::vector<cudaEvent_t> ev_k;  // instrumented per-kernel timing
+  ncclComm_t comm = nullptr;
+  std::string err;
+
+  // problem (host copies)
+  bool has_problem = false;
+  d4orm_problem prob{};
+  std::vector<double> starts, goals, obs_c, obs_r;
+  int TB = 16, Rp = 16, MAXW = 2, spc = 16, TC = 16;
+  size_t smem32 = 0, smem64 = 0;
+  int TC32 = 16, TC64 = 16;
+
+  // options
+  int precision = D4ORM_PREC_F32, noise_source = D4ORM_NOISE_PHILOX, use_graphs = 1;
+  d4orm_noise_fn noise_fn = nullptr;
+  void* noise_user = nullptr;
+
+  // device buffers (typeless where the scalar type varies)
+  DevBuf<unsigned char> z[2], base, msv, starts_d, goals_d, inv_d, obs_d, partial, roots;
+  DevBuf<unsigned char> states_out, controls_out;
+  DevBuf<double> var, rewards, w64, trace;
+  DevBuf<float> w32;
+  DevBuf<int> counts;
+  DevBuf<unsigned long long> errw;
+  DevBuf<uint2> keys;
+  std::vector<double> ab;  // alpha_bar of the current schedule
+
+  // cached graphs: key → per-step graph execs
+  std::string graph_key;
+  std::vector<StepGraph> graphs;
+
+  ~d4orm_cuda_ctx() {
+    cudaSetDevice(device);
+    for (auto& g : graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    for (auto* b : {&z[0], &z[1], &base, &msv, &starts_d, &goals_d, &inv_d, &obs_d, &partial, &roots,
+                    &states_out, &controls_out})
+      b->release();
+    var.release(); rewards.release(); w64.release(); trace.release(); w32.release();
+    counts.release(); errw.release(); keys.release();
+    for (auto e : ev_k) cudaEventDestroy(e);
+    for (auto e : {ev_fork, ev_join, ev_t0, ev_t1})
+      if (e) cudaEventDestroy(e);
+    if (s_main) cudaStreamDestroy(s_main);
+    if (s_noise) cudaStreamDestroy(s_noise);
+    if (comm && g_nccl.CommDestroy) g_nccl.CommDestroy(comm);
+  }
+};
+
+namespace {
+
+int fail(d4orm_cuda_ctx* c, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CU(call)                                                                              \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail(ctx, D4ORM_E_CUDA, "CUDA error %s at %s:%d (%s)", cudaGetErrorString(e_),   \
+                  __FILE__, __LINE__, #call);                                                 \
+  } while (0)
+
+#define NC(call)                                                                                       \
+  do {                                                                                                 \
+    ncclResult_t r_ = (call);                                                                          \
+    if (r_ != 0) return fail(ctx, D4ORM_E_NCCL, "NCCL error %s at %s:%d", g_nccl.GetErrorString(r_), \
+                             __FILE__, __LINE__);                                                      \
+  } while (0)
+
+bool dims_of(int kind, int* dx, int* du, int* pd) {
+  static const int DX[6] = {4, 4, 6, 2, 3, 3}, DU[6] = {2, 2, 3, 2, 3, 2}, PD[6] = {2, 2, 3, 2, 3, 2};
+  if (kind < 0 || kind > 5) return false;
+  *dx = DX[kind];
+  *du = DU[kind];
+  *pd = PD[kind];
+  return true;
+}
+
+int64_t elems_of(const d4orm_cuda_ctx* c) { return (int64_t)c->prob.robots * c->prob.du * c->prob.horizon; }
+
+template <typename S>
+size_t fit_smem(const d4orm_cuda_ctx* c, int TC) {
+  const int PD = c->prob.pdim;
+  size_t b = (size_t)PD * c->spc * c->Rp * (TC + 1) * sizeof(S);
+  b += (size_t)c->Rp * PD * sizeof(S) + (size_t)c->Rp * sizeof(S) + (size_t)(4 * c->prob.n_obstacles + 2) * sizeof(S);
+  b += 16 + 2 * d4k::kThreads * sizeof(double) + 2 * d4k::kThreads * sizeof(int);
+  return b;
+}
+
+template <typename S>
+int choose_tc(d4orm_cuda_ctx* ctx, int* tc_out, size_t* smem_out) {
+  int TC = ctx->Rp >= 16 ? (ctx->Rp < 64 ? ctx->Rp : 64) : 16;
+  while (fit_smem<S>(ctx, TC) > 200 * 1024 && TC > 4) TC /= 2;
+  if (TC >= ctx->Rp && TC % ctx->Rp != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d vs Rp %d", TC, ctx->Rp);
+  *tc_out = TC;
+  *smem_out = fit_smem<S>(ctx, TC);
+  return D4ORM_OK;
+}
+
+template <typename S>
+cudaError_t upload_as(DevBuf<unsigned char>& buf, const double* src, size_t n, cudaStream_t st) {
+  cudaError_t e = buf.ensure(n * sizeof(S));
+  if (e != cudaSuccess) return e;
+  std::vector<S> tmp(n);
+  for (size_t j = 0; j < n; ++j) tmp[j] = (S)src[j];
+  e = cudaMemcpyAsync(buf.p, tmp.data(), n * sizeof(S), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(st);
+}
+
+// Upload the problem constants in the scalar type of the current precision.
+template <typename S>
+int upload_problem(d4orm_cuda_ctx* ctx) {
+  const d4orm_problem& p = ctx->prob;
+  const int R = p.robots, PD = p.pdim;
+  CU((upload_as<S>(ctx->starts_d, ctx->starts.data(), ctx->starts.size(), ctx->s_main)));
+  CU((upload_as<S>(ctx->goals_d, ctx->goals.data(), ctx->goals.size(), ctx->s_main)));
+  std::vector<double> inv(R);
+  for (int k = 0; k < R; ++k) {
+    double s = 0.0;
+    for (int j = 0; j < PD; ++j) {
+      const double d = ctx->starts[(size_t)k * p.dx + j] - ctx->goals[(size_t)k * PD + j];
+      s += d * d;
+    }
+    // fp64 parity keeps the reference's division by the start distance
+    // (reward.cpp:81,96); fp32 multiplies by its reciprocal.
+    inv[k] = std::is_same<S, double>::value ? std::sqrt(s) : 1.0 / std::sqrt(s);
+  }
+  CU((upload_as<S>(ctx->inv_d, inv.data(), R, ctx->s_main)));
+  std::vector<double> obs((size_t)4 * p.n_obstacles + 1, 0.0);
+  for (int o = 0; o < p.n_obstacles; ++o) {
+    for (int j = 0; j < PD; ++j) obs[4 * o + j] = ctx->obs_c[(size_t)o * PD + j];
+    const double lim = ctx->obs_r[o] + p.robot_radius;
+    const double l2 = lim * lim;
+    if (std::is_same<S, double>::value) {
+      obs[4 * o + 3] = l2;
+    } else {
+      obs[4 * o + 3] = -(double)std::nextafter((float)l2, INFINITY);
+    }
+  }
+  CU((upload_as<S>(ctx->obs_d, obs.data(), obs.size(), ctx->s_main)));
+  return D4ORM_OK;
+}
+
+template <typename S>
+d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, const S* msv, double sd, int64_t M,
+                             int64_t m_global0, int step_key, double* reward, int* counts, S* states_out,
+                             S* controls_out, int TC) {
+  const d4orm_problem& p = ctx->prob;
+  d4k::FitParams<S> f{};
+  f.z = z;
+  f.base = base;
+  f.msv = msv;
+  f.sd = (S)sd;
+  f.starts = (const S*)ctx->starts_d.p;
+  f.goals = (const S*)ctx->goals_d.p;
+  f.inv_dstart = (const S*)ctx->inv_d.p;
+  f.obs = (const S*)ctx->obs_d.p;
+  f.n_obs = p.n_obstacles;
+  for (int d = 0; d < 3; ++d) {
+    f.lower[d] = (S)p.lower[d];
+    f.upper[d] = (S)p.upper[d];
+  }
+  f.dt = (S)p.dt;
+  f.half_dt = (S)(0.5 * p.dt);
+  f.dt6 = (S)(p.dt / 6.0);
+  const double margin = 2.0 * p.robot_radius + p.epsilon;
+  const double m2 = margin * margin;
+  if (std::is_same<S, double>::value) f.neg_margin_sq = (S)m2;
+  else f.neg_margin_sq = (S)(-(double)std::nextafter((float)m2, INFINITY));
+  f.w_t = p.w_t;
+  f.w_o = p.obstacle_weight;
+  f.w_e = p.effort_weight;
+  f.R = p.robots;
+  f.Rp = ctx->Rp;
+  f.T = p.horizon;
+  f.TC = TC;
+  f.spc = ctx->spc;
+  f.M = M;
+  f.m_global0 = m_global0;
+  f.step_key = step_key;
+  f.reward = reward;
+  f.counts = counts;
+  f.states_out = states_out;
+  f.controls_out = controls_out;
+  f.err = ctx->errw.p;
+  return f;
+}
+
+template <typename S>
+cudaError_t launch_fit(d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f, size_t smem) {
+  const dim3 grid((unsigned)((f.M + ctx->spc - 1) / ctx->spc));
+  switch (ctx->prob.kind) {
+    case 0: return d4k::launch_k23<S, 0>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
+    case 1: return d4k::launch_k23<S, 1>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
+    case 2: return d4k::launch_k23<S, 2>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
+    case 3: return d4k::launch_k23<S, 3>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
+    case 4: return d4k::launch_k23<S, 4>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
+    default: return d4k::launch_k23<S, 5>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
+  }
+}
+
+// ------------------------------------------------------------ run plumbing
+struct RunShape {
+  int64_t M = 0, Ml = 0, m0 = 0, E = 0, chunks_local = 0;
+  int N = 0;
+  double lambda = 0.1, abf = 0.05;
+  int mode = D4ORM_DEFORMATION;
+};
+
+int check_config(d4orm_cuda_ctx* ctx, const d4orm_denoiser_config* c, RunShape* rs) {
+  if (!ctx->has_problem) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: set_problem not called");
+  if (c->batch < 2) return fail(ctx, D4ORM_E_INVALID, "run_denoising: batch must be >= 2");
+  if (!(c->lambda > 0.0)) return fail(ctx, D4ORM_E_INVALID, "run_denoising: lambda must be > 0");
+  if (c->steps < 1) return fail(ctx, D4ORM_E_INVALID, "make_schedule: steps must be >= 1, got %d", c->steps);
+  if (!(c->alpha_bar_final > 0.0) || !(c->alpha_bar_final < 1.0))
+    return fail(ctx, D4ORM_E_INVALID, "make_schedule: alpha_bar_final must lie in (0, 1), got %f", c->alpha_bar_final);
+  if (c->batch % ctx->world != 0)
+    return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: batch %lld not divisible by world %d", (long long)c->batch, ctx->world);
+  rs->M = c->batch;
+  rs->Ml = c->batch / ctx->world;
+  rs->m0 = rs->Ml * ctx->rank;
+  if (ctx->world > 1 && rs->Ml % kChunk != 0)
+    return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: per-rank batch must be a multiple of %d", kChunk);
+  rs->E = elems_of(ctx);
+  rs->chunks_local = (rs->Ml + kChunk - 1) / kChunk;
+  rs->N = c->steps;
+  rs->lambda = c->lambda;
+  rs->abf = c->alpha_bar_final;
+  rs->mode = c->mode;
+  // schedule (schedule.cpp:9-27)
+  ctx->ab.assign((size_t)rs->N + 1, 1.0);
+  for (int i = 1; i <= rs->N; ++i) ctx->ab[i] = std::pow(c->alpha_bar_final, (double)i / rs->N);
+  return D4ORM_OK;
+}
+
+size_t ssize(const d4orm_cuda_ctx* c) { return c->precision == D4ORM_PREC_F64 ? sizeof(double) : sizeof(float); }
+
+int ensure_buffers(d4orm_cuda_ctx* ctx, const RunShape& rs, bool two_z) {
+  const size_t S = ssize(ctx);
+  CU(ctx->z[0].ensure((size_t)rs.Ml * rs.E * S));
+  if (two_z) CU(ctx->z[1].ensure((size_t)rs.Ml * rs.E * S));
+  CU(ctx->base.ensure((size_t)rs.E * S));
+  CU(ctx->msv.ensure((size_t)rs.E * S));
+  CU(ctx->var.ensure((size_t)rs.E));
+  CU(ctx->rewards.ensure((size_t)rs.M));
+  CU(ctx->w64.ensure((size_t)rs.M));
+  CU(ctx->w32.ensure((size_t)rs.M));
+  CU(ctx->partial.ensure((size_t)rs.chunks_local * rs.E * S));
+  CU(ctx->roots.ensure((size_t)ctx->world * rs.E * S));
+  CU(ctx->trace.ensure((size_t)4 * (rs.N + 1)));
+  CU(ctx->errw.ensure(1));
+  CU(ctx->keys.ensure((size_t)rs.N + 1));
+  return D4ORM_OK;
+}
+
+int set_keys(d4orm_cuda_ctx* ctx, const RunShape& rs, uint64_t seed) {
+  std::vector<uint2> k((size_t)rs.N + 1);
+  for (int i = 0; i <= rs.N; ++i) {
+    const uint64_t v = mix_seed(seed, (uint64_t)i);
+    k[i] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+  }
+  CU(cudaMemcpyAsync(ctx->keys.p, k.data(), sizeof(uint2) * k.size(), cudaMemcpyHostToDevice, ctx->s_main));
+  return D4ORM_OK;
+}
+
+template <typename S>
+int launch_noise(d4orm_cuda_ctx* ctx, cudaStream_t st, int slot, const RunShape& rs, int step) {
+  const int64_t groups = rs.Ml * ((rs.E + 3) / 4);
+  int64_t blocks = (groups + d4k::kThreads - 1) / d4k::kThreads;
+  if (blocks > 148 * 64) blocks = 148 * 64;
+  d4k::k_philox_noise<S><<<(unsigned)blocks, d4k::kThreads, 0, st>>>((S*)ctx->z[slot].p, rs.Ml, rs.E, rs.m0,
+                                                                     ctx->keys.p, step);
+  CU(cudaGetLastError());
+  return D4ORM_OK;
+}
+
+int host_noise(d4orm_cuda_ctx* ctx, const RunShape& rs, int step, int64_t m0, int64_t count, const double* given,
+               void* dst) {
+  std::vector<double> buf;
+  const double* src = given;
+  if (!src) {
+    if (!ctx->noise_fn) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: host noise selected but no noise fn set");
+    buf.resize((size_t)count * rs.E);
+    if (ctx->noise_fn(ctx->noise_user, step, m0, count, rs.E, buf.data()) != 0)
+      return fail(ctx, D4ORM_E_RUNTIME, "d4orm_cuda: noise fn failed at step %d", step);
+    src = buf.data();
+  }
+  const size_t n = (size_t)count * rs.E;
+  if (ctx->precision == D4ORM_PREC_F64) {
+    CU(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyHostToDevice, ctx->s_main));
+    CU(cudaStreamSynchronize(ctx->s_main));
+  } else {
+    std::vector<float> f(n);
+    for (size_t j = 0; j < n; ++j) f[j] = (float)src[j];
+    CU(cudaMemcpyAsync(dst, f.data(), n * sizeof(float), cudaMemcpyHostToDevice, ctx->s_main));
+    CU(cudaStreamSynchronize(ctx->s_main));
+  }
+  return D4ORM_OK;
+}
+
+// Enqueue one denoising step i (z for step i already in z[slot]).  When
+// `next_noise_slot` >= 0, K1 for step `next_noise_step` is forked onto the noise
+// stream into that slot.
+template <typename S>
+int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, int slot, int next_noise_slot, int next_noise_step,
+                 bool timing) {
+  const double ab_i = ctx->ab[i];
+  const double ms = 1.0 / std::sqrt(ab_i), sd = std::sqrt(1.0 / ab_i - 1.0);
+  const double sab = std::sqrt(ctx->ab[i - 1]);
+  const double next_ms = i > 1 ? 1.0 / std::sqrt(ctx->ab[i - 1]) : 0.0;
+  (void)ms;
+  const bool f64 = std::is_same<S, double>::value;
+  const int TC = f64 ? ctx->TC64 : ctx->TC32;
+  const size_t smem = f64 ? ctx->smem64 : ctx->smem32;
+  auto mark = [&](int k) -> int {
+    if (timing) CU(cudaEventRecord(ctx->ev_k[k], ctx->s_main));
+    return D4ORM_OK;
+  };
+  if (next_noise_slot >= 0) {
+    CU(cudaEventRecord(ctx->ev_fork, ctx->s_main));
+    CU(cudaStreamWaitEvent(ctx->s_noise, ctx->ev_fork, 0));
+    if (int r = launch_noise<S>(ctx, ctx->s_noise, next_noise_slot, rs, next_noise_step)) return r;
+    CU(cudaEventRecord(ctx->ev_join, ctx->s_noise));
+  }
+  if (int r = mark(0)) return r;
+  const d4k::FitParams<S> f = fit_params<S>(ctx, (const S*)ctx->z[slot].p, (const S*)ctx->base.p, (const S*)ctx->msv.p,
+                                            sd, rs.Ml, rs.m0, rs.N - i, ctx->rewards.p + rs.m0, nullptr, nullptr,
+                                            nullptr, TC);
+  CU(launch_fit<S>(ctx, f, smem));
+  if (int r = mark(1)) return r;
+  if (ctx->world > 1) {
+    NC(g_nccl.AllGather(ctx->rewards.p + rs.m0, ctx->rewards.p, (size_t)rs.Ml, ncclFloat64, ctx->comm, ctx->s_main));
+  }
+  d4k::WeightParams wp{ctx->rewards.p, rs.M, rs.lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p + 4 * (rs.N - i), i,
+                       nullptr, ctx->errw.p};
+  d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
+  CU(cudaGetLastError());
+  if (int r = mark(2)) return r;
+  const dim3 pgrid((unsigned)((rs.E + 4 * d4k::kThreads - 1) / (4 * d4k::kThreads)), (unsigned)rs.chunks_local);
+  if (f64) {
+    d4k::k_wmean_partial<S, double><<<pgrid, d4k::kThreads, 0, ctx->s_main>>>(
+        (const S*)ctx->z[slot].p, ctx->w64.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, kChunk,
+        (S*)ctx->partial.p);
+  } else {
+    d4k::k_wmean_partial<S, float><<<pgrid, d4k::kThreads, 0, ctx->s_main>>>(
+        (const S*)ctx->z[slot].p, ctx->w32.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, kChunk,
+        (S*)ctx->partial.p);
+  }
+  CU(cudaGetLastError());
+  if (int r = mark(3)) return r;
+  const unsigned tgrid = (unsigned)((rs.E + d4k::kThreads - 1) / d4k::kThreads);
+  if (ctx->world == 1) {
+    d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
+                                                                   sab, next_ms, ctx->var.p, (S*)ctx->msv.p, nullptr);
+  } else {
+    S* my_root = (S*)ctx->roots.p + (size_t)ctx->rank * rs.E;
+    d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
+                                                                   sab, next_ms, ctx->var.p, (S*)ctx->msv.p, my_root);
+    CU(cudaGetLastError());
+    NC(g_nccl.AllGather(my_root, ctx->roots.p, (size_t)rs.E, f64 ? ncclFloat64 : ncclFloat32, ctx->comm, ctx->s_main));
+    d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->roots.p, ctx->world, rs.E, sab,
+                                                                   next_ms, ctx->var.p, (S*)ctx->msv.p, nullptr);
+  }
+  CU(cudaGetLastError());
+  if (int r = mark(4)) return r;
+  if (next_noise_slot >= 0) CU(cudaStreamWaitEvent(ctx->s_main, ctx->ev_join, 0));
+  return D4ORM_OK;
+}
+
+template <typename S>
+__global__ void k_init_var(const double* var, double ms, S* msv, int64_t n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) msv[e] = (S)(ms * var[e]);
+}
+template <typename S>
+__global__ void k_cast(const double* src, S* dst, int64_t n) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < n) dst[e] = (S)src[e];
+}
+
+// Prologue of a run: base, variable init, msv for step N, noise for step N.
+template <typename S>
+int prologue(d4orm_cuda_ctx* ctx, const RunShape& rs, const double* base_host, const d4orm_denoiser_config* c,
+             bool philox) {
+  const int64_t E = rs.E;
+  std::vector<double> b(E, 0.0);
+  if (rs.mode == D4ORM_DEFORMATION) std::memcpy(b.data(), base_host, sizeof(double) * E);
+  CU((upload_as<S>(ctx->base, b.data(), E, ctx->s_main)));
+  if (int r = set_keys(ctx, rs, c->seed)) return r;
+  std::vector<double> v(E, 0.0);
+  if (rs.mode != D4ORM_DEFORMATION) {
+    // FromScratch: variable ~ N(0, I) from stream (seed, 0, 0) (denoiser.cpp:141-145)
+    if (philox) {
+      RunShape one = rs;
+      one.Ml = 1;
+      one.m0 = 0;
+      if (int r = launch_noise<S>(ctx, ctx->s_main, 1, one, 0)) return r;
+      std::vector<S> tmp(E);
+      CU(cudaMemcpyAsync(tmp.data(), ctx->z[1].p, E * sizeof(S), cudaMemcpyDeviceToHost, ctx->s_main));
+      CU(cudaStreamSynchronize(ctx->s_main));
+      for (int64_t e = 0; e < E; ++e) v[e] = (double)tmp[e];
+    } else {
+      if (!ctx->noise_fn) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: host noise selected but no noise fn set");
+      if (ctx->noise_fn(ctx->noise_user, 0, 0, 1, E, v.data()) != 0)
+        return fail(ctx, D4ORM_E_RUNTIME, "d4orm_cuda: noise fn failed at step 0");
+    }
+  }
+  CU(cudaMemcpyAsync(ctx->var.p, v.data(), sizeof(double) * E, cudaMemcpyHostToDevice, ctx->s_main));
+  k_init_var<S><<<(unsigned)((E + 255) / 256), 256, 0, ctx->s_main>>>(ctx->var.p, 1.0 / std::sqrt(ctx->ab[rs.N]),
+                                                                        (S*)ctx->msv.p, E);
+  CU(cudaGetLastError());
+  const unsigned long long init = ~0ull;
+  CU(cudaMemcpyAsync(ctx->errw.p, &init, sizeof init, cudaMemcpyHostToDevice, ctx->s_main));
+  if (philox) {
+    if (int r = launch_noise<S>(ctx, ctx->s_main, 0, rs, rs.N)) return r;
+  }
+  return D4ORM_OK;
+}
+
+// Slot for K1 of the step after i (or of step N after step 1, for chained
+// benchmark passes), or -1 when that slot is still being read by step i.
+int next_noise_slot(const RunShape& rs, int i) {
+  const int slot = (rs.N - i) & 1;
+  if (i > 1) return slot ^ 1;
+  return slot == 1 ? 0 : -1;
+}
+
+std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  char b[512];
+  snprintf(b, sizeof b, "%lld/%d/%.17g/%.17g/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p", (long long)rs.M, rs.N,
+           rs.abf, rs.lambda, ctx->precision, rs.mode, (void*)ctx->z[0].p, (void*)ctx->z[1].p, (void*)ctx->partial.p,
+           (void*)ctx->base.p, (void*)ctx->msv.p, (void*)ctx->var.p, (void*)ctx->rewards.p, (void*)ctx->w64.p,
+           (void*)ctx->w32.p, (void*)ctx->trace.p, (void*)ctx->keys.p, (void*)ctx->errw.p, (void*)ctx->roots.p);
+  return b;
+}
+
+// Per-step CUDA graphs for Philox mode (steady-state structure: z slot of step
+// i is (N-i)&1; K1 of the following step forked inside; step 1 forks K1(N) so
+// runs can be chained for benchmarking).
+template <typename S>
+int ensure_graphs(d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  const std::string key = graph_key_of(ctx, rs);
+  if (key == ctx->graph_key && (int)ctx->graphs.size() == rs.N + 1) return D4ORM_OK;
+  for (auto& g : ctx->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.assign((size_t)rs.N + 1, StepGraph{});
+  for (int i = rs.N; i >= 1; --i) {
+    const int slot = (rs.N - i) & 1;
+    const int next_step = i > 1 ? i - 1 : rs.N;
+    const int next_slot = next_noise_slot(rs, i);
+    cudaGraph_t g;
+    CU(cudaStreamBeginCapture(ctx->s_main, cudaStreamCaptureModeThreadLocal));
+    int r = enqueue_step<S>(ctx, rs, i, slot, next_slot, next_step, false);
+    cudaError_t e = cudaStreamEndCapture(ctx->s_main, &g);
+    if (r) return r;
+    CU(e);
+    CU(cudaGraphInstantiate(&ctx->graphs[i].exec, g, 0));
+    CU(cudaGraphDestroy(g));
+  }
+  ctx->graph_key = key;
+  return D4ORM_OK;
+}
+
+template <typename S>
+int run_steps(d4orm_cuda_ctx* ctx, const RunShape& rs, bool philox, int i_begin, int i_end, const double* given_noise) {
+  for (int i = i_begin; i >= i_end; --i) {
+    const int slot = philox ? (rs.N - i) & 1 : 0;
+    if (!philox) {
+      if (int r = host_noise(ctx, rs, i, rs.m0, rs.Ml, given_noise, ctx->z[0].p)) return r;
+    }
+    if (philox && ctx->use_graphs) {
+      CU(cudaGraphLaunch(ctx->graphs[i].exec, ctx->s_main));
+    } else {
+      const int next_step = i > 1 ? i - 1 : rs.N;
+      const int next_slot = philox ? next_noise_slot(rs, i) : -1;
+      if (int r = enqueue_step<S>(ctx, rs, i, slot, next_slot, next_step, false)) return r;
+    }
+  }
+  return D4ORM_OK;
+}
+
+int check_err(d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  unsigned long long e = 0;
+  CU(cudaMemcpy(&e, ctx->errw.p, sizeof e, cudaMemcpyDeviceToHost));
+  if (e == ~0ull) return D4ORM_OK;
+  if (e == 0xFFFFFFFFFFFFFFFEull) return fail(ctx, D4ORM_E_RUNTIME, "score_weights: non-finite reward");
+  const int step_key = (int)(e >> 52);
+  const long long m = (long long)((e >> 20) & 0xFFFFFFFFull);
+  const int k = (int)((e >> 10) & 1023), t = (int)(e & 1023);
+  return fail(ctx, D4ORM_E_RUNTIME, "run_denoising: sample %lld at step %d: rollout: non-finite state for robot %d at step %d",
+              m, rs.N - step_key, k, t);
+}
+
+template <typename S>
+int run_denoising_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* c, double* out_var,
+                    d4orm_trace_rec* trace) {
+  RunShape rs;
+  if (int r = check_config(ctx, c, &rs)) return r;
+  const bool philox = ctx->noise_source == D4ORM_NOISE_PHILOX;
+  if (int r = ensure_buffers(ctx, rs, philox)) return r;
+  if (int r = prologue<S>(ctx, rs, base, c, philox)) return r;
+  if (philox && ctx->use_graphs) {
+    if (int r = ensure_graphs<S>(ctx, rs)) return r;
+  }
+  if (int r = run_steps<S>(ctx, rs, philox, rs.N, 1, nullptr)) return r;
+  CU(cudaStreamSynchronize(ctx->s_main));
+  if (int r = check_err(ctx, rs)) return r;
+  CU(cudaMemcpy(out_var, ctx->var.p, sizeof(double) * rs.E, cudaMemcpyDeviceToHost));
+  if (trace) {
+    std::vector<double> t((size_t)4 * rs.N);
+    CU(cudaMemcpy(t.data(), ctx->trace.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost));
+    for (int s = 0; s < rs.N; ++s) trace[s] = {(int)t[4 * s], t[4 * s + 1], t[4 * s + 2], t[4 * s + 3]};
+  }
+  return D4ORM_OK;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char* d4orm_cuda_version(void) { return "d4orm-b200 0.1 (sm_100a)"; }
+
+int d4orm_cuda_nccl_id(void* out128) {
+  std::string e;
+  if (!g_nccl.load(&e)) return D4ORM_E_NCCL;
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != 0) return D4ORM_E_NCCL;
+  std::memcpy(out128, &id, sizeof id);
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_create(int device, int rank, int world, const void* nccl_id, d4orm_cuda_ctx** out) {
+  *out = nullptr;
+  d4orm_cuda_ctx* ctx = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return D4ORM_E_CUDA;
+  if (device < 0 || device >= ndev || world < 1 || rank < 0 || rank >= world) return D4ORM_E_INVALID;
+  std::unique_ptr<d4orm_cuda_ctx> c(new d4orm_cuda_ctx);
+  ctx = c.get();
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  CU(cudaSetDevice(device));
+  CU(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&c->s_noise, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  CU(cudaEventCreate(&c->ev_t0));
+  CU(cudaEventCreate(&c->ev_t1));
+  c->ev_k.resize(5);
+  for (auto& e : c->ev_k) CU(cudaEventCreate(&e));
+  if (world > 1) {
+    std::string e;
+    if (!g_nccl.load(&e) || !nccl_id) {
+      c.release();
+      return D4ORM_E_NCCL;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    if (g_nccl.CommInitRank(&c->comm, world, id, rank) != 0) {
+      c.release();
+      return D4ORM_E_NCCL;
+    }
+  }
+  *out = c.release();
+  return D4ORM_OK;
+}
+
+void d4orm_cuda_destroy(d4orm_cuda_ctx* ctx) { delete ctx; }
+
+const char* d4orm_cuda_last_error(const d4orm_cuda_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int d4orm_cuda_set_options(d4orm_cuda_ctx* ctx, int precision, int noise_source, int use_graphs) {
+  if (precision != D4ORM_PREC_F32 && precision != D4ORM_PREC_F64) return fail(ctx, D4ORM_E_INVALID, "bad precision");
+  if (noise_source != D4ORM_NOISE_PHILOX && noise_source != D4ORM_NOISE_HOST)
+    return fail(ctx, D4ORM_E_INVALID, "bad noise source");
+  const bool changed = precision != ctx->precision;
+  ctx->precision = precision;
+  ctx->noise_source = noise_source;
+  ctx->use_graphs = use_graphs;
+  ctx->graph_key.clear();
+  if (changed && ctx->has_problem) {
+    cudaSetDevice(ctx->device);
+    return precision == D4ORM_PREC_F64 ? upload_problem<double>(ctx) : upload_problem<float>(ctx);
+  }
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_set_noise_fn(d4orm_cuda_ctx* ctx, d4orm_noise_fn fn, void* user) {
+  ctx->noise_fn = fn;
+  ctx->noise_user = user;
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* p) {
+  int dx, du, pd;
+  if (!dims_of(p->kind, &dx, &du, &pd)) return fail(ctx, D4ORM_E_INVALID, "unknown model kind: %d", p->kind);
+  if (p->dx != dx || p->du != du || p->pdim != pd)
+    return fail(ctx, D4ORM_E_INVALID, "d4orm_problem: dims (%d,%d,%d) do not match model kind %d", p->dx, p->du,
+                p->pdim, p->kind);
+  if (p->robots < 1 || p->horizon < 1) return fail(ctx, D4ORM_E_INVALID, "rollout: empty control trajectory");
+  if (p->robots > 256) return fail(ctx, D4ORM_E_UNSUPPORTED, "d4orm_cuda: at most 256 robots");
+  if (p->horizon > 1023) return fail(ctx, D4ORM_E_UNSUPPORTED, "d4orm_cuda: horizon at most 1023");
+  if (!(p->dt > 0.0)) return fail(ctx, D4ORM_E_INVALID, "rollout: dt must be positive");
+  for (int j = 0; j < dx * p->robots; ++j)
+    if (!std::isfinite(p->starts[j])) return fail(ctx, D4ORM_E_INVALID, "rollout: non-finite start state");
+  for (int k = 0; k < p->robots; ++k) {
+    double s = 0.0;
+    for (int j = 0; j < pd; ++j) {
+      const double d = p->starts[k * dx + j] - p->goals[k * pd + j];
+      s += d * d;
+    }
+    if (!(std::sqrt(s) > 0.0))
+      return fail(ctx, D4ORM_E_INVALID, "total_reward: robot %d starts on its goal (degenerate scenario)", k);
+  }
+  ctx->prob = *p;
+  ctx->starts.assign(p->starts, p->starts + (size_t)dx * p->robots);
+  ctx->goals.assign(p->goals, p->goals + (size_t)pd * p->robots);
+  ctx->obs_c.assign(p->obs_centers, p->obs_centers + (size_t)pd * p->n_obstacles);
+  ctx->obs_r.assign(p->obs_radii, p->obs_radii + p->n_obstacles);
+  ctx->prob.starts = ctx->starts.data();
+  ctx->prob.goals = ctx->goals.data();
+  ctx->prob.obs_centers = ctx->obs_c.data();
+  ctx->prob.obs_radii = ctx->obs_r.data();
+  const int R = p->robots;
+  ctx->TB = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
+  ctx->Rp = (R + ctx->TB - 1) / ctx->TB * ctx->TB;
+  ctx->MAXW = ctx->Rp <= 64 ? 2 : 8;
+  ctx->spc = d4k::kThreads / ctx->Rp;
+  if (int r = choose_tc<float>(ctx, &ctx->TC32, &ctx->smem32)) return r;
+  if (int r = choose_tc<double>(ctx, &ctx->TC64, &ctx->smem64)) return r;
+  ctx->has_problem = true;
+  ctx->graph_key.clear();
+  CU(cudaSetDevice(ctx->device));
+  return ctx->precision == D4ORM_PREC_F64 ? upload_problem<double>(ctx) : upload_problem<float>(ctx);
+}
+
+int d4orm_cuda_run_denoising(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* config,
+                             double* out_variable, d4orm_trace_rec* trace) {
+  CU(cudaSetDevice(ctx->device));
+  return ctx->precision == D4ORM_PREC_F64 ? run_denoising_t<double>(ctx, base, config, out_variable, trace)
+                                          : run_denoising_t<float>(ctx, base, config, out_variable, trace);
+}
+
+extern "C++" template <typename S>
+int denoise_step_t(d4orm_cuda_ctx* ctx, const double* base, const double* var_in, const double* noise, int i,
+                          const d4orm_denoiser_config* c, double* var_out, double* rewards, double* weights,
+                          d4orm_trace_rec* rec) {
+  RunShape rs;
+  if (int r = check_config(ctx, c, &rs)) return r;
+  if (i < 1 || i > rs.N)
+    return fail(ctx, D4ORM_E_INVALID, "denoise_step: step index %d outside 1..%d", i, rs.N);
+  if (int r = ensure_buffers(ctx, rs, false)) return r;
+  const int64_t E = rs.E;
+  std::vector<double> b(E, 0.0);
+  if (rs.mode == D4ORM_DEFORMATION) std::memcpy(b.data(), base, sizeof(double) * E);
+  CU((upload_as<S>(ctx->base, b.data(), E, ctx->s_main)));
+  CU(cudaMemcpyAsync(ctx->var.p, var_in, sizeof(double) * E, cudaMemcpyHostToDevice, ctx->s_main));
+  k_init_var<S><<<(unsigned)((E + 255) / 256), 256, 0, ctx->s_main>>>(ctx->var.p, 1.0 / std::sqrt(ctx->ab[i]),
+                                                                        (S*)ctx->msv.p, E);
+  CU(cudaGetLastError());
+  const unsigned long long init = ~0ull;
+  CU(cudaMemcpyAsync(ctx->errw.p, &init, sizeof init, cudaMemcpyHostToDevice, ctx->s_main));
+  if (int r = set_keys(ctx, rs, c->seed)) return r;
+  if (noise) {
+    if (int r = host_noise(ctx, rs, i, rs.m0, rs.Ml, noise + (size_t)rs.m0 * E, ctx->z[0].p)) return r;
+  } else {
+    if (int r = launch_noise<S>(ctx, ctx->s_main, 0, rs, i)) return r;
+  }
+  if (int r = enqueue_step<S>(ctx, rs, i, 0, -1, 0, false)) return r;
+  CU(cudaStreamSynchronize(ctx->s_main));
+  if (int r = check_err(ctx, rs)) return r;
+  if (var_out) CU(cudaMemcpy(var_out, ctx->var.p, sizeof(double) * E, cudaMemcpyDeviceToHost));
+  if (rewards) CU(cudaMemcpy(rewards, ctx->rewards.p, sizeof(double) * rs.M, cudaMemcpyDeviceToHost));
+  if (weights) CU(cudaMemcpy(weights, ctx->w64.p, sizeof(double) * rs.M, cudaMemcpyDeviceToHost));
+  if (rec) {
+    double t[4];
+    CU(cudaMemcpy(t, ctx->trace.p + 4 * (rs.N - i), sizeof t, cudaMemcpyDeviceToHost));
+    *rec = {(int)t[0], t[1], t[2], t[3]};
+  }
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_denoise_step(d4orm_cuda_ctx* ctx, const double* base, const double* variable_in, const double* noise,
+                            int i, const d4orm_denoiser_config* config, double* variable_out, double* rewards,
+                            double* weights, d4orm_trace_rec* rec) {
+  CU(cudaSetDevice(ctx->device));
+  return ctx->precision == D4ORM_PREC_F64
+             ? denoise_step_t<double>(ctx, base, variable_in, noise, i, config, variable_out, rewards, weights, rec)
+             : denoise_step_t<float>(ctx, base, variable_in, noise, i, config, variable_out, rewards, weights, rec);
+}
+
+extern "C++" template <typename S>
+int rollout_fitness_t(d4orm_cuda_ctx* ctx, const double* u, int64_t count, double* states, double* controls,
+                             double* rewards, int64_t* counts) {
+  if (!ctx->has_problem) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: set_problem not called");
+  if (count < 1) return D4ORM_OK;
+  const d4orm_problem& p = ctx->prob;
+  const int64_t E = elems_of(ctx);
+  const int64_t NS = (int64_t)(p.horizon + 1) * p.robots * p.dx, NC = (int64_t)(p.horizon + 1) * p.robots * p.du;
+  CU(ctx->z[0].ensure((size_t)count * E * sizeof(S)));
+  CU(ctx->base.ensure((size_t)E * sizeof(S)));
+  CU(ctx->msv.ensure((size_t)E * sizeof(S)));
+  CU(ctx->rewards.ensure((size_t)count));
+  CU(ctx->counts.ensure((size_t)count * 2));
+  CU(ctx->errw.ensure(1));
+  CU(ctx->states_out.ensure((size_t)count * NS * sizeof(S)));
+  CU(ctx->controls_out.ensure((size_t)count * NC * sizeof(S)));
+  CU(cudaMemsetAsync(ctx->base.p, 0, E * sizeof(S), ctx->s_main));
+  CU(cudaMemsetAsync(ctx->msv.p, 0, E * sizeof(S), ctx->s_main));
+  CU(cudaMemsetAsync(ctx->controls_out.p, 0, count * NC * sizeof(S), ctx->s_main));
+  const unsigned long long init = ~0ull;
+  CU(cudaMemcpyAsync(ctx->errw.p, &init, sizeof init, cudaMemcpyHostToDevice, ctx->s_main));
+  CU((upload_as<S>(ctx->z[0], u, (size_t)count * E, ctx->s_main)));
+  const bool f64 = std::is_same<S, double>::value;
+  // candidate = base(0) + (msv(0) + 1*u) = u exactly
+  const d4k::FitParams<S> f = fit_params<S>(ctx, (const S*)ctx->z[0].p, (const S*)ctx->base.p, (const S*)ctx->msv.p,
+                                            1.0, count, 0, 0, ctx->rewards.p, ctx->counts.p, (S*)ctx->states_out.p,
+                                            (S*)ctx->controls_out.p, f64 ? ctx->TC64 : ctx->TC32);
+  CU(launch_fit<S>(ctx, f, f64 ? ctx->smem64 : ctx->smem32));
+  CU(cudaStreamSynchronize(ctx->s_main));
+  unsigned long long e = 0;
+  CU(cudaMemcpy(&e, ctx->errw.p, sizeof e, cudaMemcpyDeviceToHost));
+  if (e != ~0ull) {
+    const long long m = (long long)((e >> 20) & 0xFFFFFFFFull);
+    return fail(ctx, D4ORM_E_RUNTIME, "batch_rollout: member %lld: rollout: non-finite state for robot %d at step %d", m,
+                (int)((e >> 10) & 1023), (int)(e & 1023));
+  }
+  if (rewards) CU(cudaMemcpy(rewards, ctx->rewards.p, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  if (counts) {
+    std::vector<int> c2((size_t)count * 2);
+    CU(cudaMemcpy(c2.data(), ctx->counts.p, sizeof(int) * c2.size(), cudaMemcpyDeviceToHost));
+    for (size_t j = 0; j < c2.size(); ++j) counts[j] = c2[j];
+  }
+  if (states || controls) {
+    std::vector<S> tmp((size_t)count * (NS > NC ? NS : NC));
+    if (states) {
+      CU(cudaMemcpy(tmp.data(), ctx->states_out.p, sizeof(S) * count * NS, cudaMemcpyDeviceToHost));
+      for (int64_t j = 0; j < count * NS; ++j) states[j] = (double)tmp[j];
+    }
+    if (controls) {
+      CU(cudaMemcpy(tmp.data(), ctx->controls_out.p, sizeof(S) * count * NC, cudaMemcpyDeviceToHost));
+      for (int64_t j = 0; j < count * NC; ++j) controls[j] = (double)tmp[j];
+    }
+  }
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_rollout_fitness(d4orm_cuda_ctx* ctx, const double* u, int64_t count, double* states, double* controls,
+                               double* rewards, int64_t* counts) {
+  CU(cudaSetDevice(ctx->device));
+  return ctx->precision == D4ORM_PREC_F64 ? rollout_fitness_t<double>(ctx, u, count, states, controls, rewards, counts)
+                                          : rollout_fitness_t<float>(ctx, u, count, states, controls, rewards, counts);
+}
+
+int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t m, double lambda, double* weights,
+                             double* trace3) {
+  CU(cudaSetDevice(ctx->device));
+  if (m < 2) return fail(ctx, D4ORM_E_INVALID, "score_weights: need at least 2 rewards");
+  if (!(lambda > 0.0)) return fail(ctx, D4ORM_E_INVALID, "score_weights: lambda must be positive");
+  for (int64_t j = 0; j < m; ++j)
+    if (!std::isfinite(rewards[j]))
+      return fail(ctx, D4ORM_E_RUNTIME, "score_weights: non-finite reward for sample %lld", (long long)j);
+  CU(ctx->rewards.ensure((size_t)m));
+  CU(ctx->w64.ensure((size_t)m));
+  CU(ctx->w32.ensure((size_t)m));
+  CU(ctx->trace.ensure(4));
+  CU(ctx->errw.ensure(1));
+  CU(cudaMemcpyAsync(ctx->rewards.p, rewards, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->s_main));
+  d4k::WeightParams wp{ctx->rewards.p, m, lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p, 0, nullptr, ctx->errw.p};
+  d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(ctx->s_main));
+  CU(cudaMemcpy(weights, ctx->w64.p, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  if (trace3) {
+    double t[4];
+    CU(cudaMemcpy(t, ctx->trace.p, sizeof t, cudaMemcpyDeviceToHost));
+    trace3[0] = t[1];
+    trace3[1] = t[2];
+    trace3[2] = t[3];
+  }
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_t m0, int64_t count, float* out) {
+  CU(cudaSetDevice(ctx->device));
+  if (!ctx->has_problem) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: set_problem not called");
+  RunShape rs;
+  rs.E = elems_of(ctx);
+  rs.Ml = count;
+  rs.m0 = m0;
+  rs.N = step;
+  CU(ctx->z[0].ensure((size_t)count * rs.E * sizeof(float)));
+  CU(ctx->keys.ensure((size_t)step + 1));
+  if (int r = set_keys(ctx, rs, seed)) return r;
+  if (int r = launch_noise<float>(ctx, ctx->s_main, 0, rs, step)) return r;
+  CU(cudaStreamSynchronize(ctx->s_main));
+  CU(cudaMemcpy(out, ctx->z[0].p, sizeof(float) * count * rs.E, cudaMemcpyDeviceToHost));
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_launches_per_step(const d4orm_cuda_ctx* ctx) { return ctx->world > 1 ? 6 : 5; }
+
+extern "C++" template <typename S>
+int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* c, int warmup, int steps,
+                   double* ms_total, double* kernel_ms) {
+  RunShape rs;
+  if (int r = check_config(ctx, c, &rs)) return r;
+  if (ctx->noise_source != D4ORM_NOISE_PHILOX) return fail(ctx, D4ORM_E_INVALID, "bench requires Philox noise");
+  if (int r = ensure_buffers(ctx, rs, true)) return r;
+  if (int r = prologue<S>(ctx, rs, base, c, true)) return r;
+  if (ctx->use_graphs) {
+    if (int r = ensure_graphs<S>(ctx, rs)) return r;
+  }
+  // step j → denoising index i = N - (j mod N): a chain of full passes
+  auto run_range = [&](int j0, int count) -> int {
+    for (int j = j0; j < j0 + count; ++j) {
+      const int i = rs.N - (j % rs.N);
+      if (i == rs.N && j > 0 && next_noise_slot(rs, 1) < 0) {
+        if (int r = launch_noise<S>(ctx, ctx->s_main, 0, rs, rs.N)) return r;
+      }
+      if (int r = run_steps<S>(ctx, rs, true, i, i, nullptr)) return r;
+    }
+    return D4ORM_OK;
+  };
+  if (int r = run_range(0, warmup)) return r;
+  CU(cudaStreamSynchronize(ctx->s_main));
+  CU(cudaEventRecord(ctx->ev_t0, ctx->s_main));
+  if (int r = run_range(warmup, steps)) return r;
+  CU(cudaEventRecord(ctx->ev_t1, ctx->s_main));
+  CU(cudaEventSynchronize(ctx->ev_t1));
+  float ms = 0.f;
+  CU(cudaEventElapsedTime(&ms, ctx->ev_t0, ctx->ev_t1));
+  *ms_total = ms;
+  if (int r = check_err(ctx, rs)) return r;
+  if (kernel_ms) {
+    // Instrumented pass (eager launches with events between kernels, K1 on
+    // the main stream so its time is attributable).
+    double acc[5] = {0, 0, 0, 0, 0};
+    cudaEvent_t e0;
+    CU(cudaEventCreate(&e0));
+    const int reps = steps < 1 ? 1 : steps;
+    for (int j = 0; j < reps; ++j) {
+      const int i = rs.N - ((warmup + steps + j) % rs.N);
+      const int slot = (rs.N - i) & 1;
+      CU(cudaEventRecord(e0, ctx->s_main));
+      if (int r = launch_noise<S>(ctx, ctx->s_main, slot ^ 1, rs, i > 1 ? i - 1 : rs.N)) return r;
+      if (int r = enqueue_step<S>(ctx, rs, i, slot, -1, 0, true)) return r;
+      CU(cudaEventSynchronize(ctx->ev_k[4]));
+      float t[5];
+      CU(cudaEventElapsedTime(&t[0], e0, ctx->ev_k[0]));
+      CU(cudaEventElapsedTime(&t[1], ctx->ev_k[0], ctx->ev_k[1]));
+      CU(cudaEventElapsedTime(&t[2], ctx->ev_k[1], ctx->ev_k[2]));
+      CU(cudaEventElapsedTime(&t[3], ctx->ev_k[2], ctx->ev_k[3]));
+      CU(cudaEventElapsedTime(&t[4], ctx->ev_k[3], ctx->ev_k[4]));
+      for (int k = 0; k < 5; ++k) acc[k] += t[k];
+    }
+    cudaEventDestroy(e0);
+    for (int k = 0; k < 5; ++k) kernel_ms[k] = acc[k] / reps;
+  }
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_bench_steps(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* config, int warmup,
+                           int steps, double* ms_total, double* kernel_ms) {
+  CU(cudaSetDevice(ctx->device));
+  return ctx->precision == D4ORM_PREC_F64 ? bench_t<double>(ctx, base, config, warmup, steps, ms_total, kernel_ms)
+                                          : bench_t<float>(ctx, base, config, warmup, steps, ms_total, kernel_ms);
+}
+
+}  // extern "C"

@@ -1,0 +1,241 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle on
+identical inputs and identical noise.
+
+Tolerances (written here):
+  * fp64 parity mode: states rel 1e-12 (holonomic kinds are exact sums;
+    sin/cos kinds differ from glibc by ulps), rewards abs 1e-12, collision /
+    obstacle counts exact, weights rel 1e-9, variable rel 1e-9.
+  * fp32 throughput mode: states abs 2e-5 m, rewards abs 2e-5 (+ one
+    w_t/(R·T) per explained decision flip), weights compared as log-weights
+    where w > 1e-6, variable rel 1e-4 of its scale.
+"""
+import numpy as np
+import pytest
+
+import paper_2503_12204_b200 as d4
+from paper_2503_12204_b200 import scenarios as S
+from oracle.oracle import make_config
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "holo2d": lambda: S.antipodal_circle(6, 4.0, S.HOLO2D, horizon=24),
+    "diffdrive": lambda: S.antipodal_circle(5, 4.0, S.DIFFDRIVE, horizon=24),
+    "holo3d": lambda: S.antipodal_sphere(7, 4.0, horizon=24),
+    "C1": lambda: S.baseline_config(1).problem,
+    "C2": lambda: S.baseline_config(2).problem.with_horizon(40),
+    "C3": lambda: S.baseline_config(3).problem.with_horizon(40),
+    "C4": lambda: S.baseline_config(4).problem.with_horizon(40),
+    "C5": lambda: S.baseline_config(5).problem.with_horizon(24),
+    "R40": lambda: S.random_square(40, 8.0, 3, S.HOLO2D_VEL, robot_radius=0.15, horizon=16, lower=[-1, -1], upper=[1, 1]),
+}
+
+
+def controls_for(p, count, seed, scale=1.5):
+    rng = np.random.default_rng(seed)
+    # biased toward the goals so robots meet (collisions happen) + noise
+    d = (p.goals - p.starts[:, : p.pdim])
+    drift = np.zeros((p.robots, p.du))
+    if p.kind in (S.HOLO2D_VEL, S.HOLO3D_VEL):
+        drift = d / (p.horizon * p.dt)
+    return drift[None, None] + scale * rng.normal(size=(count, p.horizon, p.robots, p.du))
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    g = d4.GpuDenoiser()
+    yield g
+    g.close()
+
+
+def oracle_rollout_batch(oracle, p, u):
+    out = []
+    for m in range(u.shape[0]):
+        st, ct = oracle.rollout(p, u[m])
+        r, nc, no = oracle.total_reward(p, st)
+        out.append((st, ct, r, nc, no))
+    return out
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_rollout_fitness_f64_matches_oracle(gpu, oracle, case):
+    p = CASES[case]()
+    gpu.set_options(d4.PREC_F64, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    u = controls_for(p, 24, 1)
+    st, ct, rw, cnt = gpu.rollout_fitness(u)
+    ref = oracle_rollout_batch(oracle, p, u)
+    for m, (rs, rc, rr, nc, no) in enumerate(ref):
+        if p.kind in (S.DIFFDRIVE, S.UNICYCLE):
+            np.testing.assert_allclose(st[m], rs, rtol=1e-12, atol=1e-12)
+        else:
+            np.testing.assert_array_equal(st[m], rs)
+        np.testing.assert_array_equal(ct[m], rc)
+        assert abs(rw[m] - rr) <= 1e-12, (m, rw[m], rr)
+        assert (cnt[m, 0], cnt[m, 1]) == (nc, no), (m, cnt[m], nc, no)
+
+
+def explain_flips(oracle, p, st_gpu, nc_gpu, no_gpu):
+    """Recount conflicts on the GPU's own (fp32) positions with the fp64 rule:
+    a count difference vs the oracle is 'explained' when it disappears."""
+    r, nc, no = oracle.total_reward(p, st_gpu)
+    return nc == nc_gpu and no == no_gpu
+
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_rollout_fitness_f32_matches_oracle(gpu, oracle, case):
+    p = CASES[case]()
+    gpu.set_options(d4.PREC_F32, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    u = controls_for(p, 24, 2)
+    st, ct, rw, cnt = gpu.rollout_fitness(u)
+    ref = oracle_rollout_batch(oracle, p, u)
+    unit = max(p.w_t, p.obstacle_weight) / (p.robots * p.horizon)
+    for m, (rs, rc, rr, nc, no) in enumerate(ref):
+        np.testing.assert_allclose(st[m], rs, atol=2e-5, rtol=1e-5)
+        np.testing.assert_allclose(ct[m], rc, atol=1e-6, rtol=1e-6)
+        flips = abs(cnt[m, 0] - nc) + abs(cnt[m, 1] - no)
+        if flips:
+            assert explain_flips(oracle, p, st[m], cnt[m, 0], cnt[m, 1]), (m, cnt[m], nc, no)
+        assert abs(rw[m] - rr) <= 2e-5 + flips * unit, (m, rw[m], rr, flips)
+
+
+def test_collisions_are_counted(gpu, oracle):
+    """Robots parked in conflict, and exactly on the (2R_a+eps) boundary: the
+    reference's `<=` counts it."""
+    p = S.Problem(S.HOLO2D_VEL, starts=[[0, 0], [0.25, 0], [3, 3]], goals=[[1, 1], [2, 2], [-3, -3]],
+                  horizon=4, lower=[-1, -1], upper=[1, 1], robot_radius=0.1, epsilon=0.05)
+    u = np.zeros((1, 4, 3, 2))
+    for prec in (d4.PREC_F64, d4.PREC_F32):
+        gpu.set_options(prec, d4.NOISE_HOST)
+        gpu.set_problem(p)
+        st, ct, rw, cnt = gpu.rollout_fitness(u)
+        r, nc, no = oracle.total_reward(p, st[0].astype(np.float64))
+        assert nc == 8 and cnt[0, 0] == 8, (prec, cnt, nc)
+        assert abs(rw[0] - r) < 1e-6
+
+
+@pytest.mark.parametrize("m", [2, 3, 1000, 8192, 70001])
+def test_score_weights(gpu, oracle, m):
+    rng = np.random.default_rng(m)
+    r = rng.normal(size=m) * 0.01 + 0.3
+    w, t3 = gpu.score_weights(r, 0.1)
+    wo = oracle.score_weights(r, 0.1)
+    np.testing.assert_allclose(w, wo, rtol=1e-9, atol=1e-300)
+    assert abs(t3[2] - oracle.weight_entropy(wo)) < 1e-9 * max(1, abs(t3[2]))
+    assert t3[0] == r.max() and abs(t3[1] - r.mean()) < 1e-12
+
+
+def test_score_weights_degenerate_and_errors(gpu):
+    w, _ = gpu.score_weights(np.full(10, 0.5), 0.1)
+    np.testing.assert_array_equal(w, np.full(10, 0.1))
+    with pytest.raises(ValueError):
+        gpu.score_weights(np.ones(1), 0.1)
+    with pytest.raises(ValueError):
+        gpu.score_weights(np.ones(4), 0.0)
+    with pytest.raises(d4.D4ormError, match="non-finite reward for sample 2"):
+        gpu.score_weights(np.array([0.1, 0.2, np.nan, 0.3]), 0.1)
+
+
+@pytest.mark.parametrize("case", ["holo2d", "C2", "C3", "C4", "R40"])
+@pytest.mark.parametrize("prec", [d4.PREC_F64, d4.PREC_F32])
+def test_denoise_step_teacher_forced(gpu, oracle, case, prec):
+    p = CASES[case]()
+    M, N, i = 512, 10, 7
+    cfg = d4.DenoiserConfig(steps=N, batch=M, seed=11)
+    ocfg = make_config(N, M, seed=11)
+    ab, _ = oracle.make_schedule(N, 0.05)
+    rng = np.random.default_rng(5)
+    base = controls_for(p, 1, 3, scale=0.3)[0]
+    var = 0.2 * rng.normal(size=base.shape)
+    noise = oracle.step_noise(11, i, 0, M, p.elems)
+    gpu.set_options(prec, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    v_g, r_g, w_g, rec_g = gpu.denoise_step(base, var, i, cfg, noise)
+    v_o, r_o, w_o, rec_o = oracle.denoise_step(p, base, var, ab, ocfg, i, noise)
+    if prec == d4.PREC_F64:
+        np.testing.assert_allclose(r_g, r_o, atol=1e-12)
+        np.testing.assert_allclose(w_g, w_o, rtol=1e-8, atol=1e-300)
+        np.testing.assert_allclose(v_g, v_o, rtol=1e-9, atol=1e-12)
+    else:
+        unit = max(p.w_t, p.obstacle_weight) / (p.robots * p.horizon)
+        dr = np.abs(r_g - r_o)
+        assert (dr <= 2e-5 + 4 * unit).all(), dr.max()
+        assert (dr <= 2e-5).mean() > 0.95
+        scale = np.abs(v_o).max()
+        # weights are sharp (λ=0.1 on z-scores); compare the averaged variable
+        np.testing.assert_allclose(v_g, v_o, atol=2e-3 * scale)
+    assert rec_g[0] == i
+
+
+@pytest.mark.parametrize("case", ["holo2d", "C1", "C3"])
+def test_run_denoising_host_noise_f64(gpu, oracle, case):
+    """Free-running N steps with the oracle's own NormalStream noise: fp64 GPU
+    path tracks the reference within 1e-9 relative."""
+    p = CASES[case]()
+    M, N = 256, 8
+    for mode in (d4.DEFORMATION, d4.FROM_SCRATCH):
+        cfg = d4.DenoiserConfig(steps=N, batch=M, seed=4, mode=mode)
+        base = controls_for(p, 1, 4, scale=0.3)[0]
+        gpu.set_options(d4.PREC_F64, d4.NOISE_HOST)
+        gpu.set_problem(p)
+        gpu.set_noise_provider(lambda step, m0, count, elems: (
+            oracle.normal_fill(oracle.mix_seed(4, 0, 0), elems)[None] if step == 0 else
+            oracle.step_noise(4, step, m0, count, elems)))
+        v_g, tr_g = gpu.run_denoising(base, cfg)
+        v_o, tr_o = oracle.run_denoising(p, base, make_config(N, M, seed=4, mode=mode))
+        np.testing.assert_allclose(v_g, v_o, rtol=1e-9, atol=1e-12)
+        for a, b in zip(tr_g, tr_o):
+            assert a[0] == b[0]
+            np.testing.assert_allclose(a[1:], b[1:], rtol=1e-9, atol=1e-12)
+
+
+def test_run_denoising_philox_deterministic(gpu):
+    p = CASES["C2"]()
+    cfg = d4.DenoiserConfig(steps=6, batch=1024, seed=9)
+    base = np.zeros((p.horizon, p.robots, p.du))
+    gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX, graphs=True)
+    gpu.set_problem(p)
+    v1, t1 = gpu.run_denoising(base, cfg)
+    v2, t2 = gpu.run_denoising(base, cfg)
+    gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX, graphs=False)
+    v3, t3 = gpu.run_denoising(base, cfg)
+    np.testing.assert_array_equal(v1, v2)
+    np.testing.assert_array_equal(v1, v3)
+    assert t1 == t2 == t3
+    assert np.abs(v1).max() > 0
+
+
+def test_philox_noise_is_standard_normal_and_shard_invariant(gpu):
+    p = CASES["C2"]()
+    gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX)
+    gpu.set_problem(p)
+    z = gpu.philox_noise(123, 50, 0, 64)
+    assert abs(z.mean()) < 0.01 and abs(z.std() - 1) < 0.01
+    z2 = gpu.philox_noise(123, 50, 32, 32)
+    np.testing.assert_array_equal(z[32:], z2)
+    z3 = gpu.philox_noise(123, 49, 0, 64)
+    assert not np.array_equal(z, z3)
+
+
+def test_nonfinite_state_error_message(gpu):
+    p = S.Problem(S.HOLO2D_VEL, starts=[[0, 0], [1, 1]], goals=[[1, 0], [0, 1]], horizon=5,
+                  lower=[-np.inf, -np.inf], upper=[np.inf, np.inf])
+    u = np.zeros((2, 5, 2, 2))
+    u[1, 2, 1, 0] = np.inf
+    gpu.set_options(d4.PREC_F32, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    with pytest.raises(d4.D4ormError, match="member 1: rollout: non-finite state for robot 1 at step 3"):
+        gpu.rollout_fitness(u)
+
+
+def test_invalid_arguments(gpu):
+    p = CASES["holo2d"]()
+    gpu.set_problem(p)
+    with pytest.raises(ValueError, match="batch must be >= 2"):
+        gpu.run_denoising(np.zeros((p.horizon, p.robots, p.du)), d4.DenoiserConfig(steps=2, batch=1))
+    with pytest.raises(ValueError, match="lambda must be > 0"):
+        gpu.run_denoising(np.zeros((p.horizon, p.robots, p.du)), d4.DenoiserConfig(steps=2, batch=4, lam=0))
+    bad = S.Problem(S.HOLO2D, starts=[[0, 0, 0, 0]], goals=[[0, 0]], horizon=3)
+    with pytest.raises(ValueError, match="starts on its goal"):
+        gpu.set_problem(bad)
