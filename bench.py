@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""bench.py — the denoise-step hot path on B200, one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5] [--impl ours|reference]
+
+A "step" is one denoising step (denoiser.cpp:152-180) over the whole batch of
+samples: Philox noise, rollout+fitness of every sample, softmax weights, the
+weighted mean and the update.  Default workload: BASELINE config C5 (2D
+velocity-input holonomic, R=64, T=256, N=262144 samples/step, 16 obstacles),
+the configuration the FP32-roofline target and the 1/2/4/8-GPU scaling are
+quoted on; --config selects another BASELINE shape.  Samples are sharded
+across ranks (one process per GPU, torchrun); total work is fixed → "strong".
+
+value    rollouts+fitness evaluations/s with inputs resident in HBM (device
+         CUDA-event timing of exactly K steps, max over ranks)
+e2e      the same metric through the public C-ABI call d4orm_cuda_run_denoising
+         with host buffers (H2D base, D2H variable+trace inside the region)
+roofline dominant kernel K2+K3 (rollout+fitness), FP32-bound: algorithmic
+         FLOPs per launch / its CUDA-event launch time, against the
+         FP32 peak measured live on this GPU (d4orm_cuda_fp32_peak)
+--impl reference  the reference's own CPU implementation (oracle/_ref: proj/src
+         compiled unchanged) on all host cores, bounded sample per step
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "joint-trajectory rollouts+fitness evals/sec"
+UNIT = "evals/s"
+
+
+def algorithmic_flops_per_eval(p) -> float:
+    """F = T·[R·(f_dyn + 3·du + 3p + 3) + 3p·R(R−1)/2 + 3p·R·O]."""
+    R, T, du, pd, O = p.robots, p.horizon, p.du, p.pdim, len(p.obs_radii)
+    f_dyn = {0: 40, 1: 2 * 4, 2: 2 * 6, 3: 2 * du, 4: 2 * du, 5: 40}[p.kind]
+    return T * (R * (f_dyn + 3 * du + 3 * pd + 3) + 3 * pd * R * (R - 1) / 2 + 3 * pd * R * O)
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clocks / throttle reasons sampled during the timed region (NVML)."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x10: "sync_boost"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz, self.ok = [], set(), None, False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # reported, never fatal
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "note": "NVML unavailable"}
+        load = [s for s in self.samples if s > 0.5 * (self.max_mhz or 1)] or self.samples
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_setup(world: int):
+    """Control plane only (barrier, 128-byte NCCL id broadcast, max-over-ranks):
+    gloo over 127.0.0.1.  The per-step data exchange is NCCL inside the library."""
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group("gloo", rank=int(os.environ["RANK"]), world_size=world)
+    return dist
+
+
+def reduce_max(dist, v: float) -> float:
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_reference_step(ref, p, batch: int, seed: int, workers: int = 0) -> float:
+    """One denoising step of the reference's own run_denoising (steps=1) over
+    `batch` samples on all host cores; returns seconds."""
+    from oracle.oracle import make_config
+    base = np.zeros((p.horizon, p.robots, p.du))
+    t0 = time.perf_counter()
+    ref.run_denoising(p, base, make_config(1, batch, seed=seed, workers=workers))
+    return time.perf_counter() - t0
+
+
+def reference_checker():
+    from oracle.oracle import REF_SO, ORACLE_SO, Oracle, Reference
+    if REF_SO.exists():
+        return Reference(), "reference", "oracle/_ref: reference proj/src compiled unchanged"
+    if not ORACLE_SO.exists():
+        import subprocess
+        subprocess.run(["make", "-s", "-f", str(ROOT / "oracle" / "Makefile")], check=True)
+    return Oracle(), "port", "oracle/d4orm_oracle.c (plain-C restatement, pinned bitwise to the reference)"
+
+
+def size_cpu_sample(ref, p, M: int, budget_s: float) -> tuple[int, float]:
+    """Largest power-of-two sample ≤ M whose reference step takes ≈budget_s."""
+    b = min(M, 256)
+    t = cpu_reference_step(ref, p, b, 1)
+    while b < M and t * 2 <= budget_s:
+        b = min(M, b * 2)
+        t = cpu_reference_step(ref, p, b, 1)
+    return b, t
+
+
+def config_json(rc, world: int) -> dict:
+    p = rc.problem
+    return {"workload": rc.name, "model": p.name, "robots": p.robots, "horizon": p.horizon, "samples_per_step": rc.samples,
+            "denoising_steps": rc.steps, "iterations": rc.iterations, "obstacles": int(len(p.obs_radii)),
+            "global_batch": rc.samples, "seq_len": p.horizon, "parallelism": f"samples-sharded x{world}",
+            "l2": "inputs larger than L2 (per-step noise buffer > 126 MB)"}
+
+
+def run_reference_arm(args, rc, rank: int, world: int):
+    if rank != 0:
+        return
+    p = rc.problem
+    ref, kind, what = reference_checker()
+    cores = os.cpu_count() or 1
+    per_step_budget = max(0.5, min(2.0, 150.0 / max(1, args.steps + args.warmup)))
+    batch, _ = size_cpu_sample(ref, p, rc.samples, per_step_budget)
+    for j in range(args.warmup):
+        cpu_reference_step(ref, p, batch, 100 + j)
+    times = [cpu_reference_step(ref, p, batch, 200 + j) for j in range(args.steps)]
+    total = sum(times)
+    value = batch * args.steps / total
+    sample = (f"{batch} of {rc.samples} samples per step ({what}; velocity-input/unicycle kinds via the "
+              f"reference's rk4_with extension point), run_denoising steps=1, workers=0 (all {cores} threads)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(rc, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--graphs", type=int, default=1)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_2503_12204_b200 import scenarios as S
+    rc = S.baseline_config(args.config)
+
+    if args.impl == "reference":
+        run_reference_arm(args, rc, rank, world)
+        return
+
+    import paper_2503_12204_b200 as d4
+    from paper_2503_12204_b200._lib import lib
+    dist = dist_setup(world) if world > 1 else None
+    nccl_id = None
+    if world > 1:
+        buf = C.create_string_buffer(128)
+        obj = [None]
+        if rank == 0:
+            assert lib().d4orm_cuda_nccl_id(buf) == 0, "ncclGetUniqueId failed"
+            obj = [bytes(buf.raw)]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    p = rc.problem
+    M = rc.samples
+    Ml = M // world
+    g = d4.GpuDenoiser(p, device=local_rank, rank=rank, world=world, nccl_id=nccl_id, precision=d4.PREC_F32,
+                       noise=d4.NOISE_PHILOX, graphs=bool(args.graphs))
+    cfg = d4.DenoiserConfig(steps=rc.steps, batch=M, lam=rc.lam, alpha_bar_final=rc.alpha_bar_final, seed=rc.seed)
+    base = np.zeros((p.horizon, p.robots, p.du))
+
+    L = lib()
+    L.d4orm_cuda_fp32_peak.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    peak_tf, peak_clk = C.c_double(), C.c_double()
+    L.d4orm_cuda_fp32_peak(local_rank, 5, C.byref(peak_tf), C.byref(peak_clk))
+
+    if dist:
+        dist.barrier()
+    with ClockSampler(local_rank) as clk:
+        ms, kms = g.bench_steps(base, cfg, args.warmup, args.steps, kernels=True)
+    ms = reduce_max(dist, ms)
+    if dist:
+        dist.barrier()
+    value = M * args.steps / (ms / 1e3)
+
+    # e2e through the public C-ABI call with host buffers
+    e2e = None
+    if not args.no_e2e:
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        g.run_denoising(base, cfg)
+        dt = reduce_max(dist, time.perf_counter() - t0)
+        E = p.elems
+        e2e = {"value": M * cfg.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(E * 4 + E * 8 + (cfg.steps + 1) * 8 + 8),
+               "d2h_bytes_per_step": int(E * 8 + cfg.steps * 32 + 8),
+               "step": f"one run_denoising call = {cfg.steps} denoising steps, host base in, host variable+trace out",
+               "ms_per_call": dt * 1e3}
+
+    F = algorithmic_flops_per_eval(p)
+    k23_ms = kms[1]
+    achieved = Ml * F / (k23_ms * 1e-3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(rc.name)
+    E = p.elems
+    k5_bytes = Ml * E * 4 + Ml * 4 + (Ml + 255) // 256 * E * 4 + E * 4
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (seeded scenario generators, Philox noise)", "config": config_json(rc, world),
+        "roofline": {"kernel": "k_rollout_fitness (K2+K3)", "bound": "fp32", "achieved": achieved, "peak": peak_tf.value,
+                     "unit": "TFLOP/s", "frac": achieved / peak_tf.value if peak_tf.value else None,
+                     "traffic": traffic, "flops_per_eval": F, "evals_per_launch": Ml, "launch_ms": k23_ms,
+                     "peak_source": "measured live: d4orm_cuda_fp32_peak (FFMA2 over all SMs); MEASURED_PEAKS.json has no FP32 figure"},
+        "kernel_ms": {"K1_philox": kms[0], "K2K3_rollout_fitness": kms[1], "K4_weights": kms[2],
+                      "K5_wmean_partial": kms[3], "K5_tree_update": kms[4]},
+        "k5_hbm": {"achieved_gbs": k5_bytes / (kms[3] * 1e-3) / 1e9 if kms[3] > 0 else None,
+                   "peak_gbs": _hbm_peak(), "bytes_per_launch": k5_bytes},
+        "gpu_launches": args.steps * g.launches_per_step(),
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if rank == 0 and world == 1 and not args.no_cpu:
+        ref, kind, what = reference_checker()
+        batch, t = size_cpu_sample(ref, p, M, 2.0)
+        reps = max(1, int(math.ceil(4.0 / max(t, 1e-3))))
+        tt = sum(cpu_reference_step(ref, p, batch, 300 + j) for j in range(min(reps, 5)))
+        n = min(reps, 5)
+        line["cpu_baseline"] = {"value": batch * n / tt, "unit": UNIT, "cores": os.cpu_count(), "kind": kind,
+                                "sample": f"{n} denoising step(s) x {batch} of {M} samples ({what}), all host threads"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    g.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _hbm_peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return json.loads(f.read_text())["hbm_gbs"]
+    except Exception:
+        return 6650.0  # B200_PROFILING.md fallback
+
+
+if __name__ == "__main__":
+    main()
