@@ -1,0 +1,117 @@
+// d4orm_common.cuh — model kinds, reference-exact scalar arithmetic, RK4.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <type_traits>
+
+namespace d4k {
+
+enum Kind { DIFFDRIVE = 0, HOLO2D = 1, HOLO3D = 2, HOLO2D_VEL = 3, HOLO3D_VEL = 4, UNICYCLE = 5 };
+
+template <int KIND>
+struct ModelDims;
+template <> struct ModelDims<DIFFDRIVE> { static constexpr int DX = 4, DU = 2, PD = 2; };
+template <> struct ModelDims<HOLO2D> { static constexpr int DX = 4, DU = 2, PD = 2; };
+template <> struct ModelDims<HOLO3D> { static constexpr int DX = 6, DU = 3, PD = 3; };
+template <> struct ModelDims<HOLO2D_VEL> { static constexpr int DX = 2, DU = 2, PD = 2; };
+template <> struct ModelDims<HOLO3D_VEL> { static constexpr int DX = 3, DU = 3, PD = 3; };
+template <> struct ModelDims<UNICYCLE> { static constexpr int DX = 3, DU = 2, PD = 2; };
+
+// fp64 (parity) mode evaluates every expression exactly as the reference's
+// x86-64 build does: separately rounded mul/add, never contracted to FMA.
+// fp32 (throughput) mode lets the compiler contract freely.
+template <typename S> __device__ __forceinline__ S xmul(S a, S b);
+template <typename S> __device__ __forceinline__ S xadd(S a, S b);
+template <> __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ double xadd(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float xmul(float a, float b) { return a * b; }
+template <> __device__ __forceinline__ float xadd(float a, float b) { return a + b; }
+template <typename S> __device__ __forceinline__ S xsub(S a, S b) { return xadd(a, -b); }
+
+__device__ __forceinline__ void xsincos(double a, double* s, double* c) { sincos(a, s, c); }
+__device__ __forceinline__ void xsincos(float a, float* s, float* c) { sincosf(a, s, c); }
+__device__ __forceinline__ double xsqrt(double a) { return sqrt(a); }
+__device__ __forceinline__ float xsqrt(float a) { return sqrtf(a); }
+
+// Derivative functors (dynamics.hpp:81-119 and the three BASELINE extensions).
+template <int KIND, typename S>
+__device__ __forceinline__ void deriv(const S* x, const S* u, S* f) {
+  if constexpr (KIND == DIFFDRIVE) {
+    S sn, cs;
+    xsincos(x[2], &sn, &cs);
+    f[0] = xmul(x[3], cs);
+    f[1] = xmul(x[3], sn);
+    f[2] = u[0];
+    f[3] = u[1];
+  } else if constexpr (KIND == HOLO2D) {
+    f[0] = x[2]; f[1] = x[3]; f[2] = u[0]; f[3] = u[1];
+  } else if constexpr (KIND == HOLO3D) {
+    f[0] = x[3]; f[1] = x[4]; f[2] = x[5]; f[3] = u[0]; f[4] = u[1]; f[5] = u[2];
+  } else if constexpr (KIND == HOLO2D_VEL) {
+    f[0] = u[0]; f[1] = u[1];
+  } else if constexpr (KIND == HOLO3D_VEL) {
+    f[0] = u[0]; f[1] = u[1]; f[2] = u[2];
+  } else {  // UNICYCLE
+    S sn, cs;
+    xsincos(x[2], &sn, &cs);
+    f[0] = xmul(u[0], cs);
+    f[1] = xmul(u[0], sn);
+    f[2] = u[1];
+  }
+}
+
+// detail::rk4_with (dynamics.hpp:123-130), element order as Eigen evaluates it:
+//   k2 = f(x + (0.5dt)k1), k3 = f(x + (0.5dt)k2), k4 = f(x + dt·k3)
+//   x' = x + (dt/6)·(((k1 + 2k2) + 2k3) + k4)
+template <int KIND, typename S>
+__device__ __forceinline__ void rk4(S* x, const S* u, S dt, S half_dt, S dt6) {
+  constexpr int DX = ModelDims<KIND>::DX;
+  S k1[DX], k2[DX], k3[DX], k4[DX], tmp[DX];
+  deriv<KIND>(x, u, k1);
+#pragma unroll
+  for (int j = 0; j < DX; ++j) tmp[j] = xadd(x[j], xmul(half_dt, k1[j]));
+  deriv<KIND>(tmp, u, k2);
+#pragma unroll
+  for (int j = 0; j < DX; ++j) tmp[j] = xadd(x[j], xmul(half_dt, k2[j]));
+  deriv<KIND>(tmp, u, k3);
+#pragma unroll
+  for (int j = 0; j < DX; ++j) tmp[j] = xadd(x[j], xmul(dt, k3[j]));
+  deriv<KIND>(tmp, u, k4);
+#pragma unroll
+  for (int j = 0; j < DX; ++j) {
+    const S acc = xadd(xadd(xadd(k1[j], xmul(S(2), k2[j])), xmul(S(2), k3[j])), k4[j]);
+    x[j] = xadd(x[j], xmul(dt6, acc));
+  }
+}
+
+// ---------------------------------------------------------- packed f32x2
+// sm_100 packed FP32 (FADD2 / FFMA2 / FMUL2): two lanes per instruction, the
+// scalar operand broadcast from one register.
+__device__ __forceinline__ uint64_t pack2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float((uint32_t)v); }
+__device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
+__device__ __forceinline__ uint32_t lo32(uint64_t v) { return (uint32_t)v; }
+__device__ __forceinline__ uint32_t hi32(uint64_t v) { return (uint32_t)(v >> 32); }
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2_b(float a, uint64_t b) { return fadd2(pack2(a, a), b); }  // (a,a)+b
+__device__ __forceinline__ uint64_t ffma2_sq(uint64_t a, uint64_t c) {                               // a*a + c
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(d) : "l"(a), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+}  // namespace d4k

@@ -26,7 +26,8 @@
 
 namespace d4k {
 template <typename S, int KIND>
-cudaError_t launch_k23(int tb, int maxw, dim3 grid, size_t smem, cudaStream_t st, const FitParams<S>& p);
+cudaError_t launch_k23(int tb, int maxw, dim3 grid, int threads, size_t smem, cudaStream_t st,
+                       const FitParams<S>& p);
 }
 
 namespace {
@@ -130,7 +131,7 @@ struct d4orm_cuda_ctx {
   void* noise_user = nullptr;
 
   // device buffers (typeless where the scalar type varies)
-  DevBuf<unsigned char> z[2], base, msv, starts_d, goals_d, inv_d, obs_d, partial, roots;
+  DevBuf<unsigned char> z[2], base, msv, bm, starts_d, goals_d, inv_d, obs_d, partial, roots;
   DevBuf<unsigned char> states_out, controls_out;
   DevBuf<double> var, rewards, w64, trace;
   DevBuf<float> w32;
@@ -201,17 +202,16 @@ int64_t elems_of(const d4orm_cuda_ctx* c) { return (int64_t)c->prob.robots * c->
 
 template <typename S>
 size_t fit_smem(const d4orm_cuda_ctx* c, int TC) {
-  const int PD = c->prob.pdim;
-  size_t b = (size_t)PD * c->spc * c->Rp * (TC + 1) * sizeof(S);
-  b += (size_t)c->Rp * PD * sizeof(S) + (size_t)c->Rp * sizeof(S) + (size_t)(4 * c->prob.n_obstacles + 2) * sizeof(S);
-  b += 16 + 2 * d4k::kThreads * sizeof(double) + 2 * d4k::kThreads * sizeof(int);
-  return b;
+  return d4k::fit_smem_bytes<S>(c->prob.pdim, c->spc, TC, c->Rp, c->prob.n_obstacles, c->spc * c->Rp);
 }
 
+// Time-chunk length: one fitness item per thread (TC = Rp, ≥ 16), a multiple
+// of the rollout prefetch depth, halved until ≥ 2 CTAs fit per SM.
 template <typename S>
 int choose_tc(d4orm_cuda_ctx* ctx, int* tc_out, size_t* smem_out) {
   int TC = ctx->Rp >= 16 ? (ctx->Rp < 64 ? ctx->Rp : 64) : 16;
-  while (fit_smem<S>(ctx, TC) > 200 * 1024 && TC > 4) TC /= 2;
+  while (fit_smem<S>(ctx, TC) > 100 * 1024 && TC > d4k::kPF) TC /= 2;
+  if (TC % d4k::kPF != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d not a multiple of %d", TC, d4k::kPF);
   if (TC >= ctx->Rp && TC % ctx->Rp != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d vs Rp %d", TC, ctx->Rp);
   *tc_out = TC;
   *smem_out = fit_smem<S>(ctx, TC);
@@ -287,8 +287,9 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
   f.dt6 = (S)(p.dt / 6.0);
   const double margin = 2.0 * p.robot_radius + p.epsilon;
   const double m2 = margin * margin;
-  if (std::is_same<S, double>::value) f.neg_margin_sq = (S)m2;
-  else f.neg_margin_sq = (S)(-(double)std::nextafter((float)m2, INFINITY));
+  if (std::is_same<S, double>::value) f.margin_sq = (S)m2;
+  else f.margin_sq = (S)(-(double)std::nextafter((float)m2, INFINITY));
+  f.bm = (const S*)ctx->bm.p;
   f.w_t = p.w_t;
   f.w_o = p.obstacle_weight;
   f.w_e = p.effort_weight;
@@ -311,13 +312,14 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
 template <typename S>
 cudaError_t launch_fit(d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f, size_t smem) {
   const dim3 grid((unsigned)((f.M + ctx->spc - 1) / ctx->spc));
+  const int th = ctx->spc * ctx->Rp;
   switch (ctx->prob.kind) {
-    case 0: return d4k::launch_k23<S, 0>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
-    case 1: return d4k::launch_k23<S, 1>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
-    case 2: return d4k::launch_k23<S, 2>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
-    case 3: return d4k::launch_k23<S, 3>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
-    case 4: return d4k::launch_k23<S, 4>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
-    default: return d4k::launch_k23<S, 5>(ctx->TB, ctx->MAXW, grid, smem, ctx->s_main, f);
+    case 0: return d4k::launch_k23<S, 0>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
+    case 1: return d4k::launch_k23<S, 1>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
+    case 2: return d4k::launch_k23<S, 2>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
+    case 3: return d4k::launch_k23<S, 3>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
+    case 4: return d4k::launch_k23<S, 4>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
+    default: return d4k::launch_k23<S, 5>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
   }
 }
 
@@ -363,6 +365,7 @@ int ensure_buffers(d4orm_cuda_ctx* ctx, const RunShape& rs, bool two_z) {
   if (two_z) CU(ctx->z[1].ensure((size_t)rs.Ml * rs.E * S));
   CU(ctx->base.ensure((size_t)rs.E * S));
   CU(ctx->msv.ensure((size_t)rs.E * S));
+  CU(ctx->bm.ensure((size_t)rs.E * S));
   CU(ctx->var.ensure((size_t)rs.E));
   CU(ctx->rewards.ensure((size_t)rs.M));
   CU(ctx->w64.ensure((size_t)rs.M));
@@ -387,11 +390,15 @@ int set_keys(d4orm_cuda_ctx* ctx, const RunShape& rs, uint64_t seed) {
 
 template <typename S>
 int launch_noise(d4orm_cuda_ctx* ctx, cudaStream_t st, int slot, const RunShape& rs, int step) {
-  const int64_t groups = rs.Ml * ((rs.E + 3) / 4);
-  int64_t blocks = (groups + d4k::kThreads - 1) / d4k::kThreads;
-  if (blocks > 148 * 64) blocks = 148 * 64;
-  d4k::k_philox_noise<S><<<(unsigned)blocks, d4k::kThreads, 0, st>>>((S*)ctx->z[slot].p, rs.Ml, rs.E, rs.m0,
-                                                                     ctx->keys.p, step);
+  const int64_t groups = (rs.E + 3) / 4;
+  const unsigned gx = (unsigned)((groups + d4k::kThreads - 1) / d4k::kThreads);
+  // ≈ 16 resident CTAs per SM worth of work in flight; grid.y strides samples
+  int64_t gy = (148LL * 16 + gx - 1) / gx;
+  if (gy > rs.Ml) gy = rs.Ml;
+  if (gy > 65535) gy = 65535;
+  if (gy < 1) gy = 1;
+  d4k::k_philox_noise<S><<<dim3(gx, (unsigned)gy), d4k::kThreads, 0, st>>>((S*)ctx->z[slot].p, rs.Ml, (int)rs.E,
+                                                                           rs.m0, ctx->keys.p, step);
   CU(cudaGetLastError());
   return D4ORM_OK;
 }
@@ -454,7 +461,7 @@ int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, int slot, int n
     NC(g_nccl.AllGather(ctx->rewards.p + rs.m0, ctx->rewards.p, (size_t)rs.Ml, ncclFloat64, ctx->comm, ctx->s_main));
   }
   d4k::WeightParams wp{ctx->rewards.p, rs.M, rs.lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p + 4 * (rs.N - i), i,
-                       nullptr, ctx->errw.p};
+                       ctx->errw.p};
   d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
   CU(cudaGetLastError());
   if (int r = mark(2)) return r;
@@ -471,17 +478,22 @@ int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, int slot, int n
   CU(cudaGetLastError());
   if (int r = mark(3)) return r;
   const unsigned tgrid = (unsigned)((rs.E + d4k::kThreads - 1) / d4k::kThreads);
+  S* bm = f64 ? nullptr : (S*)ctx->bm.p;
+  const S* bs = (const S*)ctx->base.p;
   if (ctx->world == 1) {
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
-                                                                   sab, next_ms, ctx->var.p, (S*)ctx->msv.p, nullptr);
+                                                                   sab, next_ms, ctx->var.p, (S*)ctx->msv.p, bs, bm,
+                                                                   nullptr);
   } else {
     S* my_root = (S*)ctx->roots.p + (size_t)ctx->rank * rs.E;
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
-                                                                   sab, next_ms, ctx->var.p, (S*)ctx->msv.p, my_root);
+                                                                   sab, next_ms, ctx->var.p, (S*)ctx->msv.p, bs, bm,
+                                                                   my_root);
     CU(cudaGetLastError());
     NC(g_nccl.AllGather(my_root, ctx->roots.p, (size_t)rs.E, f64 ? ncclFloat64 : ncclFloat32, ctx->comm, ctx->s_main));
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->roots.p, ctx->world, rs.E, sab,
-                                                                   next_ms, ctx->var.p, (S*)ctx->msv.p, nullptr);
+                                                                   next_ms, ctx->var.p, (S*)ctx->msv.p, bs, bm,
+                                                                   nullptr);
   }
   CU(cudaGetLastError());
   if (int r = mark(4)) return r;
@@ -490,14 +502,11 @@ int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, int slot, int n
 }
 
 template <typename S>
-__global__ void k_init_var(const double* var, double ms, S* msv, int64_t n) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n) msv[e] = (S)(ms * var[e]);
-}
-template <typename S>
-__global__ void k_cast(const double* src, S* dst, int64_t n) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e < n) dst[e] = (S)src[e];
+cudaError_t init_msv(d4orm_cuda_ctx* ctx, int64_t E, double ms) {
+  const bool f64 = std::is_same<S, double>::value;
+  d4k::k_init_var<S><<<(unsigned)((E + 255) / 256), 256, 0, ctx->s_main>>>(
+      ctx->var.p, ms, (S*)ctx->msv.p, (const S*)ctx->base.p, f64 ? nullptr : (S*)ctx->bm.p, E);
+  return cudaGetLastError();
 }
 
 // Prologue of a run: base, variable init, msv for step N, noise for step N.
@@ -528,9 +537,7 @@ int prologue(d4orm_cuda_ctx* ctx, const RunShape& rs, const double* base_host, c
     }
   }
   CU(cudaMemcpyAsync(ctx->var.p, v.data(), sizeof(double) * E, cudaMemcpyHostToDevice, ctx->s_main));
-  k_init_var<S><<<(unsigned)((E + 255) / 256), 256, 0, ctx->s_main>>>(ctx->var.p, 1.0 / std::sqrt(ctx->ab[rs.N]),
-                                                                        (S*)ctx->msv.p, E);
-  CU(cudaGetLastError());
+  CU(init_msv<S>(ctx, E, 1.0 / std::sqrt(ctx->ab[rs.N])));
   const unsigned long long init = ~0ull;
   CU(cudaMemcpyAsync(ctx->errw.p, &init, sizeof init, cudaMemcpyHostToDevice, ctx->s_main));
   if (philox) {
@@ -749,7 +756,9 @@ int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* p) {
   ctx->TB = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
   ctx->Rp = (R + ctx->TB - 1) / ctx->TB * ctx->TB;
   ctx->MAXW = ctx->Rp <= 64 ? 2 : 8;
-  ctx->spc = d4k::kThreads / ctx->Rp;
+  // 128-thread CTAs (several resident per SM: one CTA's latency-bound rollout
+  // phase overlaps another's compute-bound fitness phase)
+  ctx->spc = ctx->Rp >= 128 ? 1 : 128 / ctx->Rp;
   if (int r = choose_tc<float>(ctx, &ctx->TC32, &ctx->smem32)) return r;
   if (int r = choose_tc<double>(ctx, &ctx->TC64, &ctx->smem64)) return r;
   ctx->has_problem = true;
@@ -779,9 +788,7 @@ int denoise_step_t(d4orm_cuda_ctx* ctx, const double* base, const double* var_in
   if (rs.mode == D4ORM_DEFORMATION) std::memcpy(b.data(), base, sizeof(double) * E);
   CU((upload_as<S>(ctx->base, b.data(), E, ctx->s_main)));
   CU(cudaMemcpyAsync(ctx->var.p, var_in, sizeof(double) * E, cudaMemcpyHostToDevice, ctx->s_main));
-  k_init_var<S><<<(unsigned)((E + 255) / 256), 256, 0, ctx->s_main>>>(ctx->var.p, 1.0 / std::sqrt(ctx->ab[i]),
-                                                                        (S*)ctx->msv.p, E);
-  CU(cudaGetLastError());
+  CU(init_msv<S>(ctx, E, 1.0 / std::sqrt(ctx->ab[i])));
   const unsigned long long init = ~0ull;
   CU(cudaMemcpyAsync(ctx->errw.p, &init, sizeof init, cudaMemcpyHostToDevice, ctx->s_main));
   if (int r = set_keys(ctx, rs, c->seed)) return r;
@@ -824,6 +831,8 @@ int rollout_fitness_t(d4orm_cuda_ctx* ctx, const double* u, int64_t count, doubl
   CU(ctx->z[0].ensure((size_t)count * E * sizeof(S)));
   CU(ctx->base.ensure((size_t)E * sizeof(S)));
   CU(ctx->msv.ensure((size_t)E * sizeof(S)));
+  CU(ctx->bm.ensure((size_t)E * sizeof(S)));
+  CU(cudaMemsetAsync(ctx->bm.p, 0, E * sizeof(S), ctx->s_main));
   CU(ctx->rewards.ensure((size_t)count));
   CU(ctx->counts.ensure((size_t)count * 2));
   CU(ctx->errw.ensure(1));
@@ -890,7 +899,7 @@ int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t
   CU(ctx->trace.ensure(4));
   CU(ctx->errw.ensure(1));
   CU(cudaMemcpyAsync(ctx->rewards.p, rewards, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->s_main));
-  d4k::WeightParams wp{ctx->rewards.p, m, lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p, 0, nullptr, ctx->errw.p};
+  d4k::WeightParams wp{ctx->rewards.p, m, lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p, 0, ctx->errw.p};
   d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(ctx->s_main));

@@ -1,0 +1,494 @@
+// k23.cuh — K2+K3: fused rollout + team fitness, one kernel.
+//
+// CTA = `spc` samples × Rp robot lanes (blockDim = spc·Rp ≤ 256, usually 128,
+// several CTAs resident per SM).  Time advances in chunks of TC steps:
+//
+//  phase A  thread = (sample, robot): TC RK4 steps in registers
+//           (dynamics.cpp:65-87 / dynamics.hpp:123-130), controls formed as
+//           clamp(base + mean_scale·var + std·z) (denoiser.cpp:44-45,158-159)
+//           with an 8-deep register prefetch ring on the HBM noise stream;
+//           positions → shared memory, one robot-contiguous row per (sample, t).
+//  phase B  thread = (sample, t) item: goal + obstacle terms for every robot
+//           and all R(R−1)/2 unordered pair tests of that time step
+//           (reward.cpp:88-127).  fp32: tiles of TB robots, A rows streamed
+//           against a register-resident B tile, two pair tests per packed
+//           FADD2/FFMA2 instruction; a conflict is the sign bit of
+//           d² − m²↑, OR-ed into per-robot flags (3 issue slots per pair).
+//           fp64 (parity): the reference's own loops, exact `<=` tests.
+//
+// reward[m] = (Σ goal − w_t·#conflict robot-steps − w_o·#obstacle robot-steps
+//              − w_e·Σ‖u‖²) / (R·T), reduced in a fixed order.
+#pragma once
+
+#include "d4orm_common.cuh"
+
+namespace d4k {
+
+constexpr int kFitMaxThreads = 128;
+constexpr int kPF = 8;  // rollout prefetch depth (time steps)
+
+template <typename S>
+struct FitParams {
+  const S* z;            // [M][T][R][du] (row 0 = global sample m_global0)
+  const S* base;         // [T][R][du]   (fp64 path)
+  const S* msv;          // [T][R][du]   mean_scale·variable (fp64 path)
+  const S* bm;           // [T][R][du]   base + msv (fp32 path)
+  S sd;                  // sampling std of this step
+  const S* starts;       // [R][dx]
+  const S* goals;        // [R][pd]
+  const S* inv_dstart;   // [R]  fp32: 1/‖start−goal‖; fp64: ‖start−goal‖ (divide)
+  const S* obs;          // [O][4]: cx, cy, cz, fp32: −(r+R_a)²↑ | fp64: (r+R_a)²
+  int n_obs;
+  S lower[3], upper[3];
+  S dt, half_dt, dt6;
+  S margin_sq;           // fp32: −(2R_a+ε)²↑ ; fp64: (2R_a+ε)²
+  double w_t, w_o, w_e;
+  int R, Rp, T, TC, spc;
+  int64_t M;             // samples in this launch
+  int64_t m_global0;     // global index of row 0 (error keys)
+  int step_key;          // N − i (error key)
+  double* reward;        // [M]
+  int* counts;           // [M][2] or null
+  S* states_out;         // [M][T+1][R][dx] or null
+  S* controls_out;       // [M][T+1][R][du] or null
+  unsigned long long* err;
+};
+
+template <typename S>
+struct FitSmem {
+  S* pos;     // [PD][spc][TC][RS]
+  S* goal;    // [PD][Rp]  fp32: −goal ; fp64: goal
+  S* inv;     // [Rp]
+  S* one;     // [Rp]      1 valid / 0 padding
+  S* obs;     // [O][4]
+  double* red;   // [nthreads]
+  double* eff;   // [nthreads]
+  int* cnt;      // [2·nthreads]
+  int RS, TC, spc, Rp;
+  __device__ __forceinline__ S* row(int c, int s, int tc) const {
+    return pos + ((size_t)(c * spc + s) * TC + tc) * RS;
+  }
+};
+
+template <typename S>
+__host__ __device__ inline size_t fit_smem_bytes(int PD, int spc, int TC, int Rp, int nobs, int nthreads) {
+  const int RS = Rp + 2;
+  size_t b = (size_t)PD * spc * TC * RS * sizeof(S);
+  b += (size_t)PD * Rp * sizeof(S) + 2 * (size_t)Rp * sizeof(S) + (size_t)4 * (nobs + 1) * sizeof(S);
+  b = (b + 15) & ~size_t(15);
+  b += 2 * (size_t)nthreads * sizeof(double) + 2 * (size_t)nthreads * sizeof(int);
+  return b;
+}
+
+// ---------------------------------------------------------------- fp32 tiles
+template <int PD>
+__device__ __forceinline__ uint64_t pair2_f32(float nxa, float nya, float nza, uint64_t xb, uint64_t yb, uint64_t zb,
+                                              uint64_t nm2) {
+  const uint64_t dx = fadd2_b(nxa, xb);
+  const uint64_t dy = fadd2_b(nya, yb);
+  uint64_t t;
+  if constexpr (PD == 3) {
+    t = ffma2_sq(fadd2_b(nza, zb), nm2);
+    t = ffma2_sq(dy, t);
+  } else {
+    t = ffma2_sq(dy, nm2);
+  }
+  return ffma2_sq(dx, t);
+}
+
+template <int PD>
+__device__ __forceinline__ uint32_t pair1_f32(float xa, float ya, float za, float xb, float yb, float zb, float nm2) {
+  const float dx = xb - xa, dy = yb - ya;
+  float t = fmaf(dy, dy, nm2);
+  if constexpr (PD == 3) t = fmaf(zb - za, zb - za, t);
+  return __float_as_uint(fmaf(dx, dx, t));
+}
+
+template <int TB>
+__device__ __forceinline__ uint32_t sign_mask(const uint32_t* f) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = TB - 1; j >= 0; --j) m = __funnelshift_l(f[j], m, 1);  // (m << 1) | sign(f[j])
+  return m;
+}
+
+template <int PD, int TB>
+struct PackedTile {
+  uint64_t x[TB / 2], y[TB / 2], z[PD == 3 ? TB / 2 : 1];
+  __device__ __forceinline__ void load(const float* X, const float* Y, const float* Z, int k0) {
+#pragma unroll
+    for (int j = 0; j < TB / 2; ++j) {
+      x[j] = *reinterpret_cast<const uint64_t*>(X + k0 + 2 * j);
+      y[j] = *reinterpret_cast<const uint64_t*>(Y + k0 + 2 * j);
+      if constexpr (PD == 3) z[j] = *reinterpret_cast<const uint64_t*>(Z + k0 + 2 * j);
+    }
+  }
+};
+
+// One (sample, t) item in fp32: returns Σ goal terms; conflict / obstacle counts.
+template <int PD, int TB, int MAXW>
+__device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int tc, int R, int n_obs, float nm2,
+                                          int* nconf, int* nobs) {
+  const float* X = sm.row(0, s, tc);
+  const float* Y = sm.row(1, s, tc);
+  const float* Z = PD == 3 ? sm.row(2, s, tc) : X;
+  const int ntiles = sm.Rp / TB;
+  const uint64_t nm2p = pack2(nm2, nm2);
+  uint32_t cm[MAXW];
+#pragma unroll
+  for (int w = 0; w < MAXW; ++w) cm[w] = 0;
+  float gacc = 0.f;
+  int no = 0;
+  for (int a = 0; a < ntiles; ++a) {
+    PackedTile<PD, TB> A;
+    A.load(X, Y, Z, a * TB);
+    // ---- goal (reward.cpp:92-97) and obstacle (reward.cpp:112-125) terms
+    uint32_t om = 0;
+#pragma unroll
+    for (int j = 0; j < TB / 2; ++j) {
+      const int k = a * TB + 2 * j;
+      const uint64_t gx = *reinterpret_cast<const uint64_t*>(sm.goal + k);
+      const uint64_t gy = *reinterpret_cast<const uint64_t*>(sm.goal + sm.Rp + k);
+      const uint64_t dx = fadd2(A.x[j], gx), dy = fadd2(A.y[j], gy);
+      uint64_t d2 = fmul2(dx, dx);
+      d2 = ffma2_sq(dy, d2);
+      if constexpr (PD == 3) {
+        const uint64_t gz = *reinterpret_cast<const uint64_t*>(sm.goal + 2 * sm.Rp + k);
+        d2 = ffma2_sq(fadd2(A.z[j], gz), d2);
+      }
+      gacc += fmaf(-sqrtf(lo_f(d2)), sm.inv[k], sm.one[k]);
+      gacc += fmaf(-sqrtf(hi_f(d2)), sm.inv[k + 1], sm.one[k + 1]);
+      uint64_t oacc = 0;
+      for (int o = 0; o < n_obs; ++o) {
+        const float4 ob = *reinterpret_cast<const float4*>(sm.obs + 4 * o);  // −cx, −cy, −cz, −L²↑
+        const uint64_t ox = fadd2_b(ob.x, A.x[j]);
+        const uint64_t oy = fadd2_b(ob.y, A.y[j]);
+        uint64_t t = ffma2_sq(oy, pack2(ob.w, ob.w));
+        if constexpr (PD == 3) t = ffma2_sq(fadd2_b(ob.z, A.z[j]), t);
+        oacc |= ffma2_sq(ox, t);
+      }
+      om |= ((lo32(oacc) >> 31) | ((hi32(oacc) >> 31) << 1)) << (2 * j);
+    }
+    const int kv = R - a * TB;  // valid robots in this tile
+    no += __popc(kv >= 32 ? om : (om & ((1u << (kv > 0 ? kv : 0)) - 1u)));
+    // ---- pairs inside tile A
+    uint32_t f[TB];
+#pragma unroll
+    for (int q = 0; q < TB; ++q) f[q] = 0;
+#pragma unroll
+    for (int i = 0; i < TB / 2; ++i) {
+      const float x0 = lo_f(A.x[i]), x1 = hi_f(A.x[i]), y0 = lo_f(A.y[i]), y1 = hi_f(A.y[i]);
+      const float z0 = PD == 3 ? lo_f(A.z[i]) : 0.f, z1 = PD == 3 ? hi_f(A.z[i]) : 0.f;
+#pragma unroll
+      for (int j = i + 1; j < TB / 2; ++j) {
+        const uint64_t t0 = pair2_f32<PD>(-x0, -y0, -z0, A.x[j], A.y[j], PD == 3 ? A.z[j] : 0ull, nm2p);
+        const uint64_t t1 = pair2_f32<PD>(-x1, -y1, -z1, A.x[j], A.y[j], PD == 3 ? A.z[j] : 0ull, nm2p);
+        f[2 * i] |= lo32(t0) | hi32(t0);
+        f[2 * i + 1] |= lo32(t1) | hi32(t1);
+        f[2 * j] |= lo32(t0) | lo32(t1);
+        f[2 * j + 1] |= hi32(t0) | hi32(t1);
+      }
+      const uint32_t t = pair1_f32<PD>(x0, y0, z0, x1, y1, z1, nm2);
+      f[2 * i] |= t;
+      f[2 * i + 1] |= t;
+    }
+    uint32_t ma = sign_mask<TB>(f);
+    // ---- A × B tiles
+    for (int b = a + 1; b < ntiles; ++b) {
+      PackedTile<PD, TB> B;
+      B.load(X, Y, Z, b * TB);
+      uint32_t fb[TB];
+#pragma unroll
+      for (int q = 0; q < TB; ++q) fb[q] = 0;
+      // A rows streamed from shared memory (two robots per LDS.64), so only
+      // the packed B tile and its flags stay register-resident.
+#pragma unroll 2
+      for (int i = 0; i < TB / 2; ++i) {
+        const float2 ax = *reinterpret_cast<const float2*>(X + a * TB + 2 * i);
+        const float2 ay = *reinterpret_cast<const float2*>(Y + a * TB + 2 * i);
+        const float2 az = PD == 3 ? *reinterpret_cast<const float2*>(Z + a * TB + 2 * i) : make_float2(0.f, 0.f);
+        const float nx0 = -ax.x, nx1 = -ax.y, ny0 = -ay.x, ny1 = -ay.y, nz0 = -az.x, nz1 = -az.y;
+        uint32_t fa0 = 0, fa1 = 0;
+#pragma unroll
+        for (int j = 0; j < TB / 2; ++j) {
+          const uint64_t t0 = pair2_f32<PD>(nx0, ny0, nz0, B.x[j], B.y[j], PD == 3 ? B.z[j] : 0ull, nm2p);
+          const uint64_t t1 = pair2_f32<PD>(nx1, ny1, nz1, B.x[j], B.y[j], PD == 3 ? B.z[j] : 0ull, nm2p);
+          fa0 |= lo32(t0) | hi32(t0);
+          fa1 |= lo32(t1) | hi32(t1);
+          fb[2 * j] |= lo32(t0) | lo32(t1);
+          fb[2 * j + 1] |= hi32(t0) | hi32(t1);
+        }
+        ma |= ((fa0 >> 31) | ((fa1 >> 31) << 1)) << (2 * i);
+      }
+      const uint32_t mb = sign_mask<TB>(fb);
+      const int wb = (b * TB) >> 5, sh = (b * TB) & 31;
+#pragma unroll
+      for (int w = 0; w < MAXW; ++w)
+        if (w == wb) cm[w] |= mb << sh;
+    }
+    const int wa = (a * TB) >> 5, sha = (a * TB) & 31;
+#pragma unroll
+    for (int w = 0; w < MAXW; ++w)
+      if (w == wa) cm[w] |= ma << sha;
+  }
+  int c = 0;
+#pragma unroll
+  for (int w = 0; w < MAXW; ++w) {
+    const int kv = R - 32 * w;
+    if (kv > 0) c += __popc(kv >= 32 ? cm[w] : (cm[w] & ((1u << kv) - 1u)));
+  }
+  *nconf += c;
+  *nobs += no;
+  return gacc;
+}
+
+// One (sample, t) item in fp64: the reference's loops (reward.cpp:88-127) on
+// shared-memory positions, exact `<=` tests; returns Σ goal terms.
+template <int PD>
+__device__ __forceinline__ double item_f64(const FitSmem<double>& sm, int s, int tc, int R, int n_obs, double m2,
+                                           int* nconf, int* nobs) {
+  const double* X = sm.row(0, s, tc);
+  const double* Y = sm.row(1, s, tc);
+  const double* Z = PD == 3 ? sm.row(2, s, tc) : X;
+  double g = 0.0;
+  for (int k = 0; k < R; ++k) {
+    double gsq = 0.0, d;
+    d = __dadd_rn(X[k], -sm.goal[k]);
+    gsq = __dadd_rn(gsq, __dmul_rn(d, d));
+    d = __dadd_rn(Y[k], -sm.goal[sm.Rp + k]);
+    gsq = __dadd_rn(gsq, __dmul_rn(d, d));
+    if constexpr (PD == 3) {
+      d = __dadd_rn(Z[k], -sm.goal[2 * sm.Rp + k]);
+      gsq = __dadd_rn(gsq, __dmul_rn(d, d));
+    }
+    g = __dadd_rn(g, __dadd_rn(1.0, -(sqrt(gsq) / sm.inv[k])));
+    for (int l = 0; l < R; ++l) {
+      if (l == k) continue;
+      double s2 = 0.0;
+      d = __dadd_rn(X[k], -X[l]);
+      s2 = __dadd_rn(s2, __dmul_rn(d, d));
+      d = __dadd_rn(Y[k], -Y[l]);
+      s2 = __dadd_rn(s2, __dmul_rn(d, d));
+      if constexpr (PD == 3) {
+        d = __dadd_rn(Z[k], -Z[l]);
+        s2 = __dadd_rn(s2, __dmul_rn(d, d));
+      }
+      if (s2 <= m2) {
+        ++*nconf;
+        break;
+      }
+    }
+    for (int o = 0; o < n_obs; ++o) {
+      const double* ob = sm.obs + 4 * o;
+      double s2 = 0.0;
+      d = __dadd_rn(X[k], -ob[0]);
+      s2 = __dadd_rn(s2, __dmul_rn(d, d));
+      d = __dadd_rn(Y[k], -ob[1]);
+      s2 = __dadd_rn(s2, __dmul_rn(d, d));
+      if constexpr (PD == 3) {
+        d = __dadd_rn(Z[k], -ob[2]);
+        s2 = __dadd_rn(s2, __dmul_rn(d, d));
+      }
+      if (s2 <= ob[3]) {
+        ++*nobs;
+        break;
+      }
+    }
+  }
+  return g;
+}
+
+template <typename S, int KIND, int TB, int MAXW>
+__global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const FitParams<S> p) {
+  constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
+  constexpr bool F32 = std::is_same<S, float>::value;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, nthreads = blockDim.x;
+  const int R = p.R, Rp = p.Rp, TC = p.TC, spc = p.spc, T = p.T;
+
+  FitSmem<S> sm;
+  sm.RS = Rp + 2;
+  sm.TC = TC;
+  sm.spc = spc;
+  sm.Rp = Rp;
+  sm.pos = reinterpret_cast<S*>(smem_raw);
+  sm.goal = sm.pos + (size_t)PD * spc * TC * sm.RS;
+  sm.inv = sm.goal + (size_t)PD * Rp;
+  sm.one = sm.inv + Rp;
+  sm.obs = sm.one + Rp;
+  {
+    uintptr_t q = reinterpret_cast<uintptr_t>(sm.obs + 4 * (p.n_obs + 1));
+    q = (q + 15) & ~uintptr_t(15);
+    sm.red = reinterpret_cast<double*>(q);
+    sm.eff = sm.red + nthreads;
+    sm.cnt = reinterpret_cast<int*>(sm.eff + nthreads);
+  }
+  for (int j = tid; j < PD * Rp; j += nthreads) {
+    const int c = j / Rp, k = j % Rp;
+    const S g = k < R ? p.goals[k * PD + c] : S(0);
+    sm.goal[j] = F32 ? -g : g;
+  }
+  for (int k = tid; k < Rp; k += nthreads) {
+    sm.inv[k] = k < R ? p.inv_dstart[k] : (F32 ? S(0) : S(1));
+    sm.one[k] = k < R ? S(1) : S(0);
+  }
+  for (int j = tid; j < 4 * p.n_obs; j += nthreads) {
+    const S v = p.obs[j];
+    sm.obs[j] = (F32 && (j & 3) != 3) ? -v : v;
+  }
+
+  // ---- phase-A identity: (sample sA, robot kA)
+  const int sA = tid / Rp, kA = tid % Rp;
+  const int64_t mA = (int64_t)blockIdx.x * spc + sA;
+  const bool liveA = mA < p.M;
+  const bool robotA = liveA && kA < R;
+  S x[DX];
+#pragma unroll
+  for (int j = 0; j < DX; ++j) x[j] = robotA ? p.starts[kA * DX + j] : S(0);
+  if (liveA && kA >= R) {  // padding robots: parked far apart, never counted
+    for (int tc = 0; tc < TC; ++tc) {
+      sm.row(0, sA, tc)[kA] = S(1.0e6) + S(1.0e3) * S(kA);
+      sm.row(1, sA, tc)[kA] = S(-1.0e6) - S(1.0e3) * S(kA);
+      if constexpr (PD == 3) sm.row(2, sA, tc)[kA] = S(1.0e6);
+    }
+  }
+  if (robotA && p.states_out) {
+    S* so = p.states_out + mA * (int64_t)(T + 1) * R * DX + (int64_t)kA * DX;
+#pragma unroll
+    for (int j = 0; j < DX; ++j) so[j] = x[j];
+  }
+  const S* zrow = p.z + (liveA ? mA : 0) * (int64_t)T * R * DU;
+  double effort = 0.0;
+  bool bad = false;
+
+  // prefetch ring: noise (HBM stream) + base/mean-scaled variable (L2-resident);
+  // chunk-local, so it is dead (no registers) during the fitness phase
+  S zq[kPF][DU], bq[kPF][DU], mq[kPF][F32 ? 1 : DU];
+  auto fetch = [&](int t, int t_end, int slot) {
+    if (robotA && t < t_end) {
+      const int64_t e = ((int64_t)t * R + kA) * DU;
+#pragma unroll
+      for (int d = 0; d < DU; ++d) {
+        zq[slot][d] = __ldcs(zrow + e + d);
+        if constexpr (F32) {
+          bq[slot][d] = __ldg(p.bm + e + d);
+        } else {
+          bq[slot][d] = __ldg(p.base + e + d);
+          mq[slot][d] = __ldg(p.msv + e + d);
+        }
+      }
+    }
+  };
+  // ---- phase-B identity: items (sB, tc), ipt consecutive per thread
+  const int ipt = TC >= Rp ? TC / Rp : 1;
+  const int item0 = TC >= Rp ? tid * ipt : tid;
+  const int sB = item0 / TC;
+  const int64_t mB = (int64_t)blockIdx.x * spc + sB;
+  const bool liveB = item0 < spc * TC && mB < p.M;
+  double gsum = 0.0;
+  int nconf = 0, nobs = 0;
+
+  __syncthreads();
+
+  for (int t0 = 0; t0 < T; t0 += TC) {
+    // ===== phase A: integrate TC steps
+    if (robotA) {
+      const int t_end = t0 + TC < T ? t0 + TC : T;
+#pragma unroll
+      for (int j = 0; j < kPF; ++j) fetch(t0 + j, t_end, j);
+      for (int tc = 0; tc < TC; tc += kPF) {
+#pragma unroll
+        for (int j = 0; j < kPF; ++j) {
+          const int t = t0 + tc + j;
+          if (t < T) {
+            S u[DU];
+#pragma unroll
+            for (int d = 0; d < DU; ++d) {
+              S v;
+              if constexpr (F32) {
+                v = fmaf(p.sd, zq[j][d], bq[j][d]);  // base + (mean_scale·var + std·z)
+              } else {
+                v = xadd(bq[j][d], xadd(mq[j][d], xmul(p.sd, zq[j][d])));
+              }
+              v = (v < p.lower[d]) ? p.lower[d] : v;  // cwiseMax(lower)
+              v = (p.upper[d] < v) ? p.upper[d] : v;  // cwiseMin(upper)
+              u[d] = v;
+              if (p.w_e != 0.0) effort += (double)v * (double)v;
+            }
+            fetch(t + kPF, t_end, j);
+            rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
+            bool fin = true;
+#pragma unroll
+            for (int q = 0; q < DX; ++q) fin = fin && isfinite(x[q]);
+            if (!fin && !bad) {
+              bad = true;
+              const unsigned long long key = ((unsigned long long)p.step_key << 52) |
+                                             ((unsigned long long)(p.m_global0 + mA) << 20) |
+                                             ((unsigned long long)kA << 10) | (unsigned long long)(t + 1);
+              atomicMin(p.err, key);
+            }
+            sm.row(0, sA, tc + j)[kA] = x[0];
+            sm.row(1, sA, tc + j)[kA] = x[1];
+            if constexpr (PD == 3) sm.row(2, sA, tc + j)[kA] = x[2];
+            if (p.states_out) {
+              S* so = p.states_out + (mA * (int64_t)(T + 1) + t + 1) * R * DX + (int64_t)kA * DX;
+#pragma unroll
+              for (int q = 0; q < DX; ++q) so[q] = x[q];
+            }
+            if (p.controls_out) {
+              S* co = p.controls_out + (mA * (int64_t)(T + 1) + t) * R * DU + (int64_t)kA * DU;
+#pragma unroll
+              for (int d = 0; d < DU; ++d) co[d] = u[d];
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ===== phase B: fitness of the TC steps just integrated
+    if (liveB) {
+      for (int j = 0; j < ipt; ++j) {
+        const int tc = item0 + j - sB * TC;
+        if (t0 + tc >= T) break;
+        if constexpr (F32) {
+          gsum += (double)item_f32<PD, TB, MAXW>(sm, sB, tc, R, p.n_obs, p.margin_sq, &nconf, &nobs);
+        } else {
+          gsum += item_f64<PD>(sm, sB, tc, R, p.n_obs, p.margin_sq, &nconf, &nobs);
+        }
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- per-sample deterministic reduction
+  sm.red[tid] = liveB ? gsum : 0.0;
+  sm.eff[tid] = robotA ? effort : 0.0;
+  sm.cnt[2 * tid] = liveB ? nconf : 0;
+  sm.cnt[2 * tid + 1] = liveB ? nobs : 0;
+  __syncthreads();
+  if (liveB && item0 == sB * TC) {
+    const int nt = TC >= Rp ? Rp : TC;
+    const int first = TC >= Rp ? sB * Rp : sB * TC;
+    double g = 0.0;
+    long long nc = 0, no = 0;
+    for (int q = 0; q < nt; ++q) {
+      g += sm.red[first + q];
+      nc += sm.cnt[2 * (first + q)];
+      no += sm.cnt[2 * (first + q) + 1];
+    }
+    double value = g - p.w_t * (double)nc - p.w_o * (double)no;
+    if (p.w_e != 0.0) {  // effort extension
+      double eff = 0.0;
+      for (int k = 0; k < R; ++k) eff += sm.eff[sB * Rp + k];
+      value -= p.w_e * eff;
+    }
+    p.reward[mB] = value / ((double)R * (double)T);
+    if (p.counts) {
+      p.counts[2 * mB] = (int)nc;
+      p.counts[2 * mB + 1] = (int)no;
+    }
+  }
+}
+
+}  // namespace d4k

@@ -8,32 +8,33 @@
 namespace d4k {
 
 template <typename S, int KIND, int TB, int MAXW>
-cudaError_t launch_k23_tb(dim3 grid, size_t smem, cudaStream_t st, const FitParams<S>& p) {
+cudaError_t launch_k23_tb(dim3 grid, int threads, size_t smem, cudaStream_t st, const FitParams<S>& p) {
   auto fn = k_rollout_fitness<S, KIND, TB, MAXW>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, kThreads, smem, st>>>(p);
+  fn<<<grid, threads, smem, st>>>(p);
   return cudaGetLastError();
 }
 
 template <typename S, int KIND>
-cudaError_t launch_k23(int tb, int maxw, dim3 grid, size_t smem, cudaStream_t st, const FitParams<S>& p) {
+cudaError_t launch_k23(int tb, int maxw, dim3 grid, int threads, size_t smem, cudaStream_t st,
+                       const FitParams<S>& p) {
   if (maxw <= 2) {
     switch (tb) {
-      case 4: return launch_k23_tb<S, KIND, 4, 2>(grid, smem, st, p);
-      case 8: return launch_k23_tb<S, KIND, 8, 2>(grid, smem, st, p);
-      case 16: return launch_k23_tb<S, KIND, 16, 2>(grid, smem, st, p);
+      case 4: return launch_k23_tb<S, KIND, 4, 2>(grid, threads, smem, st, p);
+      case 8: return launch_k23_tb<S, KIND, 8, 2>(grid, threads, smem, st, p);
+      case 16: return launch_k23_tb<S, KIND, 16, 2>(grid, threads, smem, st, p);
       default: return cudaErrorInvalidValue;
     }
   }
-  if (tb == 16) return launch_k23_tb<S, KIND, 16, 8>(grid, smem, st, p);
+  if (tb == 16) return launch_k23_tb<S, KIND, 16, 8>(grid, threads, smem, st, p);
   return cudaErrorInvalidValue;
 }
 
 #define D4K_INSTANTIATE_K23(KIND)                                                                  \
-  template cudaError_t launch_k23<float, KIND>(int, int, dim3, size_t, cudaStream_t,               \
+  template cudaError_t launch_k23<float, KIND>(int, int, dim3, int, size_t, cudaStream_t,          \
                                                const FitParams<float>&);                            \
-  template cudaError_t launch_k23<double, KIND>(int, int, dim3, size_t, cudaStream_t,              \
+  template cudaError_t launch_k23<double, KIND>(int, int, dim3, int, size_t, cudaStream_t,         \
                                                 const FitParams<double>&);
 
 }  // namespace d4k

@@ -216,6 +216,8 @@ def test_philox_noise_is_standard_normal_and_shard_invariant(gpu):
     np.testing.assert_array_equal(z[32:], z2)
     z3 = gpu.philox_noise(123, 49, 0, 64)
     assert not np.array_equal(z, z3)
+    big = gpu.philox_noise(7, 3, 0, 2048)  # 8.4M normals: finite, tails bounded by Box-Muller on 23-bit uniforms
+    assert np.isfinite(big).all() and np.abs(big).max() < 6.5
 
 
 def test_nonfinite_state_error_message(gpu):
