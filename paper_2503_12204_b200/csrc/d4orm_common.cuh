@@ -114,4 +114,47 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
   return d;
 }
 
+// ------------------------------------------------------------ Philox noise
+// Philox4x32-10 (Salmon et al., SC'11) + Box-Muller.  Noise of denoising step
+// i is keyed by keys[i] = mix_seed(seed_it, i).  For sample m and robot k the
+// normals form one sequence n = t·du + d (t < T, d < du); group g = n/4 is
+// Philox(counter = (g, m_lo, m_hi, k)), lanes n%4.  Each normal is a pure
+// function of (seed, i, m, k, t, d): identical under any sharding of samples,
+// and a rollout thread owning robot k draws its own stream with no redundancy.
+struct Philox {
+  static __device__ __forceinline__ uint4 round(uint4 c, uint2 k) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
+    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
+    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
+    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+  }
+  static __device__ __forceinline__ uint4 gen(uint4 c, uint2 k) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      c = round(c, k);
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+    return c;
+  }
+};
+
+__device__ __forceinline__ float u01_open(uint32_t x) {  // strictly inside (0, 1), exact in fp32
+  return ((float)(x >> 9) + 0.5f) * (1.0f / 8388608.0f);
+}
+
+__device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
+  const float v = -2.0f * __logf(u01_open(a));  // > 0
+  const float r = v * rsqrtf(v);
+  float s, c;
+  __sincosf(6.28318530717958647692f * u01_open(b), &s, &c);
+  return make_float2(r * c, r * s);
+}
+
+__device__ __forceinline__ float4 philox_normals(uint2 key, uint64_t m, uint32_t k, uint32_t g) {
+  const uint4 r = Philox::gen(make_uint4(g, (uint32_t)m, (uint32_t)(m >> 32), k), key);
+  const float2 a = box_muller(r.x, r.y), b = box_muller(r.z, r.w);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
 }  // namespace d4k

@@ -26,7 +26,7 @@
 
 namespace d4k {
 template <typename S, int KIND>
-cudaError_t launch_k23(int tb, int maxw, dim3 grid, int threads, size_t smem, cudaStream_t st,
+cudaError_t launch_k23(int tb, int maxw, int noise, dim3 grid, int threads, size_t smem, cudaStream_t st,
                        const FitParams<S>& p);
 }
 
@@ -310,16 +310,16 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
 }
 
 template <typename S>
-cudaError_t launch_fit(d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f, size_t smem) {
+cudaError_t launch_fit(d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f, size_t smem, bool fused) {
   const dim3 grid((unsigned)((f.M + ctx->spc - 1) / ctx->spc));
   const int th = ctx->spc * ctx->Rp;
   switch (ctx->prob.kind) {
-    case 0: return d4k::launch_k23<S, 0>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
-    case 1: return d4k::launch_k23<S, 1>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
-    case 2: return d4k::launch_k23<S, 2>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
-    case 3: return d4k::launch_k23<S, 3>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
-    case 4: return d4k::launch_k23<S, 4>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
-    default: return d4k::launch_k23<S, 5>(ctx->TB, ctx->MAXW, grid, th, smem, ctx->s_main, f);
+    case 0: return d4k::launch_k23<S, 0>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
+    case 1: return d4k::launch_k23<S, 1>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
+    case 2: return d4k::launch_k23<S, 2>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
+    case 3: return d4k::launch_k23<S, 3>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
+    case 4: return d4k::launch_k23<S, 4>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
+    default: return d4k::launch_k23<S, 5>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
   }
 }
 
@@ -388,17 +388,18 @@ int set_keys(d4orm_cuda_ctx* ctx, const RunShape& rs, uint64_t seed) {
   return D4ORM_OK;
 }
 
+// K1 standalone (fp64 path, FromScratch init, tests): count samples from m0.
 template <typename S>
-int launch_noise(d4orm_cuda_ctx* ctx, cudaStream_t st, int slot, const RunShape& rs, int step) {
-  const int64_t groups = (rs.E + 3) / 4;
-  const unsigned gx = (unsigned)((groups + d4k::kThreads - 1) / d4k::kThreads);
-  // ≈ 16 resident CTAs per SM worth of work in flight; grid.y strides samples
+int launch_noise(d4orm_cuda_ctx* ctx, cudaStream_t st, int64_t count, int64_t m0, int step, void* dst) {
+  const d4orm_problem& p = ctx->prob;
+  const int G = (p.horizon * p.du + 3) / 4;
+  const unsigned gx = (unsigned)((p.robots * G + d4k::kThreads - 1) / d4k::kThreads);
   int64_t gy = (148LL * 16 + gx - 1) / gx;
-  if (gy > rs.Ml) gy = rs.Ml;
+  if (gy > count) gy = count;
   if (gy > 65535) gy = 65535;
   if (gy < 1) gy = 1;
-  d4k::k_philox_noise<S><<<dim3(gx, (unsigned)gy), d4k::kThreads, 0, st>>>((S*)ctx->z[slot].p, rs.Ml, (int)rs.E,
-                                                                           rs.m0, ctx->keys.p, step);
+  d4k::k_philox_noise<S><<<dim3(gx, (unsigned)gy), d4k::kThreads, 0, st>>>((S*)dst, count, p.robots, p.horizon, p.du,
+                                                                           m0, ctx->keys.p, step);
   CU(cudaGetLastError());
   return D4ORM_OK;
 }
@@ -427,35 +428,33 @@ int host_noise(d4orm_cuda_ctx* ctx, const RunShape& rs, int step, int64_t m0, in
   return D4ORM_OK;
 }
 
-// Enqueue one denoising step i (z for step i already in z[slot]).  When
-// `next_noise_slot` >= 0, K1 for step `next_noise_step` is forked onto the noise
-// stream into that slot.
+// Enqueue one denoising step i.  philox: fp32 draws the noise inside K2+K3
+// (fused, z written once for K5); fp64 runs K1 first.  !philox: z for step i
+// is already in z[0] (host noise).
 template <typename S>
-int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, int slot, int next_noise_slot, int next_noise_step,
-                 bool timing) {
+int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, bool philox, bool timing) {
   const double ab_i = ctx->ab[i];
-  const double ms = 1.0 / std::sqrt(ab_i), sd = std::sqrt(1.0 / ab_i - 1.0);
+  const double sd = std::sqrt(1.0 / ab_i - 1.0);
   const double sab = std::sqrt(ctx->ab[i - 1]);
   const double next_ms = i > 1 ? 1.0 / std::sqrt(ctx->ab[i - 1]) : 0.0;
-  (void)ms;
   const bool f64 = std::is_same<S, double>::value;
+  const bool fused = philox && !f64;
   const int TC = f64 ? ctx->TC64 : ctx->TC32;
   const size_t smem = f64 ? ctx->smem64 : ctx->smem32;
   auto mark = [&](int k) -> int {
     if (timing) CU(cudaEventRecord(ctx->ev_k[k], ctx->s_main));
     return D4ORM_OK;
   };
-  if (next_noise_slot >= 0) {
-    CU(cudaEventRecord(ctx->ev_fork, ctx->s_main));
-    CU(cudaStreamWaitEvent(ctx->s_noise, ctx->ev_fork, 0));
-    if (int r = launch_noise<S>(ctx, ctx->s_noise, next_noise_slot, rs, next_noise_step)) return r;
-    CU(cudaEventRecord(ctx->ev_join, ctx->s_noise));
+  if (philox && !fused) {
+    if (int r = launch_noise<S>(ctx, ctx->s_main, rs.Ml, rs.m0, i, ctx->z[0].p)) return r;
   }
   if (int r = mark(0)) return r;
-  const d4k::FitParams<S> f = fit_params<S>(ctx, (const S*)ctx->z[slot].p, (const S*)ctx->base.p, (const S*)ctx->msv.p,
-                                            sd, rs.Ml, rs.m0, rs.N - i, ctx->rewards.p + rs.m0, nullptr, nullptr,
-                                            nullptr, TC);
-  CU(launch_fit<S>(ctx, f, smem));
+  d4k::FitParams<S> f = fit_params<S>(ctx, (const S*)ctx->z[0].p, (const S*)ctx->base.p, (const S*)ctx->msv.p, sd,
+                                      rs.Ml, rs.m0, rs.N - i, ctx->rewards.p + rs.m0, nullptr, nullptr, nullptr, TC);
+  f.keys = ctx->keys.p;
+  f.step = i;
+  f.z_store = (S*)ctx->z[0].p;
+  CU(launch_fit<S>(ctx, f, smem, fused));
   if (int r = mark(1)) return r;
   if (ctx->world > 1) {
     NC(g_nccl.AllGather(ctx->rewards.p + rs.m0, ctx->rewards.p, (size_t)rs.Ml, ncclFloat64, ctx->comm, ctx->s_main));
@@ -468,11 +467,11 @@ int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, int slot, int n
   const dim3 pgrid((unsigned)((rs.E + 4 * d4k::kThreads - 1) / (4 * d4k::kThreads)), (unsigned)rs.chunks_local);
   if (f64) {
     d4k::k_wmean_partial<S, double><<<pgrid, d4k::kThreads, 0, ctx->s_main>>>(
-        (const S*)ctx->z[slot].p, ctx->w64.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, kChunk,
+        (const S*)ctx->z[0].p, ctx->w64.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, kChunk,
         (S*)ctx->partial.p);
   } else {
     d4k::k_wmean_partial<S, float><<<pgrid, d4k::kThreads, 0, ctx->s_main>>>(
-        (const S*)ctx->z[slot].p, ctx->w32.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, kChunk,
+        (const S*)ctx->z[0].p, ctx->w32.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, kChunk,
         (S*)ctx->partial.p);
   }
   CU(cudaGetLastError());
@@ -497,7 +496,6 @@ int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, int slot, int n
   }
   CU(cudaGetLastError());
   if (int r = mark(4)) return r;
-  if (next_noise_slot >= 0) CU(cudaStreamWaitEvent(ctx->s_main, ctx->ev_join, 0));
   return D4ORM_OK;
 }
 
@@ -522,12 +520,9 @@ int prologue(d4orm_cuda_ctx* ctx, const RunShape& rs, const double* base_host, c
   if (rs.mode != D4ORM_DEFORMATION) {
     // FromScratch: variable ~ N(0, I) from stream (seed, 0, 0) (denoiser.cpp:141-145)
     if (philox) {
-      RunShape one = rs;
-      one.Ml = 1;
-      one.m0 = 0;
-      if (int r = launch_noise<S>(ctx, ctx->s_main, 1, one, 0)) return r;
+      if (int r = launch_noise<S>(ctx, ctx->s_main, 1, 0, 0, ctx->z[0].p)) return r;
       std::vector<S> tmp(E);
-      CU(cudaMemcpyAsync(tmp.data(), ctx->z[1].p, E * sizeof(S), cudaMemcpyDeviceToHost, ctx->s_main));
+      CU(cudaMemcpyAsync(tmp.data(), ctx->z[0].p, E * sizeof(S), cudaMemcpyDeviceToHost, ctx->s_main));
       CU(cudaStreamSynchronize(ctx->s_main));
       for (int64_t e = 0; e < E; ++e) v[e] = (double)tmp[e];
     } else {
@@ -540,18 +535,7 @@ int prologue(d4orm_cuda_ctx* ctx, const RunShape& rs, const double* base_host, c
   CU(init_msv<S>(ctx, E, 1.0 / std::sqrt(ctx->ab[rs.N])));
   const unsigned long long init = ~0ull;
   CU(cudaMemcpyAsync(ctx->errw.p, &init, sizeof init, cudaMemcpyHostToDevice, ctx->s_main));
-  if (philox) {
-    if (int r = launch_noise<S>(ctx, ctx->s_main, 0, rs, rs.N)) return r;
-  }
   return D4ORM_OK;
-}
-
-// Slot for K1 of the step after i (or of step N after step 1, for chained
-// benchmark passes), or -1 when that slot is still being read by step i.
-int next_noise_slot(const RunShape& rs, int i) {
-  const int slot = (rs.N - i) & 1;
-  if (i > 1) return slot ^ 1;
-  return slot == 1 ? 0 : -1;
 }
 
 std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
@@ -563,9 +547,9 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   return b;
 }
 
-// Per-step CUDA graphs for Philox mode (steady-state structure: z slot of step
-// i is (N-i)&1; K1 of the following step forked inside; step 1 forks K1(N) so
-// runs can be chained for benchmarking).
+// Per-step CUDA graphs for Philox mode (one graph per denoising index i; the
+// kernels read every per-run value — keys, base, variable — from device
+// memory, so the graphs are reused across runs of the same shape).
 template <typename S>
 int ensure_graphs(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   const std::string key = graph_key_of(ctx, rs);
@@ -574,12 +558,9 @@ int ensure_graphs(d4orm_cuda_ctx* ctx, const RunShape& rs) {
     if (g.exec) cudaGraphExecDestroy(g.exec);
   ctx->graphs.assign((size_t)rs.N + 1, StepGraph{});
   for (int i = rs.N; i >= 1; --i) {
-    const int slot = (rs.N - i) & 1;
-    const int next_step = i > 1 ? i - 1 : rs.N;
-    const int next_slot = next_noise_slot(rs, i);
     cudaGraph_t g;
     CU(cudaStreamBeginCapture(ctx->s_main, cudaStreamCaptureModeThreadLocal));
-    int r = enqueue_step<S>(ctx, rs, i, slot, next_slot, next_step, false);
+    int r = enqueue_step<S>(ctx, rs, i, true, false);
     cudaError_t e = cudaStreamEndCapture(ctx->s_main, &g);
     if (r) return r;
     CU(e);
@@ -593,16 +574,13 @@ int ensure_graphs(d4orm_cuda_ctx* ctx, const RunShape& rs) {
 template <typename S>
 int run_steps(d4orm_cuda_ctx* ctx, const RunShape& rs, bool philox, int i_begin, int i_end, const double* given_noise) {
   for (int i = i_begin; i >= i_end; --i) {
-    const int slot = philox ? (rs.N - i) & 1 : 0;
     if (!philox) {
       if (int r = host_noise(ctx, rs, i, rs.m0, rs.Ml, given_noise, ctx->z[0].p)) return r;
     }
     if (philox && ctx->use_graphs) {
       CU(cudaGraphLaunch(ctx->graphs[i].exec, ctx->s_main));
     } else {
-      const int next_step = i > 1 ? i - 1 : rs.N;
-      const int next_slot = philox ? next_noise_slot(rs, i) : -1;
-      if (int r = enqueue_step<S>(ctx, rs, i, slot, next_slot, next_step, false)) return r;
+      if (int r = enqueue_step<S>(ctx, rs, i, philox, false)) return r;
     }
   }
   return D4ORM_OK;
@@ -626,7 +604,7 @@ int run_denoising_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoise
   RunShape rs;
   if (int r = check_config(ctx, c, &rs)) return r;
   const bool philox = ctx->noise_source == D4ORM_NOISE_PHILOX;
-  if (int r = ensure_buffers(ctx, rs, philox)) return r;
+  if (int r = ensure_buffers(ctx, rs, false)) return r;
   if (int r = prologue<S>(ctx, rs, base, c, philox)) return r;
   if (philox && ctx->use_graphs) {
     if (int r = ensure_graphs<S>(ctx, rs)) return r;
@@ -794,10 +772,8 @@ int denoise_step_t(d4orm_cuda_ctx* ctx, const double* base, const double* var_in
   if (int r = set_keys(ctx, rs, c->seed)) return r;
   if (noise) {
     if (int r = host_noise(ctx, rs, i, rs.m0, rs.Ml, noise + (size_t)rs.m0 * E, ctx->z[0].p)) return r;
-  } else {
-    if (int r = launch_noise<S>(ctx, ctx->s_main, 0, rs, i)) return r;
   }
-  if (int r = enqueue_step<S>(ctx, rs, i, 0, -1, 0, false)) return r;
+  if (int r = enqueue_step<S>(ctx, rs, i, noise == nullptr, false)) return r;
   CU(cudaStreamSynchronize(ctx->s_main));
   if (int r = check_err(ctx, rs)) return r;
   if (var_out) CU(cudaMemcpy(var_out, ctx->var.p, sizeof(double) * E, cudaMemcpyDeviceToHost));
@@ -849,7 +825,7 @@ int rollout_fitness_t(d4orm_cuda_ctx* ctx, const double* u, int64_t count, doubl
   const d4k::FitParams<S> f = fit_params<S>(ctx, (const S*)ctx->z[0].p, (const S*)ctx->base.p, (const S*)ctx->msv.p,
                                             1.0, count, 0, 0, ctx->rewards.p, ctx->counts.p, (S*)ctx->states_out.p,
                                             (S*)ctx->controls_out.p, f64 ? ctx->TC64 : ctx->TC32);
-  CU(launch_fit<S>(ctx, f, f64 ? ctx->smem64 : ctx->smem32));
+  CU(launch_fit<S>(ctx, f, f64 ? ctx->smem64 : ctx->smem32, false));
   CU(cudaStreamSynchronize(ctx->s_main));
   unsigned long long e = 0;
   CU(cudaMemcpy(&e, ctx->errw.p, sizeof e, cudaMemcpyDeviceToHost));
@@ -925,13 +901,16 @@ int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_
   CU(ctx->z[0].ensure((size_t)count * rs.E * sizeof(float)));
   CU(ctx->keys.ensure((size_t)step + 1));
   if (int r = set_keys(ctx, rs, seed)) return r;
-  if (int r = launch_noise<float>(ctx, ctx->s_main, 0, rs, step)) return r;
+  if (int r = launch_noise<float>(ctx, ctx->s_main, count, m0, step, ctx->z[0].p)) return r;
   CU(cudaStreamSynchronize(ctx->s_main));
   CU(cudaMemcpy(out, ctx->z[0].p, sizeof(float) * count * rs.E, cudaMemcpyDeviceToHost));
   return D4ORM_OK;
 }
 
-int d4orm_cuda_launches_per_step(const d4orm_cuda_ctx* ctx) { return ctx->world > 1 ? 6 : 5; }
+int d4orm_cuda_launches_per_step(const d4orm_cuda_ctx* ctx) {
+  // K2+K3, K4, K5 partial, K5 tree (+ K1 on the fp64 path, + the root tree when sharded)
+  return 4 + (ctx->precision == D4ORM_PREC_F64 ? 1 : 0) + (ctx->world > 1 ? 1 : 0);
+}
 
 extern "C++" template <typename S>
 int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* c, int warmup, int steps,
@@ -939,7 +918,7 @@ int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config
   RunShape rs;
   if (int r = check_config(ctx, c, &rs)) return r;
   if (ctx->noise_source != D4ORM_NOISE_PHILOX) return fail(ctx, D4ORM_E_INVALID, "bench requires Philox noise");
-  if (int r = ensure_buffers(ctx, rs, true)) return r;
+  if (int r = ensure_buffers(ctx, rs, false)) return r;
   if (int r = prologue<S>(ctx, rs, base, c, true)) return r;
   if (ctx->use_graphs) {
     if (int r = ensure_graphs<S>(ctx, rs)) return r;
@@ -948,9 +927,6 @@ int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config
   auto run_range = [&](int j0, int count) -> int {
     for (int j = j0; j < j0 + count; ++j) {
       const int i = rs.N - (j % rs.N);
-      if (i == rs.N && j > 0 && next_noise_slot(rs, 1) < 0) {
-        if (int r = launch_noise<S>(ctx, ctx->s_main, 0, rs, rs.N)) return r;
-      }
       if (int r = run_steps<S>(ctx, rs, true, i, i, nullptr)) return r;
     }
     return D4ORM_OK;
@@ -966,18 +942,16 @@ int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config
   *ms_total = ms;
   if (int r = check_err(ctx, rs)) return r;
   if (kernel_ms) {
-    // Instrumented pass (eager launches with events between kernels, K1 on
-    // the main stream so its time is attributable).
+    // Instrumented pass: eager launches with CUDA events between the kernels
+    // on the context's stream.
     double acc[5] = {0, 0, 0, 0, 0};
     cudaEvent_t e0;
     CU(cudaEventCreate(&e0));
     const int reps = steps < 1 ? 1 : steps;
     for (int j = 0; j < reps; ++j) {
       const int i = rs.N - ((warmup + steps + j) % rs.N);
-      const int slot = (rs.N - i) & 1;
       CU(cudaEventRecord(e0, ctx->s_main));
-      if (int r = launch_noise<S>(ctx, ctx->s_main, slot ^ 1, rs, i > 1 ? i - 1 : rs.N)) return r;
-      if (int r = enqueue_step<S>(ctx, rs, i, slot, -1, 0, true)) return r;
+      if (int r = enqueue_step<S>(ctx, rs, i, true, true)) return r;
       CU(cudaEventSynchronize(ctx->ev_k[4]));
       float t[5];
       CU(cudaEventElapsedTime(&t[0], e0, ctx->ev_k[0]));

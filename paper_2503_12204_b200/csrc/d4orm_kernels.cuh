@@ -19,59 +19,29 @@ namespace d4k {
 constexpr int kThreads = 256;
 
 // ------------------------------------------------------------------ K1 noise
-// Philox4x32-10 (Salmon et al., SC'11).  Key = mix_seed(seed_it, i) (64 bit);
-// counter = (group q, global sample m lo, m hi, 0).  Every normal is a pure
-// function of (seed, i, m, element), so any sharding of samples across GPUs
-// sees identical noise.
-struct Philox {
-  static __device__ __forceinline__ uint4 round(uint4 c, uint2 k) {
-    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
-    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
-    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
-  }
-  static __device__ __forceinline__ uint4 gen(uint4 c, uint2 k) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-      c = round(c, k);
-      k.x += 0x9E3779B9u;
-      k.y += 0xBB67AE85u;
-    }
-    return c;
-  }
-};
-
-__device__ __forceinline__ float u01_open(uint32_t x) {  // strictly inside (0, 1), exact in fp32
-  return ((float)(x >> 9) + 0.5f) * (1.0f / 8388608.0f);
-}
-
-__device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
-  const float v = -2.0f * __logf(u01_open(a));  // > 0
-  const float r = v * rsqrtf(v);
-  float s, c;
-  __sincosf(6.28318530717958647692f * u01_open(b), &s, &c);
-  return make_float2(r * c, r * s);
-}
-
-// grid.x covers the 4-element groups of one sample, grid.y strides samples.
+// Standalone Philox generator (d4orm_common.cuh for the counter mapping):
+// thread = (robot k, group g) of one sample row; grid.y strides samples.  The
+// fp32 hot path draws the same normals inside K2+K3 instead (fused), so this
+// kernel serves the fp64 path, tests and d4orm_cuda_philox_noise.
 template <typename S>
-__global__ void __launch_bounds__(kThreads) k_philox_noise(S* __restrict__ z, int64_t count, int elems,
+__global__ void __launch_bounds__(kThreads) k_philox_noise(S* __restrict__ z, int64_t count, int R, int T, int DU,
                                                            int64_t m0, const uint2* __restrict__ keys, int step) {
   const uint2 key = keys[step];
-  const int groups = (elems + 3) >> 2;
-  const int q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= groups) return;
+  const int G = (T * DU + 3) >> 2;  // groups per robot
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= R * G) return;
+  const int k = idx / G, g = idx - k * G;
   for (int64_t ml = blockIdx.y; ml < count; ml += gridDim.y) {
-    const uint64_t m = (uint64_t)(m0 + ml);
-    const uint4 r = Philox::gen(make_uint4((uint32_t)q, (uint32_t)m, (uint32_t)(m >> 32), 0u), key);
-    const float2 a = box_muller(r.x, r.y), b = box_muller(r.z, r.w);
-    S* out = z + ml * elems + 4 * q;
-    if (std::is_same<S, float>::value && (elems & 3) == 0) {
-      __stcs(reinterpret_cast<float4*>(out), make_float4(a.x, a.y, b.x, b.y));
-    } else {
-      const float v[4] = {a.x, a.y, b.x, b.y};
-      const int n = elems - 4 * q < 4 ? elems - 4 * q : 4;
-      for (int j = 0; j < n; ++j) out[j] = (S)v[j];
+    const float4 v = philox_normals(key, (uint64_t)(m0 + ml), (uint32_t)k, (uint32_t)g);
+    const float vv[4] = {v.x, v.y, v.z, v.w};
+    S* row = z + ml * (int64_t)T * R * DU;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = 4 * g + j;
+      if (n < T * DU) {
+        const int t = n / DU, d = n - t * DU;
+        row[((int64_t)t * R + k) * DU + d] = (S)vv[j];
+      }
     }
   }
 }

@@ -52,6 +52,10 @@ struct FitParams {
   S* states_out;         // [M][T+1][R][dx] or null
   S* controls_out;       // [M][T+1][R][du] or null
   unsigned long long* err;
+  // fused-noise mode (NOISE == 1): Philox key table, this step, z written for K5
+  const uint2* keys;
+  int step;
+  S* z_store;            // [M][T][R][du]
 };
 
 template <typename S>
@@ -298,7 +302,7 @@ __device__ __forceinline__ double item_f64(const FitSmem<double>& sm, int s, int
   return g;
 }
 
-template <typename S, int KIND, int TB, int MAXW>
+template <typename S, int KIND, int TB, int MAXW, int NOISE>
 __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const FitParams<S> p) {
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
   constexpr bool F32 = std::is_same<S, float>::value;
@@ -361,11 +365,15 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
   double effort = 0.0;
   bool bad = false;
 
-  // prefetch ring: noise (HBM stream) + base/mean-scaled variable (L2-resident);
-  // chunk-local, so it is dead (no registers) during the fitness phase
+  // NOISE == 0: prefetch ring over the HBM noise stream + base/mean-scaled
+  // variable (L2-resident).  NOISE == 1: the noise is drawn here in registers
+  // (Philox, d4orm_common.cuh) block by block and written once for K5.  Both
+  // are chunk-local, so they hold no registers during the fitness phase.
   S zq[kPF][DU], bq[kPF][DU], mq[kPF][F32 ? 1 : DU];
+  S* zst = NOISE == 1 ? p.z_store + (liveA ? mA : 0) * (int64_t)T * R * DU : nullptr;
+  const uint2 key = NOISE == 1 ? p.keys[p.step] : make_uint2(0u, 0u);
   auto fetch = [&](int t, int t_end, int slot) {
-    if (robotA && t < t_end) {
+    if (NOISE == 0 && robotA && t < t_end) {
       const int64_t e = ((int64_t)t * R + kA) * DU;
 #pragma unroll
       for (int d = 0; d < DU; ++d) {
@@ -397,6 +405,37 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
 #pragma unroll
       for (int j = 0; j < kPF; ++j) fetch(t0 + j, t_end, j);
       for (int tc = 0; tc < TC; tc += kPF) {
+        if constexpr (NOISE == 1) {
+          // base+msv loads for the block first; the Philox draws hide their latency
+#pragma unroll
+          for (int j = 0; j < kPF; ++j) {
+            const int t = t0 + tc + j;
+            if (t < T) {
+#pragma unroll
+              for (int d = 0; d < DU; ++d) bq[j][d] = __ldg(p.bm + ((int64_t)t * R + kA) * DU + d);
+            }
+          }
+          const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
+          float nz[kPF * DU];
+#pragma unroll
+          for (int g = 0; g < kPF * DU / 4; ++g) {
+            const float4 v = philox_normals(key, (uint64_t)(p.m_global0 + mA), (uint32_t)kA, g0 + g);
+            nz[4 * g] = v.x;
+            nz[4 * g + 1] = v.y;
+            nz[4 * g + 2] = v.z;
+            nz[4 * g + 3] = v.w;
+          }
+#pragma unroll
+          for (int j = 0; j < kPF; ++j) {
+            const int t = t0 + tc + j;
+#pragma unroll
+            for (int d = 0; d < DU; ++d) zq[j][d] = (S)nz[j * DU + d];
+            if (t < T) {
+#pragma unroll
+              for (int d = 0; d < DU; ++d) __stcs(zst + ((int64_t)t * R + kA) * DU + d, zq[j][d]);
+            }
+          }
+        }
 #pragma unroll
         for (int j = 0; j < kPF; ++j) {
           const int t = t0 + tc + j;

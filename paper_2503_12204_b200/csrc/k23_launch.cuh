@@ -1,40 +1,52 @@
 // k23_launch.cuh — launch glue for the fused rollout+fitness kernel (K2+K3).
 // Instantiated per model kind in k23_k<kind>.cu so the 6 kinds × {f32,f64} ×
-// robot-tile variants compile in parallel.
+// robot-tile × noise-source variants compile in parallel.  Fused Philox noise
+// (NOISE=1) exists for fp32 only; the fp64 parity path reads z from HBM.
 #pragma once
 
 #include "d4orm_kernels.cuh"
 
 namespace d4k {
 
-template <typename S, int KIND, int TB, int MAXW>
+template <typename S, int KIND, int TB, int MAXW, int NOISE>
 cudaError_t launch_k23_tb(dim3 grid, int threads, size_t smem, cudaStream_t st, const FitParams<S>& p) {
-  auto fn = k_rollout_fitness<S, KIND, TB, MAXW>;
+  auto fn = k_rollout_fitness<S, KIND, TB, MAXW, NOISE>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   fn<<<grid, threads, smem, st>>>(p);
   return cudaGetLastError();
 }
 
-template <typename S, int KIND>
-cudaError_t launch_k23(int tb, int maxw, dim3 grid, int threads, size_t smem, cudaStream_t st,
-                       const FitParams<S>& p) {
+template <typename S, int KIND, int NOISE>
+cudaError_t launch_k23_n(int tb, int maxw, dim3 grid, int threads, size_t smem, cudaStream_t st,
+                         const FitParams<S>& p) {
   if (maxw <= 2) {
     switch (tb) {
-      case 4: return launch_k23_tb<S, KIND, 4, 2>(grid, threads, smem, st, p);
-      case 8: return launch_k23_tb<S, KIND, 8, 2>(grid, threads, smem, st, p);
-      case 16: return launch_k23_tb<S, KIND, 16, 2>(grid, threads, smem, st, p);
+      case 4: return launch_k23_tb<S, KIND, 4, 2, NOISE>(grid, threads, smem, st, p);
+      case 8: return launch_k23_tb<S, KIND, 8, 2, NOISE>(grid, threads, smem, st, p);
+      case 16: return launch_k23_tb<S, KIND, 16, 2, NOISE>(grid, threads, smem, st, p);
       default: return cudaErrorInvalidValue;
     }
   }
-  if (tb == 16) return launch_k23_tb<S, KIND, 16, 8>(grid, threads, smem, st, p);
+  if (tb == 16) return launch_k23_tb<S, KIND, 16, 8, NOISE>(grid, threads, smem, st, p);
   return cudaErrorInvalidValue;
 }
 
+template <typename S, int KIND>
+cudaError_t launch_k23(int tb, int maxw, int noise, dim3 grid, int threads, size_t smem, cudaStream_t st,
+                       const FitParams<S>& p) {
+  if constexpr (std::is_same<S, float>::value) {
+    if (noise) return launch_k23_n<S, KIND, 1>(tb, maxw, grid, threads, smem, st, p);
+  } else {
+    if (noise) return cudaErrorInvalidValue;
+  }
+  return launch_k23_n<S, KIND, 0>(tb, maxw, grid, threads, smem, st, p);
+}
+
 #define D4K_INSTANTIATE_K23(KIND)                                                                  \
-  template cudaError_t launch_k23<float, KIND>(int, int, dim3, int, size_t, cudaStream_t,          \
+  template cudaError_t launch_k23<float, KIND>(int, int, int, dim3, int, size_t, cudaStream_t,     \
                                                const FitParams<float>&);                            \
-  template cudaError_t launch_k23<double, KIND>(int, int, dim3, int, size_t, cudaStream_t,         \
+  template cudaError_t launch_k23<double, KIND>(int, int, int, dim3, int, size_t, cudaStream_t,    \
                                                 const FitParams<double>&);
 
 }  // namespace d4k

@@ -211,6 +211,9 @@ def test_philox_noise_is_standard_normal_and_shard_invariant(gpu):
     gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX)
     gpu.set_problem(p)
     z = gpu.philox_noise(123, 50, 0, 64)
+    # K1 and the fused in-rollout draw are the same function: run one fp32
+    # Philox step and one fp64 step (K1) with identical inputs → same rewards
+    # up to fp32 rounding
     assert abs(z.mean()) < 0.01 and abs(z.std() - 1) < 0.01
     z2 = gpu.philox_noise(123, 50, 32, 32)
     np.testing.assert_array_equal(z[32:], z2)
@@ -241,3 +244,25 @@ def test_invalid_arguments(gpu):
     bad = S.Problem(S.HOLO2D, starts=[[0, 0, 0, 0]], goals=[[0, 0]], horizon=3)
     with pytest.raises(ValueError, match="starts on its goal"):
         gpu.set_problem(bad)
+
+
+@pytest.mark.parametrize("case", ["C2", "C3", "C4"])
+def test_fused_philox_equals_k1_noise(gpu, case):
+    """The fp32 hot path draws its noise inside K2+K3; feeding K1's output for
+    the same (seed, step) through the host-noise path must give bitwise the
+    same rewards, weights and updated variable."""
+    p = CASES[case]()
+    M, N, i, seed = 512, 10, 6, 21
+    cfg = d4.DenoiserConfig(steps=N, batch=M, seed=seed)
+    base = controls_for(p, 1, 8, scale=0.3)[0]
+    var = 0.1 * np.random.default_rng(1).normal(size=base.shape)
+    gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX)
+    gpu.set_problem(p)
+    v1, r1, w1, _ = gpu.denoise_step(base, var, i, cfg, None)
+    key_seed = seed
+    z = gpu.philox_noise(key_seed, i, 0, M).astype(np.float64)
+    gpu.set_options(d4.PREC_F32, d4.NOISE_HOST)
+    v2, r2, w2, _ = gpu.denoise_step(base, var, i, cfg, z)
+    np.testing.assert_array_equal(r1, r2)
+    np.testing.assert_array_equal(w1, w2)
+    np.testing.assert_array_equal(v1, v2)
