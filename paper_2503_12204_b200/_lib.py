@@ -6,12 +6,13 @@ is visible, every call raises.  PyTorch is not needed on this path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libd4orm_b200.so"
+LIB_PATH = Path(os.environ.get("D4ORM_LIB", str(_PKG / "libd4orm_b200.so")))
 
 D4ORM_OK, D4ORM_E_INVALID, D4ORM_E_RUNTIME, D4ORM_E_CUDA, D4ORM_E_NCCL, D4ORM_E_UNSUPPORTED = range(6)
 PREC_F32, PREC_F64 = 0, 1

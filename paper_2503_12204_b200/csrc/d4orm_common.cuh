@@ -93,6 +93,11 @@ __device__ __forceinline__ uint64_t pack2(float a, float b) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
   return r;
 }
+__device__ __forceinline__ float sqrt_approx(float x) {  // MUFU.SQRT (fp32 throughput path)
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float((uint32_t)v); }
 __device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
 __device__ __forceinline__ uint32_t lo32(uint64_t v) { return (uint32_t)v; }
@@ -123,10 +128,11 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
 // and a rollout thread owning robot k draws its own stream with no redundancy.
 struct Philox {
   static __device__ __forceinline__ uint4 round(uint4 c, uint2 k) {
-    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u;
-    const uint32_t hi0 = __umulhi(M0, c.x), lo0 = M0 * c.x;
-    const uint32_t hi1 = __umulhi(M1, c.z), lo1 = M1 * c.z;
-    return make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    // one IMAD.WIDE.U32 per 32x32→64 product (hi and lo together)
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    return make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k.x, (uint32_t)p1, (uint32_t)(p0 >> 32) ^ c.w ^ k.y,
+                      (uint32_t)p0);
   }
   static __device__ __forceinline__ uint4 gen(uint4 c, uint2 k) {
 #pragma unroll
@@ -139,8 +145,10 @@ struct Philox {
   }
 };
 
-__device__ __forceinline__ float u01_open(uint32_t x) {  // strictly inside (0, 1), exact in fp32
-  return ((float)(x >> 9) + 0.5f) * (1.0f / 8388608.0f);
+// (2k+1)·2^-24 for k = x >> 9: strictly inside (0, 1) and exact.  Built from the
+// bits as [1,2) − (1 − 2^-24): one LOP3 + one FADD.
+__device__ __forceinline__ float u01_open(uint32_t x) {
+  return __uint_as_float((x >> 9) | 0x3f800000u) - 0.99999994039535522461f;
 }
 
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {

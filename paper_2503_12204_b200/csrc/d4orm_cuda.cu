@@ -514,6 +514,19 @@ int prologue(d4orm_cuda_ctx* ctx, const RunShape& rs, const double* base_host, c
   const int64_t E = rs.E;
   std::vector<double> b(E, 0.0);
   if (rs.mode == D4ORM_DEFORMATION) std::memcpy(b.data(), base_host, sizeof(double) * E);
+  if (!std::is_same<S, double>::value) {
+    // NaN in base reaches every sample's rollout (denoiser.cpp:158-160) and the
+    // reference fails on the first robot/step that sees it; the fp32 FMNMX clamp
+    // would absorb it, so report it here (sample 0 is the first to fail).
+    const d4orm_problem& pp = ctx->prob;
+    for (int k = 0; k < pp.robots; ++k)
+      for (int t = 0; t < pp.horizon; ++t)
+        for (int d = 0; d < pp.du; ++d)
+          if (std::isnan(b[((int64_t)t * pp.robots + k) * pp.du + d]))
+            return fail(ctx, D4ORM_E_RUNTIME,
+                        "run_denoising: sample 0 at step %d: rollout: non-finite state for robot %d at step %d", rs.N,
+                        k, t + 1);
+  }
   CU((upload_as<S>(ctx->base, b.data(), E, ctx->s_main)));
   if (int r = set_keys(ctx, rs, c->seed)) return r;
   std::vector<double> v(E, 0.0);
@@ -819,6 +832,19 @@ int rollout_fitness_t(d4orm_cuda_ctx* ctx, const double* u, int64_t count, doubl
   CU(cudaMemsetAsync(ctx->controls_out.p, 0, count * NC * sizeof(S), ctx->s_main));
   const unsigned long long init = ~0ull;
   CU(cudaMemcpyAsync(ctx->errw.p, &init, sizeof init, cudaMemcpyHostToDevice, ctx->s_main));
+  if (!std::is_same<S, double>::value) {
+    // fp32 clamps with FMNMX, which would absorb a NaN control; the reference
+    // propagates it to a non-finite state — report that exactly here.
+    const d4orm_problem& pp = ctx->prob;
+    for (int64_t m = 0; m < count; ++m)
+      for (int k = 0; k < pp.robots; ++k)
+        for (int t = 0; t < pp.horizon; ++t)
+          for (int d = 0; d < pp.du; ++d)
+            if (std::isnan(u[m * E + ((int64_t)t * pp.robots + k) * pp.du + d]))
+              return fail(ctx, D4ORM_E_RUNTIME,
+                          "batch_rollout: member %lld: rollout: non-finite state for robot %d at step %d",
+                          (long long)m, k, t + 1);
+  }
   CU((upload_as<S>(ctx->z[0], u, (size_t)count * E, ctx->s_main)));
   const bool f64 = std::is_same<S, double>::value;
   // candidate = base(0) + (msv(0) + 1*u) = u exactly

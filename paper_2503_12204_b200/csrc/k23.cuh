@@ -63,7 +63,7 @@ struct FitSmem {
   S* pos;     // [PD][spc][TC][RS]
   S* goal;    // [PD][Rp]  fp32: −goal ; fp64: goal
   S* inv;     // [Rp]
-  S* one;     // [Rp]      1 valid / 0 padding
+  // (inv is [2·Rp]: (1/‖s−g‖ or ‖s−g‖, valid) pairs)
   S* obs;     // [O][4]
   double* red;   // [nthreads]
   double* eff;   // [nthreads]
@@ -146,8 +146,7 @@ __device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int t
   for (int a = 0; a < ntiles; ++a) {
     PackedTile<PD, TB> A;
     A.load(X, Y, Z, a * TB);
-    // ---- goal (reward.cpp:92-97) and obstacle (reward.cpp:112-125) terms
-    uint32_t om = 0;
+    // ---- goal terms (reward.cpp:92-97)
 #pragma unroll
     for (int j = 0; j < TB / 2; ++j) {
       const int k = a * TB + 2 * j;
@@ -160,19 +159,37 @@ __device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int t
         const uint64_t gz = *reinterpret_cast<const uint64_t*>(sm.goal + 2 * sm.Rp + k);
         d2 = ffma2_sq(fadd2(A.z[j], gz), d2);
       }
-      gacc += fmaf(-sqrtf(lo_f(d2)), sm.inv[k], sm.one[k]);
-      gacc += fmaf(-sqrtf(hi_f(d2)), sm.inv[k + 1], sm.one[k + 1]);
-      uint64_t oacc = 0;
-      for (int o = 0; o < n_obs; ++o) {
-        const float4 ob = *reinterpret_cast<const float4*>(sm.obs + 4 * o);  // −cx, −cy, −cz, −L²↑
-        const uint64_t ox = fadd2_b(ob.x, A.x[j]);
-        const uint64_t oy = fadd2_b(ob.y, A.y[j]);
-        uint64_t t = ffma2_sq(oy, pack2(ob.w, ob.w));
-        if constexpr (PD == 3) t = ffma2_sq(fadd2_b(ob.z, A.z[j]), t);
-        oacc |= ffma2_sq(ox, t);
-      }
-      om |= ((lo32(oacc) >> 31) | ((hi32(oacc) >> 31) << 1)) << (2 * j);
+      const float2 io0 = *reinterpret_cast<const float2*>(sm.inv + 2 * k);  // (1/‖s−g‖, valid)
+      const float2 io1 = *reinterpret_cast<const float2*>(sm.inv + 2 * k + 2);
+      gacc += fmaf(-sqrt_approx(lo_f(d2)), io0.x, io0.y);
+      gacc += fmaf(-sqrt_approx(hi_f(d2)), io1.x, io1.y);
     }
+    // ---- obstacle terms (reward.cpp:112-125): obstacles outer, the tile's
+    // robot pairs inner (independent chains), two obstacles per pass
+    uint32_t olo[TB / 2], ohi[TB / 2];
+#pragma unroll
+    for (int j = 0; j < TB / 2; ++j) olo[j] = ohi[j] = 0;
+    for (int o = 0; o < n_obs; o += 2) {
+      const float4 b0 = *reinterpret_cast<const float4*>(sm.obs + 4 * o);  // −cx, −cy, −cz, −L²↑
+      const float4 b1 = *reinterpret_cast<const float4*>(sm.obs + 4 * o + 4);  // padded: never hits
+      const uint64_t l0 = pack2(b0.w, b0.w), l1 = pack2(b1.w, b1.w);
+#pragma unroll
+      for (int j = 0; j < TB / 2; ++j) {
+        uint64_t t0 = ffma2_sq(fadd2_b(b0.y, A.y[j]), l0);
+        uint64_t t1 = ffma2_sq(fadd2_b(b1.y, A.y[j]), l1);
+        if constexpr (PD == 3) {
+          t0 = ffma2_sq(fadd2_b(b0.z, A.z[j]), t0);
+          t1 = ffma2_sq(fadd2_b(b1.z, A.z[j]), t1);
+        }
+        t0 = ffma2_sq(fadd2_b(b0.x, A.x[j]), t0);
+        t1 = ffma2_sq(fadd2_b(b1.x, A.x[j]), t1);
+        olo[j] |= lo32(t0) | lo32(t1);
+        ohi[j] |= hi32(t0) | hi32(t1);
+      }
+    }
+    uint32_t om = 0;
+#pragma unroll
+    for (int j = 0; j < TB / 2; ++j) om |= ((olo[j] >> 31) | ((ohi[j] >> 31) << 1)) << (2 * j);
     const int kv = R - a * TB;  // valid robots in this tile
     no += __popc(kv >= 32 ? om : (om & ((1u << (kv > 0 ? kv : 0)) - 1u)));
     // ---- pairs inside tile A
@@ -265,7 +282,7 @@ __device__ __forceinline__ double item_f64(const FitSmem<double>& sm, int s, int
       d = __dadd_rn(Z[k], -sm.goal[2 * sm.Rp + k]);
       gsq = __dadd_rn(gsq, __dmul_rn(d, d));
     }
-    g = __dadd_rn(g, __dadd_rn(1.0, -(sqrt(gsq) / sm.inv[k])));
+    g = __dadd_rn(g, __dadd_rn(1.0, -(sqrt(gsq) / sm.inv[2 * k])));
     for (int l = 0; l < R; ++l) {
       if (l == k) continue;
       double s2 = 0.0;
@@ -302,6 +319,132 @@ __device__ __forceinline__ double item_f64(const FitSmem<double>& sm, int s, int
   return g;
 }
 
+// ------------------------------------------------- fp32 fused rollout (phase A)
+// One robot's `nsteps` steps of a chunk: the block's base+msv loads are issued
+// first, the Philox draws (in registers) hide their latency, z is written once
+// for K5, then the RK4 steps run; positions go to the chunk's shared rows.
+// Pointers advance by a stride per step (no per-step 64-bit index math).  The
+// returned value is 0 unless some state went non-finite (NaN/inf propagate
+// through fma(x, 0, acc)); the caller then replays the chunk exactly.
+template <int KIND, bool FULL>
+__device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, const float* bmp, float* zp, int RDU,
+                                            uint64_t m, int kA, uint32_t g0, uint2 key, float* px, float* py, float* pz,
+                                            int RS, float* x, float& eff32, float& chk) {
+  constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
+  float bq[kPF][DU];
+#pragma unroll
+  for (int j = 0; j < kPF; ++j) {
+    if (FULL || j < nb) {
+      if constexpr (DU == 2) {
+        const float2 v = __ldg(reinterpret_cast<const float2*>(bmp + j * RDU));
+        bq[j][0] = v.x;
+        bq[j][1] = v.y;
+      } else {
+#pragma unroll
+        for (int d = 0; d < DU; ++d) bq[j][d] = __ldg(bmp + j * RDU + d);
+      }
+    }
+  }
+  float nz[kPF * DU];
+#pragma unroll
+  for (int g = 0; g < kPF * DU / 4; ++g) {
+    const float4 v = philox_normals(key, m, (uint32_t)kA, g0 + g);
+    nz[4 * g] = v.x;
+    nz[4 * g + 1] = v.y;
+    nz[4 * g + 2] = v.z;
+    nz[4 * g + 3] = v.w;
+  }
+#pragma unroll
+  for (int j = 0; j < kPF; ++j) {
+    if (FULL || j < nb) {
+      if constexpr (DU == 2) {
+        __stcs(reinterpret_cast<float2*>(zp + j * RDU), make_float2(nz[2 * j], nz[2 * j + 1]));
+      } else {
+#pragma unroll
+        for (int d = 0; d < DU; ++d) __stcs(zp + j * RDU + d, nz[j * DU + d]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kPF; ++j) {
+    if (FULL || j < nb) {
+      float u[DU];
+#pragma unroll
+      for (int d = 0; d < DU; ++d) {
+        // base + (mean_scale·var + std·z), clamped; FMNMX equals cwiseMax/Min
+        // here because NaN inputs are rejected on the host before launch
+        u[d] = fminf(fmaxf(fmaf(p.sd, nz[j * DU + d], bq[j][d]), p.lower[d]), p.upper[d]);
+        eff32 = fmaf(u[d], u[d], eff32);
+      }
+      rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
+      float s = x[0];
+#pragma unroll
+      for (int q = 1; q < DX; ++q) s += x[q];
+      chk = fmaf(s, 0.f, chk);
+      px[j * RS] = x[0];
+      py[j * RS] = x[1];
+      if constexpr (PD == 3) pz[j * RS] = x[2];
+    }
+  }
+}
+
+template <int KIND>
+__device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const FitSmem<float>& sm, int sA, int kA,
+                                               int64_t m, int t0, int nsteps, float* x, float* zrow, uint2 key,
+                                               float& eff32) {
+  constexpr int DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
+  const int RDU = p.R * DU;
+  const int64_t e0 = ((int64_t)t0 * p.R + kA) * DU;
+  const float* bmp = p.bm + e0;
+  float* zp = zrow + e0;
+  float* px = sm.row(0, sA, 0) + kA;
+  float* py = sm.row(1, sA, 0) + kA;
+  float* pz = PD == 3 ? sm.row(2, sA, 0) + kA : px;
+  const int RS = sm.RS;
+  float chk = 0.f;
+  for (int tc = 0; tc < nsteps; tc += kPF) {
+    const int nb = nsteps - tc;
+    const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
+    if (nb >= kPF) {
+      fused_block<KIND, true>(p, kPF, bmp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk);
+    } else {
+      fused_block<KIND, false>(p, nb, bmp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk);
+    }
+    bmp += kPF * RDU;
+    zp += kPF * RDU;
+    px += kPF * RS;
+    py += kPF * RS;
+    pz += kPF * RS;
+  }
+  return chk;
+}
+
+// Exact replay of a chunk whose states went non-finite (rare): the same
+// controls from the stored z, first failing (robot, step) reported as in
+// dynamics.cpp:81-84.
+template <int KIND>
+__device__ __noinline__ void rollout_check(const FitParams<float>& p, int kA, int64_t m, int t0, int nsteps,
+                                           const float* x_in, const float* zrow) {
+  constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU;
+  float x[DX];
+  for (int q = 0; q < DX; ++q) x[q] = x_in[q];
+  for (int tc = 0; tc < nsteps; ++tc) {
+    const int t = t0 + tc;
+    const int64_t e = ((int64_t)t * p.R + kA) * DU;
+    float u[DU];
+    for (int d = 0; d < DU; ++d) u[d] = fminf(fmaxf(fmaf(p.sd, zrow[e + d], p.bm[e + d]), p.lower[d]), p.upper[d]);
+    rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
+    bool fin = true;
+    for (int q = 0; q < DX; ++q) fin = fin && isfinite(x[q]);
+    if (!fin) {
+      const unsigned long long key = ((unsigned long long)p.step_key << 52) | ((unsigned long long)m << 20) |
+                                     ((unsigned long long)kA << 10) | (unsigned long long)(t + 1);
+      atomicMin(p.err, key);
+      return;
+    }
+  }
+}
+
 template <typename S, int KIND, int TB, int MAXW, int NOISE>
 __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const FitParams<S> p) {
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
@@ -318,8 +461,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
   sm.pos = reinterpret_cast<S*>(smem_raw);
   sm.goal = sm.pos + (size_t)PD * spc * TC * sm.RS;
   sm.inv = sm.goal + (size_t)PD * Rp;
-  sm.one = sm.inv + Rp;
-  sm.obs = sm.one + Rp;
+  sm.obs = sm.inv + 2 * Rp;
   {
     uintptr_t q = reinterpret_cast<uintptr_t>(sm.obs + 4 * (p.n_obs + 1));
     q = (q + 15) & ~uintptr_t(15);
@@ -332,14 +474,15 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
     const S g = k < R ? p.goals[k * PD + c] : S(0);
     sm.goal[j] = F32 ? -g : g;
   }
-  for (int k = tid; k < Rp; k += nthreads) {
-    sm.inv[k] = k < R ? p.inv_dstart[k] : (F32 ? S(0) : S(1));
-    sm.one[k] = k < R ? S(1) : S(0);
+  for (int k = tid; k < Rp; k += nthreads) {  // interleaved (1/‖s−g‖ | ‖s−g‖, valid)
+    sm.inv[2 * k] = k < R ? p.inv_dstart[k] : (F32 ? S(0) : S(1));
+    sm.inv[2 * k + 1] = k < R ? S(1) : S(0);
   }
   for (int j = tid; j < 4 * p.n_obs; j += nthreads) {
     const S v = p.obs[j];
     sm.obs[j] = (F32 && (j & 3) != 3) ? -v : v;
   }
+  if (F32 && (p.n_obs & 1) && tid < 4) sm.obs[4 * p.n_obs + tid] = tid == 3 ? S(1.0e30) : S(0);  // never-hit pad
 
   // ---- phase-A identity: (sample sA, robot kA)
   const int sA = tid / Rp, kA = tid % Rp;
@@ -363,6 +506,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
   }
   const S* zrow = p.z + (liveA ? mA : 0) * (int64_t)T * R * DU;
   double effort = 0.0;
+  float eff32 = 0.f;
   bool bad = false;
 
   // NOISE == 0: prefetch ring over the HBM noise stream + base/mean-scaled
@@ -400,42 +544,20 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
 
   for (int t0 = 0; t0 < T; t0 += TC) {
     // ===== phase A: integrate TC steps
-    if (robotA) {
+    if constexpr (NOISE == 1) {
+      if (robotA) {
+        const int nsteps = t0 + TC < T ? TC : T - t0;
+        float x0[DX];
+#pragma unroll
+        for (int q = 0; q < DX; ++q) x0[q] = x[q];
+        const float chk = rollout_fused<KIND>(p, sm, sA, kA, p.m_global0 + mA, t0, nsteps, x, zst, key, eff32);
+        if (!(chk == 0.f)) rollout_check<KIND>(p, kA, p.m_global0 + mA, t0, nsteps, x0, zst);
+      }
+    } else if (robotA) {
       const int t_end = t0 + TC < T ? t0 + TC : T;
 #pragma unroll
       for (int j = 0; j < kPF; ++j) fetch(t0 + j, t_end, j);
       for (int tc = 0; tc < TC; tc += kPF) {
-        if constexpr (NOISE == 1) {
-          // base+msv loads for the block first; the Philox draws hide their latency
-#pragma unroll
-          for (int j = 0; j < kPF; ++j) {
-            const int t = t0 + tc + j;
-            if (t < T) {
-#pragma unroll
-              for (int d = 0; d < DU; ++d) bq[j][d] = __ldg(p.bm + ((int64_t)t * R + kA) * DU + d);
-            }
-          }
-          const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
-          float nz[kPF * DU];
-#pragma unroll
-          for (int g = 0; g < kPF * DU / 4; ++g) {
-            const float4 v = philox_normals(key, (uint64_t)(p.m_global0 + mA), (uint32_t)kA, g0 + g);
-            nz[4 * g] = v.x;
-            nz[4 * g + 1] = v.y;
-            nz[4 * g + 2] = v.z;
-            nz[4 * g + 3] = v.w;
-          }
-#pragma unroll
-          for (int j = 0; j < kPF; ++j) {
-            const int t = t0 + tc + j;
-#pragma unroll
-            for (int d = 0; d < DU; ++d) zq[j][d] = (S)nz[j * DU + d];
-            if (t < T) {
-#pragma unroll
-              for (int d = 0; d < DU; ++d) __stcs(zst + ((int64_t)t * R + kA) * DU + d, zq[j][d]);
-            }
-          }
-        }
 #pragma unroll
         for (int j = 0; j < kPF; ++j) {
           const int t = t0 + tc + j;
@@ -445,14 +567,16 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
             for (int d = 0; d < DU; ++d) {
               S v;
               if constexpr (F32) {
-                v = fmaf(p.sd, zq[j][d], bq[j][d]);  // base + (mean_scale·var + std·z)
+                // base + (mean_scale·var + std·z), clamped (FMNMX; NaN inputs are
+                // rejected on the host before launch, so this equals cwiseMax/Min)
+                v = fminf(fmaxf(fmaf(p.sd, zq[j][d], bq[j][d]), p.lower[d]), p.upper[d]);
               } else {
                 v = xadd(bq[j][d], xadd(mq[j][d], xmul(p.sd, zq[j][d])));
+                v = (v < p.lower[d]) ? p.lower[d] : v;  // cwiseMax(lower), dynamics.cpp:78
+                v = (p.upper[d] < v) ? p.upper[d] : v;  // cwiseMin(upper)
               }
-              v = (v < p.lower[d]) ? p.lower[d] : v;  // cwiseMax(lower)
-              v = (p.upper[d] < v) ? p.upper[d] : v;  // cwiseMin(upper)
               u[d] = v;
-              if (p.w_e != 0.0) effort += (double)v * (double)v;
+              eff32 = fmaf(v, v, eff32);  // effort extension (w_e·Σ‖u‖²)
             }
             fetch(t + kPF, t_end, j);
             rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
@@ -469,12 +593,12 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
             sm.row(0, sA, tc + j)[kA] = x[0];
             sm.row(1, sA, tc + j)[kA] = x[1];
             if constexpr (PD == 3) sm.row(2, sA, tc + j)[kA] = x[2];
-            if (p.states_out) {
+            if (NOISE == 0 && p.states_out) {
               S* so = p.states_out + (mA * (int64_t)(T + 1) + t + 1) * R * DX + (int64_t)kA * DX;
 #pragma unroll
               for (int q = 0; q < DX; ++q) so[q] = x[q];
             }
-            if (p.controls_out) {
+            if (NOISE == 0 && p.controls_out) {
               S* co = p.controls_out + (mA * (int64_t)(T + 1) + t) * R * DU + (int64_t)kA * DU;
 #pragma unroll
               for (int d = 0; d < DU; ++d) co[d] = u[d];
@@ -483,10 +607,16 @@ __global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const Fit
         }
       }
     }
+    effort += (double)eff32;  // per-chunk fp32 partial → fp64 accumulator
+    eff32 = 0.f;
     __syncthreads();
 
     // ===== phase B: fitness of the TC steps just integrated
+#ifdef D4K_EXPERIMENT_SKIP_B
+    if (liveB && p.n_obs < 0) {
+#else
     if (liveB) {
+#endif
       for (int j = 0; j < ipt; ++j) {
         const int tc = item0 + j - sB * TC;
         if (t0 + tc >= T) break;
