@@ -78,6 +78,9 @@ typedef struct {
   double alpha_bar_final;
   uint64_t seed;
   int mode;
+  /* NoiseSchedule::alpha_bar (steps+1 values, alpha_bar[0] = 1), or NULL for
+   * make_schedule(steps, alpha_bar_final) (schedule.cpp:9-27). */
+  const double* alpha_bar;
 } d4orm_denoiser_config;
 
 /* DenoiseStepRecord (denoiser.hpp:29-34) */

@@ -43,7 +43,8 @@ class Problem_C(C.Structure):
 
 class DenoiserConfig_C(C.Structure):
     _fields_ = [("steps", C.c_int), ("batch", C.c_int64), ("lambda_", C.c_double),
-                ("alpha_bar_final", C.c_double), ("seed", C.c_uint64), ("mode", C.c_int)]
+                ("alpha_bar_final", C.c_double), ("seed", C.c_uint64), ("mode", C.c_int),
+                ("alpha_bar", C.POINTER(C.c_double))]
 
 
 class TraceRec_C(C.Structure):

@@ -353,7 +353,15 @@ int check_config(d4orm_cuda_ctx* ctx, const d4orm_denoiser_config* c, RunShape* 
   rs->mode = c->mode;
   // schedule (schedule.cpp:9-27)
   ctx->ab.assign((size_t)rs->N + 1, 1.0);
-  for (int i = 1; i <= rs->N; ++i) ctx->ab[i] = std::pow(c->alpha_bar_final, (double)i / rs->N);
+  if (c->alpha_bar) {  // the caller's NoiseSchedule (denoiser.cpp uses `schedule`, not the config knob)
+    for (int i = 0; i <= rs->N; ++i) {
+      if (!(c->alpha_bar[i] > 0.0) || !(c->alpha_bar[i] <= 1.0))
+        return fail(ctx, D4ORM_E_INVALID, "run_denoising: alpha_bar[%d] = %g outside (0, 1]", i, c->alpha_bar[i]);
+      ctx->ab[i] = c->alpha_bar[i];
+    }
+  } else {
+    for (int i = 1; i <= rs->N; ++i) ctx->ab[i] = std::pow(c->alpha_bar_final, (double)i / rs->N);
+  }
   return D4ORM_OK;
 }
 
