@@ -1,0 +1,58 @@
+"""Sample sharding and the GPU-count-invariant reduction of the weighted mean.
+
+This is the host-side statement of the multi-GPU protocol the C-ABI runs with
+NCCL inside each step's CUDA graph (csrc/d4orm_cuda.cu, enqueue_step):
+
+* rank r of G owns the contiguous samples [r·M/G, (r+1)·M/G); the Philox noise
+  counter uses the *global* sample index, so the sample set is identical for
+  any G;
+* rewards are all-gathered, so every rank computes the same z-scored weights
+  from the full vector (score_weights needs the global std — SURVEY F4);
+* Σ_m w_m·sample_m is summed per chunk of CHUNK samples and the chunk partials
+  are combined by a binary-counter pairwise tree (k_wmean_tree).  A rank owns an
+  aligned power-of-two block of chunks, so its local root is one subtree of the
+  single-GPU tree; after all-gathering the G roots every rank finishes the same
+  tree — the result is bitwise identical for G = 1, 2, 4, 8.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+CHUNK = 256  # kChunk in csrc/d4orm_cuda.cu
+
+
+def shard_range(M: int, world: int, rank: int) -> tuple[int, int]:
+    """(first global sample, count) of `rank`."""
+    if M % world:
+        raise ValueError(f"batch {M} not divisible by world {world}")
+    Ml = M // world
+    if world > 1 and Ml % CHUNK:
+        raise ValueError(f"per-rank batch must be a multiple of {CHUNK}")
+    return rank * Ml, Ml
+
+
+def pairwise_tree(parts):
+    """Binary-counter pairwise sum, exactly k_wmean_tree's order: equal-size
+    subtrees merge as (older + newer); leftovers fold right to left."""
+    stack = []
+    for cnt, v in enumerate(parts):
+        k = cnt
+        while k & 1:
+            v = stack.pop() + v
+            k >>= 1
+        stack.append(v)
+    total = stack.pop()
+    while stack:
+        total = stack.pop() + total
+    return total
+
+
+def chunk_partials(samples: np.ndarray, weights: np.ndarray, chunk: int = CHUNK):
+    """Per-chunk Σ_m w_m·sample_m in ascending m (k_wmean_partial)."""
+    out = []
+    for c0 in range(0, samples.shape[0], chunk):
+        acc = np.zeros(samples.shape[1:])
+        for m in range(c0, min(c0 + chunk, samples.shape[0])):
+            acc = acc + weights[m] * samples[m]
+        out.append(acc)
+    return out
