@@ -1,15 +1,16 @@
 // d4orm_cuda.cu — context, orchestration and C-ABI (include/d4orm_cuda.h).
 //
-// One denoising step (denoiser.cpp:152-180) is five launches on the context's
-// stream, captured once per (problem, config, step) as a CUDA graph:
+// One denoising step (denoiser.cpp:152-180) is four kernel launches on the
+// context's stream, captured once per (problem, config, step) as a CUDA graph:
 //
-//   K1(i-1) Philox noise for the *next* step, on a forked branch (HBM-bound,
-//           overlaps the compute-bound K2+K3 of this step; z is double-buffered)
-//   K2+K3(i) rollout + fitness → reward[m]           (this rank's samples)
-//   [NCCL all-gather of rewards when world > 1]
-//   K4(i)   z-scored softmax weights over all M rewards (every rank, identical)
-//   K5(i)   chunked weighted mean + deterministic tree → variable, mean-scaled
-//           variable for step i-1 [NCCL all-gather of chunk-tree roots]
+//   K2+K3(i) rollout + fitness → reward[m] (this rank's samples); on the fp32
+//            path the Philox noise (K1) is drawn inside it and z is stored once
+//            for K5; the fp64 parity path runs the standalone K1 first
+//   [ncclAllGather of the rewards when sharded]
+//   K4(i)    z-scored softmax weights over all M rewards (every rank, identical)
+//   K5(i)    chunked weighted mean + deterministic pairwise tree → variable and
+//            the mean-scaled variable of step i-1
+//            [ncclAllGather of the chunk-tree roots when sharded]
 #include <dlfcn.h>
 
 #include <cmath>
@@ -101,6 +102,7 @@ struct DevBuf {
 };
 
 constexpr int kChunk = 256;   // samples per K5 partial (fixed → GPU-count invariant tree)
+constexpr int64_t kPartLargeE = 16384;  // E at which K5 switches to one sequential walk per thread
 constexpr int kWeightThreads = 1024;
 
 }  // namespace
@@ -148,7 +150,7 @@ struct d4orm_cuda_ctx {
     cudaSetDevice(device);
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (auto* b : {&z[0], &z[1], &base, &msv, &starts_d, &goals_d, &inv_d, &obs_d, &partial, &roots,
+    for (auto* b : {&z[0], &z[1], &base, &msv, &bm, &starts_d, &goals_d, &inv_d, &obs_d, &partial, &roots,
                     &states_out, &controls_out})
       b->release();
     var.release(); rewards.release(); w64.release(); trace.release(); w32.release();
@@ -464,7 +466,7 @@ int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, bool philox, bo
   f.z_store = (S*)ctx->z[0].p;
   CU(launch_fit<S>(ctx, f, smem, fused));
   if (int r = mark(1)) return r;
-  if (ctx->world > 1) {
+  if (ctx->comm) {
     NC(g_nccl.AllGather(ctx->rewards.p + rs.m0, ctx->rewards.p, (size_t)rs.Ml, ncclFloat64, ctx->comm, ctx->s_main));
   }
   d4k::WeightParams wp{ctx->rewards.p, rs.M, rs.lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p + 4 * (rs.N - i), i,
@@ -472,22 +474,27 @@ int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, bool philox, bo
   d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
   CU(cudaGetLastError());
   if (int r = mark(2)) return r;
-  const dim3 pgrid((unsigned)((rs.E + 4 * d4k::kThreads - 1) / (4 * d4k::kThreads)), (unsigned)rs.chunks_local);
-  if (f64) {
-    d4k::k_wmean_partial<S, double><<<pgrid, d4k::kThreads, 0, ctx->s_main>>>(
-        (const S*)ctx->z[0].p, ctx->w64.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, kChunk,
-        (S*)ctx->partial.p);
-  } else {
-    d4k::k_wmean_partial<S, float><<<pgrid, d4k::kThreads, 0, ctx->s_main>>>(
-        (const S*)ctx->z[0].p, ctx->w32.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, kChunk,
-        (S*)ctx->partial.p);
-  }
+  static_assert(kChunk == d4k::kChunkSamples, "K5 chunk size");
+  auto partial = [&](auto sub_tag) {
+    constexpr int SUB = decltype(sub_tag)::value;
+    using Sh = d4k::PartShape<SUB>;
+    const dim3 pgrid((unsigned)((rs.E + 4 * Sh::GROUPS - 1) / (4 * Sh::GROUPS)), (unsigned)rs.chunks_local);
+    if (f64) {
+      d4k::k_wmean_partial<S, double, SUB><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(
+          (const S*)ctx->z[0].p, ctx->w64.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, (S*)ctx->partial.p);
+    } else {
+      d4k::k_wmean_partial<S, float, SUB><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(
+          (const S*)ctx->z[0].p, ctx->w32.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, (S*)ctx->partial.p);
+    }
+  };
+  if (rs.E >= kPartLargeE) partial(std::integral_constant<int, 1>{});
+  else partial(std::integral_constant<int, 16>{});
   CU(cudaGetLastError());
   if (int r = mark(3)) return r;
   const unsigned tgrid = (unsigned)((rs.E + d4k::kThreads - 1) / d4k::kThreads);
   S* bm = f64 ? nullptr : (S*)ctx->bm.p;
   const S* bs = (const S*)ctx->base.p;
-  if (ctx->world == 1) {
+  if (!ctx->comm) {
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
                                                                    sab, next_ms, ctx->var.p, (S*)ctx->msv.p, bs, bm,
                                                                    nullptr);
@@ -678,7 +685,7 @@ int d4orm_cuda_create(int device, int rank, int world, const void* nccl_id, d4or
   CU(cudaEventCreate(&c->ev_t1));
   c->ev_k.resize(5);
   for (auto& e : c->ev_k) CU(cudaEventCreate(&e));
-  if (world > 1) {
+  if (world > 1 || nccl_id) {  // a 1-rank communicator exercises the same protocol on one GPU
     std::string e;
     if (!g_nccl.load(&e) || !nccl_id) {
       c.release();
@@ -943,7 +950,7 @@ int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_
 
 int d4orm_cuda_launches_per_step(const d4orm_cuda_ctx* ctx) {
   // K2+K3, K4, K5 partial, K5 tree (+ K1 on the fp64 path, + the root tree when sharded)
-  return 4 + (ctx->precision == D4ORM_PREC_F64 ? 1 : 0) + (ctx->world > 1 ? 1 : 0);
+  return 4 + (ctx->precision == D4ORM_PREC_F64 ? 1 : 0) + (ctx->comm ? 1 : 0);
 }
 
 extern "C++" template <typename S>

@@ -140,21 +140,26 @@ __global__ void __launch_bounds__(NT) k_score_weights(const WeightParams p) {
     }
     return;
   }
-  // max of the scaled values = the scaled max (monotone), denoiser.cpp:78-82
-  const double max_scaled = (best - mean) / std_dev / p.lambda;
+  // max of the scaled values = the scaled max (monotone), denoiser.cpp:78-82.
+  // (r−mean)/std/λ as one multiply by 1/(std·λ); normalisation by 1/Σ; the
+  // entropy uses log w = (s − s_max) − log Σ, so no per-sample log (all equal
+  // to the reference's expressions up to fp64 rounding).
+  const double inv = 1.0 / (std_dev * p.lambda);
+  const double max_scaled = (best - mean) * inv;
   double sum = 0.0;
   for (int64_t j = b; j < e; ++j) {
-    const double w = exp((p.reward[j] - mean) / std_dev / p.lambda - max_scaled);
+    const double w = exp((p.reward[j] - mean) * inv - max_scaled);
     p.w64[j] = w;
     sum += w;
   }
   sum = block_sum<NT>(sum, sh);
+  const double rsum = 1.0 / sum, lsum = log(sum);
   double h = 0.0;
   for (int64_t j = b; j < e; ++j) {
-    const double w = p.w64[j] / sum;
+    const double w = p.w64[j] * rsum;
     p.w64[j] = w;
     p.w32[j] = (float)w;
-    if (w > 0.0) h -= w * log(w);
+    if (w > 0.0) h -= w * (((p.reward[j] - mean) * inv - max_scaled) - lsum);
   }
   h = block_sum<NT>(h, sh);
   if (tid == 0) {
@@ -166,47 +171,112 @@ __global__ void __launch_bounds__(NT) k_score_weights(const WeightParams p) {
 }
 
 // ---------------------------------------------------- K5 weighted mean
-// Partial of Σ_m w_m·sample_m over one chunk of `ch` samples (ascending m), 4
-// consecutive elements per thread; sample_m = msv + sd·z_m (denoiser.cpp:44-45,
-// mc_average :104-106).  Streams z once (evict-first loads).
-template <typename S, typename W>
-__global__ void __launch_bounds__(kThreads) k_wmean_partial(const S* __restrict__ z, const W* __restrict__ w,
-                                                            const S* __restrict__ msv, S sd, int64_t M,
-                                                            int64_t elems, int ch, S* __restrict__ partial) {
-  const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+// Partial of Σ_m w_m·sample_m over one chunk of kPartSub·kPartLanes samples,
+// sample_m = msv + sd·z_m (denoiser.cpp:44-45, mc_average :104-106).
+// CTA = kPartGroups element groups (4 consecutive elements each) × kPartSub
+// sub-ranges: a thread accumulates its kPartLanes samples (ascending m, all
+// loads in flight at once — this kernel is HBM-latency/bandwidth bound and
+// streams z exactly once), then the kPartSub sub-partials are combined by a
+// fixed pairwise tree in shared memory.  The order is fixed by the chunk, so
+// the result is deterministic and independent of how samples are sharded.
+// Two fixed CTA shapes, chosen per problem by E (so the order is still fixed
+// for a given problem and sharding): small E splits the chunk across 16
+// sub-ranges to expose parallelism; large E already has enough CTAs along E and
+// keeps one sequential 256-sample walk per thread (best streaming efficiency).
+constexpr int kChunkSamples = 256;
+constexpr int kPartBatch = 16;  // loads in flight per thread
+template <int SUB>
+struct PartShape {
+  static constexpr int GROUPS = SUB == 1 ? 256 : 16;
+  static constexpr int LANES = kChunkSamples / SUB;
+  static constexpr int THREADS = GROUPS * SUB;
+};
+
+template <typename S, typename W, int SUB>
+__global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const S* __restrict__ z,
+                                                                           const W* __restrict__ w,
+                                                                           const S* __restrict__ msv, S sd, int64_t M,
+                                                                           int64_t elems, S* __restrict__ partial) {
+  constexpr int kPartGroups = PartShape<SUB>::GROUPS, kPartSub = SUB, kPartLanes = PartShape<SUB>::LANES;
+  __shared__ S red[kPartSub][kPartGroups][4];
+  const int g = threadIdx.x % kPartGroups, sr = threadIdx.x / kPartGroups;
+  const int64_t e0 = ((int64_t)blockIdx.x * kPartGroups + g) * 4;
   const int64_t c = blockIdx.y;
-  const int64_t mb = c * ch, me = mb + ch < M ? mb + ch : M;
-  if (e0 >= elems) return;
-  const int n = elems - e0 < 4 ? (int)(elems - e0) : 4;
+  const int64_t mb = c * (kPartSub * kPartLanes) + (int64_t)sr * kPartLanes;
+  const int n = e0 < elems ? (elems - e0 < 4 ? (int)(elems - e0) : 4) : 0;
   S acc[4] = {S(0), S(0), S(0), S(0)};
-  S mv[4] = {S(0), S(0), S(0), S(0)};
-  for (int j = 0; j < n; ++j) mv[j] = msv[e0 + j];
-  if constexpr (std::is_same<S, float>::value) {
-    if (n == 4 && (elems & 3) == 0) {
-      const float4* zp = reinterpret_cast<const float4*>(z + mb * elems + e0);
-      const int64_t stride = elems / 4;
+  if (n > 0) {
+    S mv[4] = {S(0), S(0), S(0), S(0)};
+    for (int j = 0; j < n; ++j) mv[j] = msv[e0 + j];
+    bool vec = false;
+    if constexpr (std::is_same<S, float>::value) vec = n == 4 && (elems & 3) == 0;
+    if (vec) {
+      if constexpr (std::is_same<S, float>::value && SUB == 1) {
+        // large E: one streaming walk per thread, pointer-stepped rows
+        const float4* zp = reinterpret_cast<const float4*>(z + mb * elems + e0);
+        const int64_t stride = elems / 4;
+        const int64_t me = mb + kPartLanes < M ? mb + kPartLanes : M;
 #pragma unroll 4
-      for (int64_t m = mb; m < me; ++m) {
-        const float4 v = __ldcs(zp);
-        zp += stride;
-        const float wm = (float)__ldg(w + m);
-        acc[0] = fmaf(wm, fmaf(sd, v.x, mv[0]), acc[0]);
-        acc[1] = fmaf(wm, fmaf(sd, v.y, mv[1]), acc[1]);
-        acc[2] = fmaf(wm, fmaf(sd, v.z, mv[2]), acc[2]);
-        acc[3] = fmaf(wm, fmaf(sd, v.w, mv[3]), acc[3]);
+        for (int64_t m = mb; m < me; ++m) {
+          const float4 v = __ldcs(zp);
+          zp += stride;
+          const float wm = (float)__ldg(w + m);
+          acc[0] = fmaf(wm, fmaf(sd, v.x, mv[0]), acc[0]);
+          acc[1] = fmaf(wm, fmaf(sd, v.y, mv[1]), acc[1]);
+          acc[2] = fmaf(wm, fmaf(sd, v.z, mv[2]), acc[2]);
+          acc[3] = fmaf(wm, fmaf(sd, v.w, mv[3]), acc[3]);
+        }
+      } else if constexpr (std::is_same<S, float>::value) {
+        for (int q0 = 0; q0 < kPartLanes; q0 += kPartBatch) {
+          float4 v[kPartBatch];
+          float wv[kPartBatch];
+#pragma unroll
+          for (int q = 0; q < kPartBatch; ++q) {
+            const int64_t m = mb + q0 + q;
+            if (m < M) {
+              v[q] = __ldcs(reinterpret_cast<const float4*>(z + m * elems + e0));
+              wv[q] = (float)__ldg(w + m);
+            } else {
+              v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+              wv[q] = 0.f;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kPartBatch; ++q) {
+            acc[0] = fmaf(wv[q], fmaf(sd, v[q].x, mv[0]), acc[0]);
+            acc[1] = fmaf(wv[q], fmaf(sd, v[q].y, mv[1]), acc[1]);
+            acc[2] = fmaf(wv[q], fmaf(sd, v[q].z, mv[2]), acc[2]);
+            acc[3] = fmaf(wv[q], fmaf(sd, v[q].w, mv[3]), acc[3]);
+          }
+        }
       }
-      *reinterpret_cast<float4*>(partial + c * elems + e0) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-      return;
+    } else {
+      for (int q = 0; q < kPartLanes; ++q) {
+        const int64_t m = mb + q;
+        if (m >= M) break;
+        const S wm = (S)w[m];
+        for (int j = 0; j < n; ++j) {
+          const S smp = xadd(mv[j], xmul(sd, z[m * elems + e0 + j]));
+          acc[j] = xadd(acc[j], xmul(wm, smp));
+        }
+      }
     }
   }
-  for (int64_t m = mb; m < me; ++m) {
-    const W wm = w[m];
-    for (int j = 0; j < n; ++j) {
-      const S smp = xadd(mv[j], xmul(sd, z[m * elems + e0 + j]));
-      acc[j] = xadd(acc[j], xmul((S)wm, smp));
+#pragma unroll
+  for (int j = 0; j < 4; ++j) red[sr][g][j] = acc[j];
+  __syncthreads();
+  // pairwise over the sub-ranges: strides 1, 2, ... (fixed order)
+#pragma unroll
+  for (int s = 1; s < kPartSub; s <<= 1) {
+    if ((sr & (2 * s - 1)) == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[sr][g][j] = xadd(red[sr][g][j], red[sr + s][g][j]);
     }
+    __syncthreads();
   }
-  for (int j = 0; j < n; ++j) partial[c * elems + e0 + j] = acc[j];
+  if (sr == 0 && n > 0) {
+    for (int j = 0; j < n; ++j) partial[c * elems + e0 + j] = red[0][g][j];
+  }
 }
 
 // Pairwise (binary-counter) sum of the chunk partials — a balanced binary tree
@@ -226,11 +296,21 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree(const S* __restrict__ p
   S stack[40];
   int64_t cnt = 0;
   int top = 0;
-  for (int64_t c = 0; c < nchunks; ++c) {
-    S v = partial[c * elems + e];
-    for (int64_t k = cnt; k & 1; k >>= 1) v = xadd(stack[--top], v);  // merge equal-size subtrees
-    stack[top++] = v;
-    ++cnt;
+  for (int64_t c0 = 0; c0 < nchunks; c0 += 8) {
+    S v8[8];  // eight loads in flight, then merged in order
+    const int nb = nchunks - c0 < 8 ? (int)(nchunks - c0) : 8;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < nb) v8[j] = partial[(c0 + j) * elems + e];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j < nb) {
+        S v = v8[j];
+        for (int64_t k = cnt; k & 1; k >>= 1) v = xadd(stack[--top], v);  // merge equal-size subtrees
+        stack[top++] = v;
+        ++cnt;
+      }
+    }
   }
   S total = stack[--top];
   while (top > 0) total = xadd(stack[--top], total);

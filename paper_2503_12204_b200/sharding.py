@@ -47,12 +47,22 @@ def pairwise_tree(parts):
     return total
 
 
+LARGE_E = 16384  # kPartLargeE in csrc/d4orm_cuda.cu
+
+
 def chunk_partials(samples: np.ndarray, weights: np.ndarray, chunk: int = CHUNK):
-    """Per-chunk Σ_m w_m·sample_m in ascending m (k_wmean_partial)."""
+    """Per-chunk Σ_m w_m·sample_m in k_wmean_partial's order: each of SUB
+    sub-ranges sums its LANES samples in ascending m, then the sub-sums are
+    combined by a balanced pairwise tree (SUB = 1 when E >= LARGE_E, else 16)."""
+    SUB = 1 if samples.shape[1] >= LARGE_E else 16
+    LANES = chunk // SUB
     out = []
     for c0 in range(0, samples.shape[0], chunk):
-        acc = np.zeros(samples.shape[1:])
-        for m in range(c0, min(c0 + chunk, samples.shape[0])):
-            acc = acc + weights[m] * samples[m]
-        out.append(acc)
+        subs = []
+        for s0 in range(c0, c0 + chunk, LANES):
+            acc = np.zeros(samples.shape[1:])
+            for m in range(s0, min(s0 + LANES, samples.shape[0])):
+                acc = acc + weights[m] * samples[m]
+            subs.append(acc)
+        out.append(pairwise_tree(subs))
     return out

@@ -266,3 +266,25 @@ def test_fused_philox_equals_k1_noise(gpu, case):
     np.testing.assert_array_equal(r1, r2)
     np.testing.assert_array_equal(w1, w2)
     np.testing.assert_array_equal(v1, v2)
+
+
+def test_nccl_protocol_on_one_rank():
+    """The sharded protocol (reward all-gather, chunk-tree roots all-gather, all
+    inside the step graphs) on a 1-rank NCCL communicator: bitwise the result of
+    the single-GPU path."""
+    import ctypes as C
+    from paper_2503_12204_b200._lib import lib
+    buf = C.create_string_buffer(128)
+    assert lib().d4orm_cuda_nccl_id(buf) == 0
+    p = CASES["C2"]()
+    cfg = d4.DenoiserConfig(steps=5, batch=1024, seed=13)
+    base = controls_for(p, 1, 2, scale=0.3)[0]
+    a = d4.GpuDenoiser(p)
+    b = d4.GpuDenoiser(p, rank=0, world=1, nccl_id=bytes(buf.raw))
+    va, ta = a.run_denoising(base, cfg)
+    vb, tb = b.run_denoising(base, cfg)
+    assert b.launches_per_step() == a.launches_per_step() + 1
+    np.testing.assert_array_equal(va, vb)
+    assert ta == tb
+    a.close()
+    b.close()
