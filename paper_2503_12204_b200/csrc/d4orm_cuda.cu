@@ -135,7 +135,7 @@ struct d4orm_cuda_ctx {
   // device buffers (typeless where the scalar type varies)
   DevBuf<unsigned char> z[2], base, msv, bm, starts_d, goals_d, inv_d, obs_d, partial, roots;
   DevBuf<unsigned char> states_out, controls_out;
-  DevBuf<double> var, rewards, w64, trace;
+  DevBuf<double> var, rewards, w64, trace, wscratch;
   DevBuf<float> w32;
   DevBuf<int> counts;
   DevBuf<unsigned long long> errw;
@@ -383,6 +383,7 @@ int ensure_buffers(d4orm_cuda_ctx* ctx, const RunShape& rs, bool two_z) {
   CU(ctx->partial.ensure((size_t)rs.chunks_local * rs.E * S));
   CU(ctx->roots.ensure((size_t)ctx->world * rs.E * S));
   CU(ctx->trace.ensure((size_t)4 * (rs.N + 1)));
+  CU(ctx->wscratch.ensure((size_t)6 * 160));
   CU(ctx->errw.ensure(1));
   CU(ctx->keys.ensure((size_t)rs.N + 1));
   return D4ORM_OK;
@@ -471,8 +472,23 @@ int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, bool philox, bo
   }
   d4k::WeightParams wp{ctx->rewards.p, rs.M, rs.lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p + 4 * (rs.N - i), i,
                        ctx->errw.p};
-  d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
-  CU(cudaGetLastError());
+  {
+    // 2 rewards per thread (16 beyond 148·2048 samples) held in registers;
+    // one CTA → plain launch, several → cooperative launch (grid.sync)
+    const bool big = rs.M > 148LL * d4k::kWThreads * 2;
+    const int64_t per_cta = (int64_t)d4k::kWThreads * (big ? 16 : 2);
+    const unsigned g = (unsigned)((rs.M + per_cta - 1) / per_cta);
+    if (g > 148) return fail(ctx, D4ORM_E_UNSUPPORTED, "score_weights: batch %lld too large", (long long)rs.M);
+    double* scratch = ctx->wscratch.p;
+    const void* fn = big ? (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 16>
+                         : (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 2>;
+    void* args[] = {(void*)&wp, (void*)&scratch};
+    if (g == 1) {
+      CU(cudaLaunchKernel(fn, dim3(1), dim3(d4k::kWThreads), args, 0, ctx->s_main));
+    } else {
+      CU(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(d4k::kWThreads), args, 0, ctx->s_main));
+    }
+  }
   if (int r = mark(2)) return r;
   static_assert(kChunk == d4k::kChunkSamples, "K5 chunk size");
   auto partial = [&](auto sub_tag) {
@@ -759,7 +775,7 @@ int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* p) {
   ctx->prob.obs_centers = ctx->obs_c.data();
   ctx->prob.obs_radii = ctx->obs_r.data();
   const int R = p->robots;
-  ctx->TB = R <= 4 ? 4 : (R <= 8 ? 8 : 16);
+  ctx->TB = R <= 4 ? 4 : (R <= 16 ? 8 : 16);  // small tiles for small teams: fewer registers, more CTAs/SM
   ctx->Rp = (R + ctx->TB - 1) / ctx->TB * ctx->TB;
   ctx->MAXW = ctx->Rp <= 64 ? 2 : 8;
   // 128-thread CTAs (several resident per SM: one CTA's latency-bound rollout

@@ -11,6 +11,8 @@
 // (score_weights, mc_average), schedule.cpp:29-36, denoiser.cpp:110-117.
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "d4orm_common.cuh"
 #include "k23.cuh"
 
@@ -94,9 +96,138 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
   return r;
 }
 
-// score_weights (denoiser.cpp:50-90) + trace (denoiser.cpp:172-179), one CTA.
-// Each thread owns a contiguous slice; every reduction is fixed-order, so the
-// weights are bitwise reproducible and identical on every rank.
+// score_weights (denoiser.cpp:50-90) + trace (denoiser.cpp:172-179) as one
+// cooperative grid of G CTAs (grid.sync between the four reduction phases).
+// Every thread keeps its ≤ PER rewards in registers (one load pass, all in
+// flight), CTA partials go to `scratch` and every CTA folds the G partials in
+// the same fixed order — bitwise reproducible and identical on every rank.
+constexpr int kWThreads = 1024;  // PER (rewards per thread) is 2 or 16, see the launch
+
+__device__ __forceinline__ double grid_fold(double v, double* sh, double* scratch, int slot, bool is_max) {
+  namespace cg = cooperative_groups;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmax(v, u) : v + u;
+  }
+  if ((tid & 31) == 0) sh[tid >> 5] = v;
+  __syncthreads();
+  if (tid < 32) {
+    double r = sh[tid];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, r, o);
+      r = is_max ? fmax(r, u) : r + u;
+    }
+    if (tid == 0) scratch[slot * gridDim.x + blockIdx.x] = r;
+  }
+  if (gridDim.x > 1) cg::this_grid().sync();  // cooperative launch only when G > 1
+  else __syncthreads();
+  double r = scratch[slot * gridDim.x];
+  for (unsigned b = 1; b < gridDim.x; ++b) {
+    const double u = scratch[slot * gridDim.x + b];
+    r = is_max ? fmax(r, u) : r + u;
+  }
+  __syncthreads();
+  return r;
+}
+
+template <int NT, int kWPer>
+__global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p, double* scratch) {
+  static_assert(NT == kWThreads, "k_score_weights_grid block size");
+  __shared__ double sh[32];
+  const int64_t stride = (int64_t)gridDim.x * kWThreads;
+  const int64_t g0 = (int64_t)blockIdx.x * kWThreads + threadIdx.x;
+  double r[kWPer];
+  double s = 0.0, best = -INFINITY;
+  bool finite = true;
+#pragma unroll
+  for (int q = 0; q < kWPer; ++q) {
+    const int64_t j = g0 + q * stride;
+    r[q] = j < p.M ? p.reward[j] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < kWPer; ++q) {
+    if (g0 + q * stride < p.M) {
+      finite = finite && isfinite(r[q]);
+      s += r[q];
+      best = fmax(best, r[q]);
+    }
+  }
+  const double nf = grid_fold(finite ? 0.0 : 1.0, sh, scratch, 0, false);
+  if (nf != 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(p.err, 0xFFFFFFFFFFFFFFFEull);
+    return;
+  }
+  const double mean = grid_fold(s, sh, scratch, 1, false) / (double)p.M;
+  best = grid_fold(best, sh, scratch, 2, true);
+  double v = 0.0;
+#pragma unroll
+  for (int q = 0; q < kWPer; ++q) {
+    if (g0 + q * stride < p.M) {
+      const double d = r[q] - mean;
+      v += d * d;
+    }
+  }
+  const double std_dev = sqrt(grid_fold(v, sh, scratch, 3, false) / (double)p.M);
+  const bool head = blockIdx.x == 0 && threadIdx.x == 0;
+  if (std_dev < 1e-8) {  // degenerate batch → uniform (denoiser.cpp:74-77)
+    const double u = 1.0 / (double)p.M;
+#pragma unroll
+    for (int q = 0; q < kWPer; ++q) {
+      const int64_t j = g0 + q * stride;
+      if (j < p.M) {
+        p.w64[j] = u;
+        p.w32[j] = (float)u;
+      }
+    }
+    if (head) {
+      p.trace[0] = p.step;
+      p.trace[1] = best;
+      p.trace[2] = mean;
+      p.trace[3] = -(double)p.M * u * log(u);
+    }
+    return;
+  }
+  // (r−mean)/std/λ as one multiply; max of the scaled values = scaled max
+  // (denoiser.cpp:78-82); log w = (s − s_max) − log Σ for the entropy.
+  const double inv = 1.0 / (std_dev * p.lambda);
+  const double max_scaled = (best - mean) * inv;
+  double e[kWPer];
+  double sum = 0.0;
+#pragma unroll
+  for (int q = 0; q < kWPer; ++q) {
+    e[q] = 0.0;
+    if (g0 + q * stride < p.M) {
+      r[q] = (r[q] - mean) * inv - max_scaled;  // now the shifted exponent
+      e[q] = exp(r[q]);
+      sum += e[q];
+    }
+  }
+  sum = grid_fold(sum, sh, scratch, 4, false);
+  const double rsum = 1.0 / sum, lsum = log(sum);
+  double h = 0.0;
+#pragma unroll
+  for (int q = 0; q < kWPer; ++q) {
+    const int64_t j = g0 + q * stride;
+    if (j < p.M) {
+      const double w = e[q] * rsum;
+      p.w64[j] = w;
+      p.w32[j] = (float)w;
+      if (w > 0.0) h -= w * (r[q] - lsum);
+    }
+  }
+  h = grid_fold(h, sh, scratch, 5, false);
+  if (head) {
+    p.trace[0] = p.step;
+    p.trace[1] = best;
+    p.trace[2] = mean;
+    p.trace[3] = h;
+  }
+}
+
+// Single-CTA variant (kept for d4orm_cuda_score_weights on arbitrary M).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_score_weights(const WeightParams p) {
   __shared__ double sh[NT / 32 + 1];

@@ -446,7 +446,7 @@ __device__ __noinline__ void rollout_check(const FitParams<float>& p, int kA, in
 }
 
 template <typename S, int KIND, int TB, int MAXW, int NOISE>
-__global__ void __launch_bounds__(kFitMaxThreads, 3) k_rollout_fitness(const FitParams<S> p) {
+__global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fitness(const FitParams<S> p) {
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
   constexpr bool F32 = std::is_same<S, float>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
