@@ -211,10 +211,17 @@ size_t fit_smem(const d4orm_cuda_ctx* c, int TC) {
 // of the rollout prefetch depth, halved until ≥ 2 CTAs fit per SM.
 template <typename S>
 int choose_tc(d4orm_cuda_ctx* ctx, int* tc_out, size_t* smem_out) {
-  int TC = ctx->Rp >= 16 ? (ctx->Rp < 64 ? ctx->Rp : 64) : 16;
-  while (fit_smem<S>(ctx, TC) > 100 * 1024 && TC > d4k::kPF) TC /= 2;
+  // Rp >= 64: items shared by Q = 2 threads (TC = Rp/2) to halve the position
+  // tile; then halve further (Q ≤ 4) only if the tile still exceeds 100 KB.
+  const int Rp = ctx->Rp;
+  int TC = Rp >= 16 ? (Rp > 64 ? Rp / 2 : Rp) : 16;
+  while (fit_smem<S>(ctx, TC) > 100 * 1024 && TC / 2 >= d4k::kPF && (TC / 2) % d4k::kPF == 0 &&
+         (TC / 2 >= Rp || (Rp % (TC / 2) == 0 && Rp / (TC / 2) <= 4)))
+    TC /= 2;
   if (TC % d4k::kPF != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d not a multiple of %d", TC, d4k::kPF);
-  if (TC >= ctx->Rp && TC % ctx->Rp != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d vs Rp %d", TC, ctx->Rp);
+  if (TC >= Rp && TC % Rp != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d vs Rp %d", TC, Rp);
+  if (TC < Rp && (Rp % TC != 0 || Rp / TC > 4))
+    return fail(ctx, D4ORM_E_UNSUPPORTED, "d4orm_cuda: %d robots need a %d-step tile that does not fit", ctx->prob.robots, TC);
   *tc_out = TC;
   *smem_out = fit_smem<S>(ctx, TC);
   return D4ORM_OK;
@@ -252,13 +259,19 @@ int upload_problem(d4orm_cuda_ctx* ctx) {
   CU((upload_as<S>(ctx->inv_d, inv.data(), R, ctx->s_main)));
   std::vector<double> obs((size_t)4 * p.n_obstacles + 1, 0.0);
   for (int o = 0; o < p.n_obstacles; ++o) {
-    for (int j = 0; j < PD; ++j) obs[4 * o + j] = ctx->obs_c[(size_t)o * PD + j];
     const double lim = ctx->obs_r[o] + p.robot_radius;
     const double l2 = lim * lim;
-    if (std::is_same<S, double>::value) {
+    if (std::is_same<S, double>::value) {  // the reference's form: centre, (r+R_a)²
+      for (int j = 0; j < PD; ++j) obs[4 * o + j] = ctx->obs_c[(size_t)o * PD + j];
       obs[4 * o + 3] = l2;
-    } else {
-      obs[4 * o + 3] = -(double)std::nextafter((float)l2, INFINITY);
+    } else {  // expanded form: −2c and |c|² − (r+R_a)²↑
+      double c2 = 0.0;
+      for (int j = 0; j < PD; ++j) {
+        const double c = ctx->obs_c[(size_t)o * PD + j];
+        obs[4 * o + j] = -2.0 * c;
+        c2 += c * c;
+      }
+      obs[4 * o + 3] = c2 - (double)std::nextafter((float)l2, INFINITY);
     }
   }
   CU((upload_as<S>(ctx->obs_d, obs.data(), obs.size(), ctx->s_main)));
@@ -290,7 +303,7 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
   const double margin = 2.0 * p.robot_radius + p.epsilon;
   const double m2 = margin * margin;
   if (std::is_same<S, double>::value) f.margin_sq = (S)m2;
-  else f.margin_sq = (S)(-(double)std::nextafter((float)m2, INFINITY));
+  else f.margin_sq = (S)(double)std::nextafter((float)m2, INFINITY);  // m²↑ (expanded-form tests)
   f.bm = (const S*)ctx->bm.p;
   f.w_t = p.w_t;
   f.w_o = p.obstacle_weight;

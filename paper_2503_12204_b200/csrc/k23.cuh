@@ -129,111 +129,206 @@ struct PackedTile {
   }
 };
 
-// One (sample, t) item in fp32: returns Σ goal terms; conflict / obstacle counts.
+// Column side of a tile-pair task: robots [k0, k0+TB) as −2·p and |p|²−m²↑,
+// register-resident; the row side is streamed from shared memory.
+template <int PD, int TB>
+struct ColTile {
+  uint64_t x[TB / 2], y[TB / 2], z[PD == 3 ? TB / 2 : 1], n[TB / 2];
+  __device__ __forceinline__ void load(const float* X, const float* Y, const float* Z, int k0, float m2u) {
+    const uint64_t m2n = pack2(-2.0f, -2.0f);
+#pragma unroll
+    for (int j = 0; j < TB / 2; ++j) {
+      const uint64_t bx = *reinterpret_cast<const uint64_t*>(X + k0 + 2 * j);
+      const uint64_t by = *reinterpret_cast<const uint64_t*>(Y + k0 + 2 * j);
+      uint64_t n2 = fmul2(bx, bx);
+      n2 = ffma2_sq(by, n2);
+      if constexpr (PD == 3) {
+        const uint64_t bz = *reinterpret_cast<const uint64_t*>(Z + k0 + 2 * j);
+        n2 = ffma2_sq(bz, n2);
+        z[j] = fmul2(bz, m2n);
+      }
+      x[j] = fmul2(bx, m2n);
+      y[j] = fmul2(by, m2n);
+      n[j] = fadd2_b(-m2u, n2);
+    }
+  }
+};
+
+// Expanded-form test of two row robots (scalars) against column pair j:
+// t = |a|² + (|b|² − m²↑) − 2·a·b, sign bit set ⟺ within the margin.
+template <int PD, int TB>
+__device__ __forceinline__ void row_pair_vs_col(const ColTile<PD, TB>& C, int j, float2 ax, float2 ay, float2 az,
+                                                float n0, float n1, uint64_t& t0, uint64_t& t1) {
+  t0 = fadd2_b(n0, C.n[j]);
+  t1 = fadd2_b(n1, C.n[j]);
+  t0 = ffma2(pack2(ax.x, ax.x), C.x[j], t0);
+  t1 = ffma2(pack2(ax.y, ax.y), C.x[j], t1);
+  t0 = ffma2(pack2(ay.x, ay.x), C.y[j], t0);
+  t1 = ffma2(pack2(ay.y, ay.y), C.y[j], t1);
+  if constexpr (PD == 3) {
+    t0 = ffma2(pack2(az.x, az.x), C.z[j], t0);
+    t1 = ffma2(pack2(az.y, az.y), C.z[j], t1);
+  }
+}
+
+template <int MAXW>
+__device__ __forceinline__ void or_mask(uint32_t* cm, int k0, uint32_t bits) {
+  const int w = k0 >> 5, sh = k0 & 31;
+#pragma unroll
+  for (int q = 0; q < MAXW; ++q)
+    if (q == w) cm[q] |= bits << sh;
+}
+
+// One (sample, t) item in fp32, shared by Q threads: thread q takes the tasks
+// of the (a ≤ b) tile-pair enumeration with index ≡ q (mod Q); diagonal tasks
+// also carry tile a's goal and obstacle terms.  Returns Σ goal terms; adds
+// obstacle robot-steps to *nobs and OR-s conflict flags into cm (merged across
+// the Q lanes and counted by the caller).
+//
+// Distance tests use the expanded form  t = |a|² + (|b|² − m²↑) − 2·a·b, three
+// packed FP instructions per two tests (FADD2 of the norms, then one FFMA2 per
+// coordinate against the −2-scaled partner) instead of four for the direct
+// form; the sign bit of t is the (fp32-approximate) `<=` decision of
+// reward.cpp:106,120.  Obstacles: t = |p|² + (|c|² − L²↑) − 2·p·c, with the
+// obstacle's −2c and |c|²−L²↑ precomputed.  Goal terms keep the direct form.
 template <int PD, int TB, int MAXW>
-__device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int tc, int R, int n_obs, float nm2,
-                                          int* nconf, int* nobs) {
+__device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int tc, int R, int n_obs, float m2u, int q,
+                                          int Q, uint32_t* cm, int* nobs) {
   const float* X = sm.row(0, s, tc);
   const float* Y = sm.row(1, s, tc);
   const float* Z = PD == 3 ? sm.row(2, s, tc) : X;
   const int ntiles = sm.Rp / TB;
-  const uint64_t nm2p = pack2(nm2, nm2);
-  uint32_t cm[MAXW];
-#pragma unroll
-  for (int w = 0; w < MAXW; ++w) cm[w] = 0;
   float gacc = 0.f;
-  int no = 0;
-  for (int a = 0; a < ntiles; ++a) {
-    PackedTile<PD, TB> A;
-    A.load(X, Y, Z, a * TB);
-    // ---- goal terms (reward.cpp:92-97)
+  // Lanes of one item run the same task kind in lockstep (no divergence):
+  // diagonal tiles a ≡ q (mod Q), then off-diagonal task k ≡ q (mod Q).
+  for (int a = q; a < ntiles; a += Q) {
+    {
+      // ---------------- diagonal task (a, a): goal + obstacles + inner pairs
+      {
+        PackedTile<PD, TB> A;
+        A.load(X, Y, Z, a * TB);
+        uint64_t NA[TB / 2];
 #pragma unroll
-    for (int j = 0; j < TB / 2; ++j) {
-      const int k = a * TB + 2 * j;
-      const uint64_t gx = *reinterpret_cast<const uint64_t*>(sm.goal + k);
-      const uint64_t gy = *reinterpret_cast<const uint64_t*>(sm.goal + sm.Rp + k);
-      const uint64_t dx = fadd2(A.x[j], gx), dy = fadd2(A.y[j], gy);
-      uint64_t d2 = fmul2(dx, dx);
-      d2 = ffma2_sq(dy, d2);
-      if constexpr (PD == 3) {
-        const uint64_t gz = *reinterpret_cast<const uint64_t*>(sm.goal + 2 * sm.Rp + k);
-        d2 = ffma2_sq(fadd2(A.z[j], gz), d2);
-      }
-      const float2 io0 = *reinterpret_cast<const float2*>(sm.inv + 2 * k);  // (1/‖s−g‖, valid)
-      const float2 io1 = *reinterpret_cast<const float2*>(sm.inv + 2 * k + 2);
-      gacc += fmaf(-sqrt_approx(lo_f(d2)), io0.x, io0.y);
-      gacc += fmaf(-sqrt_approx(hi_f(d2)), io1.x, io1.y);
-    }
-    // ---- obstacle terms (reward.cpp:112-125): obstacles outer, the tile's
-    // robot pairs inner (independent chains), two obstacles per pass
-    uint32_t olo[TB / 2], ohi[TB / 2];
-#pragma unroll
-    for (int j = 0; j < TB / 2; ++j) olo[j] = ohi[j] = 0;
-    for (int o = 0; o < n_obs; o += 2) {
-      const float4 b0 = *reinterpret_cast<const float4*>(sm.obs + 4 * o);  // −cx, −cy, −cz, −L²↑
-      const float4 b1 = *reinterpret_cast<const float4*>(sm.obs + 4 * o + 4);  // padded: never hits
-      const uint64_t l0 = pack2(b0.w, b0.w), l1 = pack2(b1.w, b1.w);
-#pragma unroll
-      for (int j = 0; j < TB / 2; ++j) {
-        uint64_t t0 = ffma2_sq(fadd2_b(b0.y, A.y[j]), l0);
-        uint64_t t1 = ffma2_sq(fadd2_b(b1.y, A.y[j]), l1);
-        if constexpr (PD == 3) {
-          t0 = ffma2_sq(fadd2_b(b0.z, A.z[j]), t0);
-          t1 = ffma2_sq(fadd2_b(b1.z, A.z[j]), t1);
+        for (int j = 0; j < TB / 2; ++j) {
+          uint64_t n2 = fmul2(A.x[j], A.x[j]);
+          n2 = ffma2_sq(A.y[j], n2);
+          if constexpr (PD == 3) n2 = ffma2_sq(A.z[j], n2);
+          NA[j] = n2;
         }
-        t0 = ffma2_sq(fadd2_b(b0.x, A.x[j]), t0);
-        t1 = ffma2_sq(fadd2_b(b1.x, A.x[j]), t1);
-        olo[j] |= lo32(t0) | lo32(t1);
-        ohi[j] |= hi32(t0) | hi32(t1);
+        // goal terms (reward.cpp:92-97), direct form
+#pragma unroll
+        for (int j = 0; j < TB / 2; ++j) {
+          const int k = a * TB + 2 * j;
+          const uint64_t gx = *reinterpret_cast<const uint64_t*>(sm.goal + k);
+          const uint64_t gy = *reinterpret_cast<const uint64_t*>(sm.goal + sm.Rp + k);
+          const uint64_t dx = fadd2(A.x[j], gx), dy = fadd2(A.y[j], gy);
+          uint64_t d2 = fmul2(dx, dx);
+          d2 = ffma2_sq(dy, d2);
+          if constexpr (PD == 3) {
+            const uint64_t gz = *reinterpret_cast<const uint64_t*>(sm.goal + 2 * sm.Rp + k);
+            d2 = ffma2_sq(fadd2(A.z[j], gz), d2);
+          }
+          const float2 io0 = *reinterpret_cast<const float2*>(sm.inv + 2 * k);  // (1/‖s−g‖, valid)
+          const float2 io1 = *reinterpret_cast<const float2*>(sm.inv + 2 * k + 2);
+          gacc += fmaf(-sqrt_approx(lo_f(d2)), io0.x, io0.y);
+          gacc += fmaf(-sqrt_approx(hi_f(d2)), io1.x, io1.y);
+        }
+        // obstacle terms (reward.cpp:112-125): obstacles outer, robot pairs inner
+        uint32_t olo[TB / 2], ohi[TB / 2];
+#pragma unroll
+        for (int j = 0; j < TB / 2; ++j) olo[j] = ohi[j] = 0;
+        for (int o = 0; o < n_obs; o += 2) {
+          const float4 b0 = *reinterpret_cast<const float4*>(sm.obs + 4 * o);      // −2c, |c|²−L²↑
+          const float4 b1 = *reinterpret_cast<const float4*>(sm.obs + 4 * o + 4);  // padded: never hits
+#pragma unroll
+          for (int j = 0; j < TB / 2; ++j) {
+            uint64_t t0 = fadd2_b(b0.w, NA[j]);
+            uint64_t t1 = fadd2_b(b1.w, NA[j]);
+            t0 = ffma2(A.x[j], pack2(b0.x, b0.x), t0);
+            t1 = ffma2(A.x[j], pack2(b1.x, b1.x), t1);
+            t0 = ffma2(A.y[j], pack2(b0.y, b0.y), t0);
+            t1 = ffma2(A.y[j], pack2(b1.y, b1.y), t1);
+            if constexpr (PD == 3) {
+              t0 = ffma2(A.z[j], pack2(b0.z, b0.z), t0);
+              t1 = ffma2(A.z[j], pack2(b1.z, b1.z), t1);
+            }
+            olo[j] |= lo32(t0) | lo32(t1);
+            ohi[j] |= hi32(t0) | hi32(t1);
+          }
+        }
+        uint32_t om = 0;
+#pragma unroll
+        for (int j = 0; j < TB / 2; ++j) om |= ((olo[j] >> 31) | ((ohi[j] >> 31) << 1)) << (2 * j);
+        const int kv = R - a * TB;  // valid robots in this tile
+        *nobs += __popc(kv >= 32 ? om : (om & ((1u << (kv > 0 ? kv : 0)) - 1u)));
+        // pairs inside tile a, from the tile already in registers: columns as
+        // −2·p and |p|²−m²↑, rows as scalars
+        ColTile<PD, TB> C;
+        const uint64_t m2n = pack2(-2.0f, -2.0f);
+#pragma unroll
+        for (int j = 0; j < TB / 2; ++j) {
+          C.x[j] = fmul2(A.x[j], m2n);
+          C.y[j] = fmul2(A.y[j], m2n);
+          if constexpr (PD == 3) C.z[j] = fmul2(A.z[j], m2n);
+          C.n[j] = fadd2_b(-m2u, NA[j]);
+        }
+        uint32_t f[TB];
+#pragma unroll
+        for (int k = 0; k < TB; ++k) f[k] = 0;
+#pragma unroll
+        for (int i = 0; i < TB / 2; ++i) {
+          const float2 ax = make_float2(lo_f(A.x[i]), hi_f(A.x[i]));
+          const float2 ay = make_float2(lo_f(A.y[i]), hi_f(A.y[i]));
+          const float2 az = PD == 3 ? make_float2(lo_f(A.z[i]), hi_f(A.z[i])) : make_float2(0.f, 0.f);
+          const float n0 = lo_f(NA[i]), n1 = hi_f(NA[i]);
+#pragma unroll
+          for (int j = i + 1; j < TB / 2; ++j) {
+            uint64_t t0, t1;
+            row_pair_vs_col<PD, TB>(C, j, ax, ay, az, n0, n1, t0, t1);
+            f[2 * i] |= lo32(t0) | hi32(t0);
+            f[2 * i + 1] |= lo32(t1) | hi32(t1);
+            f[2 * j] |= lo32(t0) | lo32(t1);
+            f[2 * j + 1] |= hi32(t0) | hi32(t1);
+          }
+          // the pair (2i, 2i+1) itself
+          float t = fmaf(-2.0f * ax.x, ax.y, n0 + (n1 - m2u));
+          t = fmaf(-2.0f * ay.x, ay.y, t);
+          if constexpr (PD == 3) t = fmaf(-2.0f * az.x, az.y, t);
+          f[2 * i] |= __float_as_uint(t);
+          f[2 * i + 1] |= __float_as_uint(t);
+        }
+        or_mask<MAXW>(cm, a * TB, sign_mask<TB>(f));
       }
     }
-    uint32_t om = 0;
-#pragma unroll
-    for (int j = 0; j < TB / 2; ++j) om |= ((olo[j] >> 31) | ((ohi[j] >> 31) << 1)) << (2 * j);
-    const int kv = R - a * TB;  // valid robots in this tile
-    no += __popc(kv >= 32 ? om : (om & ((1u << (kv > 0 ? kv : 0)) - 1u)));
-    // ---- pairs inside tile A
-    uint32_t f[TB];
-#pragma unroll
-    for (int q = 0; q < TB; ++q) f[q] = 0;
-#pragma unroll
-    for (int i = 0; i < TB / 2; ++i) {
-      const float x0 = lo_f(A.x[i]), x1 = hi_f(A.x[i]), y0 = lo_f(A.y[i]), y1 = hi_f(A.y[i]);
-      const float z0 = PD == 3 ? lo_f(A.z[i]) : 0.f, z1 = PD == 3 ? hi_f(A.z[i]) : 0.f;
-#pragma unroll
-      for (int j = i + 1; j < TB / 2; ++j) {
-        const uint64_t t0 = pair2_f32<PD>(-x0, -y0, -z0, A.x[j], A.y[j], PD == 3 ? A.z[j] : 0ull, nm2p);
-        const uint64_t t1 = pair2_f32<PD>(-x1, -y1, -z1, A.x[j], A.y[j], PD == 3 ? A.z[j] : 0ull, nm2p);
-        f[2 * i] |= lo32(t0) | hi32(t0);
-        f[2 * i + 1] |= lo32(t1) | hi32(t1);
-        f[2 * j] |= lo32(t0) | lo32(t1);
-        f[2 * j + 1] |= hi32(t0) | hi32(t1);
-      }
-      const uint32_t t = pair1_f32<PD>(x0, y0, z0, x1, y1, z1, nm2);
-      f[2 * i] |= t;
-      f[2 * i + 1] |= t;
+  }
+  const int n_off = ntiles * (ntiles - 1) / 2;
+  for (int k = q; k < n_off; k += Q) {
+    // ---------------- off-diagonal task k → (a, b), a < b
+    int a = 0, rem = k;
+    while (rem >= ntiles - 1 - a) {
+      rem -= ntiles - 1 - a;
+      ++a;
     }
-    uint32_t ma = sign_mask<TB>(f);
-    // ---- A × B tiles
-    for (int b = a + 1; b < ntiles; ++b) {
-      PackedTile<PD, TB> B;
-      B.load(X, Y, Z, b * TB);
+    const int b = a + 1 + rem;
+    {
+      ColTile<PD, TB> C;
+      C.load(X, Y, Z, b * TB, m2u);
       uint32_t fb[TB];
 #pragma unroll
-      for (int q = 0; q < TB; ++q) fb[q] = 0;
-      // A rows streamed from shared memory (two robots per LDS.64), so only
-      // the packed B tile and its flags stay register-resident.
+      for (int k = 0; k < TB; ++k) fb[k] = 0;
+      uint32_t ma = 0;
 #pragma unroll 2
       for (int i = 0; i < TB / 2; ++i) {
         const float2 ax = *reinterpret_cast<const float2*>(X + a * TB + 2 * i);
         const float2 ay = *reinterpret_cast<const float2*>(Y + a * TB + 2 * i);
         const float2 az = PD == 3 ? *reinterpret_cast<const float2*>(Z + a * TB + 2 * i) : make_float2(0.f, 0.f);
-        const float nx0 = -ax.x, nx1 = -ax.y, ny0 = -ay.x, ny1 = -ay.y, nz0 = -az.x, nz1 = -az.y;
+        const float n0 = fmaf(ax.x, ax.x, fmaf(ay.x, ay.x, az.x * az.x));
+        const float n1 = fmaf(ax.y, ax.y, fmaf(ay.y, ay.y, az.y * az.y));
         uint32_t fa0 = 0, fa1 = 0;
 #pragma unroll
         for (int j = 0; j < TB / 2; ++j) {
-          const uint64_t t0 = pair2_f32<PD>(nx0, ny0, nz0, B.x[j], B.y[j], PD == 3 ? B.z[j] : 0ull, nm2p);
-          const uint64_t t1 = pair2_f32<PD>(nx1, ny1, nz1, B.x[j], B.y[j], PD == 3 ? B.z[j] : 0ull, nm2p);
+          uint64_t t0, t1;
+          row_pair_vs_col<PD, TB>(C, j, ax, ay, az, n0, n1, t0, t1);
           fa0 |= lo32(t0) | hi32(t0);
           fa1 |= lo32(t1) | hi32(t1);
           fb[2 * j] |= lo32(t0) | lo32(t1);
@@ -241,25 +336,10 @@ __device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int t
         }
         ma |= ((fa0 >> 31) | ((fa1 >> 31) << 1)) << (2 * i);
       }
-      const uint32_t mb = sign_mask<TB>(fb);
-      const int wb = (b * TB) >> 5, sh = (b * TB) & 31;
-#pragma unroll
-      for (int w = 0; w < MAXW; ++w)
-        if (w == wb) cm[w] |= mb << sh;
+      or_mask<MAXW>(cm, a * TB, ma);
+      or_mask<MAXW>(cm, b * TB, sign_mask<TB>(fb));
     }
-    const int wa = (a * TB) >> 5, sha = (a * TB) & 31;
-#pragma unroll
-    for (int w = 0; w < MAXW; ++w)
-      if (w == wa) cm[w] |= ma << sha;
   }
-  int c = 0;
-#pragma unroll
-  for (int w = 0; w < MAXW; ++w) {
-    const int kv = R - 32 * w;
-    if (kv > 0) c += __popc(kv >= 32 ? cm[w] : (cm[w] & ((1u << kv) - 1u)));
-  }
-  *nconf += c;
-  *nobs += no;
   return gacc;
 }
 
@@ -480,7 +560,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
   }
   for (int j = tid; j < 4 * p.n_obs; j += nthreads) {
     const S v = p.obs[j];
-    sm.obs[j] = (F32 && (j & 3) != 3) ? -v : v;
+    sm.obs[j] = v;  // fp32: (−2c, |c|²−L²↑) precomputed on the host; fp64: (c, L²)
   }
   if (F32 && (p.n_obs & 1) && tid < 4) sm.obs[4 * p.n_obs + tid] = tid == 3 ? S(1.0e30) : S(0);  // never-hit pad
 
@@ -531,9 +611,13 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
       }
     }
   };
-  // ---- phase-B identity: items (sB, tc), ipt consecutive per thread
+  // ---- phase-B identity.  TC >= Rp: ipt consecutive items per thread;
+  // TC < Rp: each item is shared by Q = Rp/TC adjacent threads (task split).
+  // Either way the threads of sample s are [s·Rp, (s+1)·Rp).
   const int ipt = TC >= Rp ? TC / Rp : 1;
-  const int item0 = TC >= Rp ? tid * ipt : tid;
+  const int Q = TC >= Rp ? 1 : Rp / TC;
+  const int qB = TC >= Rp ? 0 : tid % Q;
+  const int item0 = TC >= Rp ? tid * ipt : tid / Q;
   const int sB = item0 / TC;
   const int64_t mB = (int64_t)blockIdx.x * spc + sB;
   const bool liveB = item0 < spc * TC && mB < p.M;
@@ -621,8 +705,23 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
         const int tc = item0 + j - sB * TC;
         if (t0 + tc >= T) break;
         if constexpr (F32) {
-          gsum += (double)item_f32<PD, TB, MAXW>(sm, sB, tc, R, p.n_obs, p.margin_sq, &nconf, &nobs);
-        } else {
+          uint32_t cm[MAXW];
+#pragma unroll
+          for (int w = 0; w < MAXW; ++w) cm[w] = 0;
+          gsum += (double)item_f32<PD, TB, MAXW>(sm, sB, tc, R, p.n_obs, p.margin_sq, qB, Q, cm, &nobs);
+          // merge the Q lanes' conflict flags (adjacent lanes, same item)
+          for (int off = 1; off < Q; off <<= 1) {
+#pragma unroll
+            for (int w = 0; w < MAXW; ++w) cm[w] |= __shfl_xor_sync(__activemask(), cm[w], off);
+          }
+          if (qB == 0) {
+#pragma unroll
+            for (int w = 0; w < MAXW; ++w) {
+              const int kv = R - 32 * w;
+              if (kv > 0) nconf += __popc(kv >= 32 ? cm[w] : (cm[w] & ((1u << kv) - 1u)));
+            }
+          }
+        } else if (qB == 0) {
           gsum += item_f64<PD>(sm, sB, tc, R, p.n_obs, p.margin_sq, &nconf, &nobs);
         }
       }
@@ -636,9 +735,9 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
   sm.cnt[2 * tid] = liveB ? nconf : 0;
   sm.cnt[2 * tid + 1] = liveB ? nobs : 0;
   __syncthreads();
-  if (liveB && item0 == sB * TC) {
-    const int nt = TC >= Rp ? Rp : TC;
-    const int first = TC >= Rp ? sB * Rp : sB * TC;
+  if (liveB && tid == sB * Rp) {  // first thread of the sample
+    const int nt = Rp;
+    const int first = sB * Rp;
     double g = 0.0;
     long long nc = 0, no = 0;
     for (int q = 0; q < nt; ++q) {

@@ -75,11 +75,32 @@ def test_rollout_fitness_f64_matches_oracle(gpu, oracle, case):
         assert (cnt[m, 0], cnt[m, 1]) == (nc, no), (m, cnt[m], nc, no)
 
 
+def _counts(p, st, delta):
+    """Conflict / obstacle robot-steps (t >= 1) with the squared thresholds
+    shifted by delta (numpy, fp64)."""
+    pos = st[1:, :, : p.pdim]
+    m2 = (2 * p.robot_radius + p.epsilon) ** 2 + delta
+    d2 = ((pos[:, :, None, :] - pos[:, None, :, :]) ** 2).sum(-1)
+    R = p.robots
+    d2[:, np.arange(R), np.arange(R)] = np.inf
+    nc = int((d2 <= m2).any(-1).sum())
+    no = 0
+    if len(p.obs_radii):
+        od2 = ((pos[:, :, None, :] - p.obs_centers[None, None]) ** 2).sum(-1)
+        no = int((od2 <= (p.obs_radii + p.robot_radius)[None, None] ** 2 + delta).any(-1).sum())
+    return nc, no
+
+
+# fp32 decisions use the expanded form |a|²+|b|²−2a·b on fp32 positions: a flip
+# is 'explained' when the GPU count lies between the counts with the squared
+# margin shifted by ∓FLIP_BAND on the GPU's own positions.
+FLIP_BAND = 2e-4
+
+
 def explain_flips(oracle, p, st_gpu, nc_gpu, no_gpu):
-    """Recount conflicts on the GPU's own (fp32) positions with the fp64 rule:
-    a count difference vs the oracle is 'explained' when it disappears."""
-    r, nc, no = oracle.total_reward(p, st_gpu)
-    return nc == nc_gpu and no == no_gpu
+    lo = _counts(p, st_gpu, -FLIP_BAND)
+    hi = _counts(p, st_gpu, FLIP_BAND)
+    return lo[0] <= nc_gpu <= hi[0] and lo[1] <= no_gpu <= hi[1]
 
 
 @pytest.mark.parametrize("case", list(CASES))
