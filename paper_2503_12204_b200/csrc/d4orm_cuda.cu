@@ -215,6 +215,10 @@ int choose_tc(d4orm_cuda_ctx* ctx, int* tc_out, size_t* smem_out) {
   // tile; then halve further (Q ≤ 4) only if the tile still exceeds 100 KB.
   const int Rp = ctx->Rp;
   int TC = Rp >= 16 ? (Rp > 64 ? Rp / 2 : Rp) : 16;
+  if (const char* e = std::getenv("D4ORM_Q")) {  // tuning knob: threads per fitness item (1, 2, 4)
+    const int q = std::atoi(e);
+    if ((q == 2 || q == 4) && Rp % q == 0 && (Rp / q) % d4k::kPF == 0) TC = Rp / q;
+  }
   while (fit_smem<S>(ctx, TC) > 100 * 1024 && TC / 2 >= d4k::kPF && (TC / 2) % d4k::kPF == 0 &&
          (TC / 2 >= Rp || (Rp % (TC / 2) == 0 && Rp / (TC / 2) <= 4)))
     TC /= 2;
@@ -789,6 +793,10 @@ int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* p) {
   ctx->prob.obs_radii = ctx->obs_r.data();
   const int R = p->robots;
   ctx->TB = R <= 4 ? 4 : (R <= 16 ? 8 : 16);  // small tiles for small teams: fewer registers, more CTAs/SM
+  if (const char* e = std::getenv("D4ORM_TB")) {  // tuning knob (4, 8 or 16)
+    const int tb = std::atoi(e);
+    if (tb == 4 || tb == 8 || tb == 16) ctx->TB = std::max(tb, R <= 4 ? 4 : (R <= 8 ? 8 : 4));
+  }
   ctx->Rp = (R + ctx->TB - 1) / ctx->TB * ctx->TB;
   ctx->MAXW = ctx->Rp <= 64 ? 2 : 8;
   // 128-thread CTAs (several resident per SM: one CTA's latency-bound rollout
