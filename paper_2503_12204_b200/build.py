@@ -39,19 +39,24 @@ def _newer(src: Path, obj: Path, deps: list[Path]) -> bool:
     return src.stat().st_mtime > t or any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, jobs: int | None = None) -> Path:
+def build(verbose: bool = False, jobs: int | None = None, defines: tuple[str, ...] = (),
+          out: Path | None = None) -> Path:
+    """Build the library.  ``defines``/``out`` produce experiment variants
+    (``-D`` flags, separate object dir and output .so) for tools/."""
     nvcc = _nvcc()
-    OBJ.mkdir(exist_ok=True)
+    obj_dir = OBJ if not defines else OBJ.parent / ("build_" + "_".join(d.split("=")[0].lower() for d in defines))
+    lib = out or LIB
+    obj_dir.mkdir(exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").rglob("*.h*"))
     srcs = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
     cmds = []
     objs = []
     for s in srcs:
-        o = OBJ / (s.name + ".o")
+        o = obj_dir / (s.name + ".o")
         objs.append(o)
         if _newer(s, o, headers):
             lang = [] if s.suffix == ".cu" else ["-x", "cu"] if False else []
-            cmds.append([nvcc, *ARCH, *NVCC_FLAGS, *lang, "-c", str(s), "-o", str(o)])
+            cmds.append([nvcc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], *lang, "-c", str(s), "-o", str(o)])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -63,9 +68,9 @@ def build(verbose: bool = False, jobs: int | None = None) -> Path:
 
     with cf.ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
         list(ex.map(run, cmds))
-    if cmds or not LIB.exists():
-        run([nvcc, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-ldl", "-lcudart"])
-    return LIB
+    if cmds or not lib.exists():
+        run([nvcc, *ARCH, "-shared", "-o", str(lib), *map(str, objs), "-ldl", "-lcudart"])
+    return lib
 
 
 def build_oracle() -> None:
@@ -75,6 +80,8 @@ def build_oracle() -> None:
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(verbose="-v" in sys.argv, defines=defs, out=Path(outs[0]) if outs else None))
     if "--oracle" in sys.argv:
         build_oracle()

@@ -131,6 +131,9 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
 // Philox(counter = (g, m_lo, m_hi, k)), lanes n%4.  Each normal is a pure
 // function of (seed, i, m, k, t, d): identical under any sharding of samples,
 // and a rollout thread owning robot k draws its own stream with no redundancy.
+#ifndef D4K_PHILOX_ROUNDS
+#define D4K_PHILOX_ROUNDS 10
+#endif
 struct Philox {
   static __device__ __forceinline__ uint4 round(uint4 c, uint2 k) {
     // one IMAD.WIDE.U32 per 32x32→64 product (hi and lo together)
@@ -141,7 +144,7 @@ struct Philox {
   }
   static __device__ __forceinline__ uint4 gen(uint4 c, uint2 k) {
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
+    for (int r = 0; r < D4K_PHILOX_ROUNDS; ++r) {
       c = round(c, k);
       k.x += 0x9E3779B9u;
       k.y += 0xBB67AE85u;

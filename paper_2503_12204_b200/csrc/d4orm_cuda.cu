@@ -13,6 +13,7 @@
 //            [ncclAllGather of the chunk-tree roots when sharded]
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -133,7 +134,7 @@ struct d4orm_cuda_ctx {
   void* noise_user = nullptr;
 
   // device buffers (typeless where the scalar type varies)
-  DevBuf<unsigned char> z[2], base, msv, bm, starts_d, goals_d, inv_d, obs_d, partial, roots;
+  DevBuf<unsigned char> z[2], base, msv, bm, starts_d, goals_d, inv_d, obs_d, ocl_d, partial, roots;
   DevBuf<unsigned char> states_out, controls_out;
   DevBuf<double> var, rewards, w64, trace, wscratch;
   DevBuf<float> w32;
@@ -150,10 +151,10 @@ struct d4orm_cuda_ctx {
     cudaSetDevice(device);
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
-    for (auto* b : {&z[0], &z[1], &base, &msv, &bm, &starts_d, &goals_d, &inv_d, &obs_d, &partial, &roots,
+    for (auto* b : {&z[0], &z[1], &base, &msv, &bm, &starts_d, &goals_d, &inv_d, &obs_d, &ocl_d, &partial, &roots,
                     &states_out, &controls_out})
       b->release();
-    var.release(); rewards.release(); w64.release(); trace.release(); w32.release();
+    var.release(); rewards.release(); w64.release(); trace.release(); w32.release(); wscratch.release();
     counts.release(); errw.release(); keys.release();
     for (auto e : ev_k) cudaEventDestroy(e);
     for (auto e : {ev_fork, ev_join, ev_t0, ev_t1})
@@ -204,7 +205,7 @@ int64_t elems_of(const d4orm_cuda_ctx* c) { return (int64_t)c->prob.robots * c->
 
 template <typename S>
 size_t fit_smem(const d4orm_cuda_ctx* c, int TC) {
-  return d4k::fit_smem_bytes<S>(c->prob.pdim, c->spc, TC, c->Rp, c->prob.n_obstacles, c->spc * c->Rp);
+  return d4k::fit_smem_bytes<S>(c->prob.pdim, c->spc, TC, c->Rp, c->prob.n_obstacles, c->spc * c->Rp, c->TB);
 }
 
 // Time-chunk length: one fitness item per thread (TC = Rp, ≥ 16), a multiple
@@ -261,22 +262,46 @@ int upload_problem(d4orm_cuda_ctx* ctx) {
     inv[k] = std::is_same<S, double>::value ? std::sqrt(s) : 1.0 / std::sqrt(s);
   }
   CU((upload_as<S>(ctx->inv_d, inv.data(), R, ctx->s_main)));
-  std::vector<double> obs((size_t)4 * p.n_obstacles + 1, 0.0);
-  for (int o = 0; o < p.n_obstacles; ++o) {
-    const double lim = ctx->obs_r[o] + p.robot_radius;
-    const double l2 = lim * lim;
-    if (std::is_same<S, double>::value) {  // the reference's form: centre, (r+R_a)²
+  const int O = p.n_obstacles;
+  std::vector<double> obs((size_t)4 * (O + 1), 0.0);
+  if (std::is_same<S, double>::value) {  // the reference's form: centre, (r+R_a)²
+    for (int o = 0; o < O; ++o) {
+      const double lim = ctx->obs_r[o] + p.robot_radius;
       for (int j = 0; j < PD; ++j) obs[4 * o + j] = ctx->obs_c[(size_t)o * PD + j];
-      obs[4 * o + 3] = l2;
-    } else {  // expanded form: −2c and |c|² − (r+R_a)²↑
+      obs[4 * o + 3] = lim * lim;
+    }
+  } else {
+    // expanded form −2c, |c|² − (r+R_a)²↑, obstacles sorted by the left end of
+    // their culling x-interval [cx − L − δ, cx + L + δ] (the obstacle count of
+    // reward.cpp:112-125 does not depend on the order); row O never hits.
+    std::vector<int> ord(O);
+    std::vector<double> left(O), right(O);
+    for (int o = 0; o < O; ++o) {
+      const double lim = ctx->obs_r[o] + p.robot_radius, cx = ctx->obs_c[(size_t)o * PD];
+      const double slack = 1e-3 + 1e-5 * (std::fabs(cx) + lim);  // > the expanded form's rounding error
+      left[o] = cx - lim - slack;
+      right[o] = cx + lim + slack;
+      ord[o] = o;
+    }
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return left[a] < left[b]; });
+    std::vector<double> ocl((size_t)2 * (O + 1), 1e30);
+    double pmax = -1e30;
+    for (int i = 0; i < O; ++i) {
+      const int o = ord[i];
+      const double lim = ctx->obs_r[o] + p.robot_radius;
       double c2 = 0.0;
       for (int j = 0; j < PD; ++j) {
         const double c = ctx->obs_c[(size_t)o * PD + j];
-        obs[4 * o + j] = -2.0 * c;
+        obs[4 * i + j] = -2.0 * c;
         c2 += c * c;
       }
-      obs[4 * o + 3] = c2 - (double)std::nextafter((float)l2, INFINITY);
+      obs[4 * i + 3] = c2 - (double)std::nextafter((float)(lim * lim), INFINITY);
+      pmax = std::max(pmax, right[o]);
+      ocl[2 * i] = std::nextafter((float)left[o], -INFINITY);   // rounded outward
+      ocl[2 * i + 1] = std::nextafter((float)pmax, INFINITY);
     }
+    obs[4 * O + 3] = 1e30;  // pad row: |p|² + 1e30 > 0
+    CU((upload_as<S>(ctx->ocl_d, ocl.data(), ocl.size(), ctx->s_main)));
   }
   CU((upload_as<S>(ctx->obs_d, obs.data(), obs.size(), ctx->s_main)));
   return D4ORM_OK;
@@ -296,6 +321,7 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
   f.goals = (const S*)ctx->goals_d.p;
   f.inv_dstart = (const S*)ctx->inv_d.p;
   f.obs = (const S*)ctx->obs_d.p;
+  f.obs_cull = std::is_same<S, float>::value ? (const S*)ctx->ocl_d.p : nullptr;
   f.n_obs = p.n_obstacles;
   for (int d = 0; d < 3; ++d) {
     f.lower[d] = (S)p.lower[d];
@@ -308,6 +334,11 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
   const double m2 = margin * margin;
   if (std::is_same<S, double>::value) f.margin_sq = (S)m2;
   else f.margin_sq = (S)(double)std::nextafter((float)m2, INFINITY);  // m²↑ (expanded-form tests)
+  f.cull_margin = (S)(margin * (1.0 + 1e-5) + 1e-3);  // pair culling: separation + rounding slack
+  // x-strip culling pays once a team spans >= 3 tiles (C5: 4); below that the
+  // per-chunk ranking costs more than it saves.  Tuning knob D4ORM_CULL=0/1.
+  f.cull = ctx->Rp / ctx->TB >= 3 ? 1 : 0;
+  if (const char* e = std::getenv("D4ORM_CULL")) f.cull = std::atoi(e) != 0;
   f.bm = (const S*)ctx->bm.p;
   f.w_t = p.w_t;
   f.w_o = p.obstacle_weight;

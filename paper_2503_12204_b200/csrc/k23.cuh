@@ -37,7 +37,10 @@ struct FitParams {
   const S* starts;       // [R][dx]
   const S* goals;        // [R][pd]
   const S* inv_dstart;   // [R]  fp32: 1/‖start−goal‖; fp64: ‖start−goal‖ (divide)
-  const S* obs;          // [O][4]: cx, cy, cz, fp32: −(r+R_a)²↑ | fp64: (r+R_a)²
+  const S* obs;          // [O+1][4] fp32: −2c, |c|²−(r+R_a)²↑ (row O: never-hit pad) | fp64: c, (r+R_a)²
+  const S* obs_cull;     // fp32: [O+1][2] x-interval (left end, prefix-max right end), obstacles sorted by left end
+  S cull_margin;         // fp32: separation (m) beyond which a pair cannot be in conflict, with rounding slack
+  int cull;              // fp32: rank robots by x per chunk and cull tile pairs / obstacles (≥ 3 tiles)
   int n_obs;
   S lower[3], upper[3];
   S dt, half_dt, dt6;
@@ -60,28 +63,37 @@ struct FitParams {
 
 template <typename S>
 struct FitSmem {
-  S* pos;     // [PD][spc][TC][RS]
-  S* goal;    // [PD][Rp]  fp32: −goal ; fp64: goal
-  S* inv;     // [Rp]
-  // (inv is [2·Rp]: (1/‖s−g‖ or ‖s−g‖, valid) pairs)
-  S* obs;     // [O][4]
+  S* pos;     // [PD][spc][TC][RS]; fp32: robot k's column is its rank in the chunk's x order
+  S* goal;    // fp64: [PD][Rp] goal
+  S* inv;     // fp64: [2·Rp] (‖s−g‖, valid)
+  S* obs;     // [O+1][4]
+  S* ocl;     // fp32: [O+1][2] obstacle x-intervals (FitParams::obs_cull)
+  int* key;   // fp32: [spc][Rp] chunk sort keys (x order)
+  float* bb;  // fp32: [2·ntiles][nthreads] per-item tile x-extent (lo, hi)
+  // the final reduction arrays alias `pos` (dead after the last chunk)
   double* red;   // [nthreads]
   double* eff;   // [nthreads]
   int* cnt;      // [2·nthreads]
-  int RS, TC, spc, Rp;
+  int RS, TC, spc, Rp, nthreads;
   __device__ __forceinline__ S* row(int c, int s, int tc) const {
     return pos + ((size_t)(c * spc + s) * TC + tc) * RS;
   }
 };
 
 template <typename S>
-__host__ __device__ inline size_t fit_smem_bytes(int PD, int spc, int TC, int Rp, int nobs, int nthreads) {
+__host__ __device__ inline size_t fit_smem_bytes(int PD, int spc, int TC, int Rp, int nobs, int nthreads, int TB) {
   const int RS = Rp + 2;
-  size_t b = (size_t)PD * spc * TC * RS * sizeof(S);
-  b += (size_t)PD * Rp * sizeof(S) + 2 * (size_t)Rp * sizeof(S) + (size_t)4 * (nobs + 1) * sizeof(S);
-  b = (b + 15) & ~size_t(15);
-  b += 2 * (size_t)nthreads * sizeof(double) + 2 * (size_t)nthreads * sizeof(int);
-  return b;
+  size_t pos = (size_t)PD * spc * TC * RS * sizeof(S);
+  const size_t red = 2 * (size_t)nthreads * sizeof(double) + 2 * (size_t)nthreads * sizeof(int);
+  size_t b = ((pos > red ? pos : red) + 15) & ~size_t(15);
+  b += (size_t)4 * (nobs + 1) * sizeof(S);
+  if (sizeof(S) == 8) {
+    b += (size_t)PD * Rp * sizeof(S) + 2 * (size_t)Rp * sizeof(S);
+  } else {
+    b += (size_t)2 * (nobs + 1) * sizeof(float) + (size_t)spc * Rp * sizeof(int) +
+         (size_t)2 * (Rp / TB) * nthreads * sizeof(float);
+  }
+  return (b + 15) & ~size_t(15);
 }
 
 // ---------------------------------------------------------------- fp32 tiles
@@ -179,67 +191,87 @@ __device__ __forceinline__ void or_mask(uint32_t* cm, int k0, uint32_t bits) {
     if (q == w) cm[q] |= bits << sh;
 }
 
+// Number of leading entries of the ascending sequence a[0], a[2], … a[2(n−1)]
+// that are < v (STRICT = false) or <= v (STRICT = true).  Branch-free with a
+// trip count that depends on n only, so the lanes of a warp stay converged.
+template <bool STRICT>
+__device__ __forceinline__ int sorted_count(const float* a, int n, float v) {
+  int base = 0, len = n;
+  while (len > 1) {
+    const int half = len >> 1;
+    const float e = a[2 * (base + half)];
+    base = (STRICT ? e <= v : e < v) ? base + half : base;
+    len -= half;
+  }
+  const float e = a[2 * base];
+  return base + ((STRICT ? e <= v : e < v) ? 1 : 0);
+}
+
 // One (sample, t) item in fp32, shared by Q threads: thread q takes the tasks
 // of the (a ≤ b) tile-pair enumeration with index ≡ q (mod Q); diagonal tasks
-// also carry tile a's goal and obstacle terms.  Returns Σ goal terms; adds
-// obstacle robot-steps to *nobs and OR-s conflict flags into cm (merged across
-// the Q lanes and counted by the caller).
+// also carry tile a's obstacle terms.  Adds obstacle robot-steps to *nobs and
+// OR-s conflict flags into cm (merged across the Q lanes and counted by the
+// caller).  The goal terms are accumulated by the rollout (phase A).
 //
 // Distance tests use the expanded form  t = |a|² + (|b|² − m²↑) − 2·a·b, three
 // packed FP instructions per two tests (FADD2 of the norms, then one FFMA2 per
 // coordinate against the −2-scaled partner) instead of four for the direct
 // form; the sign bit of t is the (fp32-approximate) `<=` decision of
 // reward.cpp:106,120.  Obstacles: t = |p|² + (|c|² − L²↑) − 2·p·c, with the
-// obstacle's −2c and |c|²−L²↑ precomputed.  Goal terms keep the direct form.
+// obstacle's −2c and |c|²−L²↑ precomputed.
+//
+// Culling (exact): robot columns are in x order (ranked at the chunk start),
+// so tiles are x-strips.  A tile pair whose x-extents are more than
+// cull_margin apart cannot hold a conflict; it is skipped when that holds for
+// every item of the warp.  Likewise only obstacles whose x-interval can meet
+// the strip's extent (warp union) are tested.  The slack in cull_margin and
+// in the obstacle intervals exceeds the expanded form's rounding error, so the
+// skipped tests are ones that would have come out negative anyway.
 template <int PD, int TB, int MAXW>
-__device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int tc, int R, int n_obs, float m2u, int q,
-                                          int Q, uint32_t* cm, int* nobs) {
+__device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc, int R, int n_obs, float m2u,
+                                         bool cull, float cmg, int q, int Q, float* bbp, uint32_t* cm, int* nobs) {
   const float* X = sm.row(0, s, tc);
   const float* Y = sm.row(1, s, tc);
   const float* Z = PD == 3 ? sm.row(2, s, tc) : X;
   const int ntiles = sm.Rp / TB;
-  float gacc = 0.f;
+  const int bbs = sm.nthreads;
   // Lanes of one item run the same task kind in lockstep (no divergence):
   // diagonal tiles a ≡ q (mod Q), then off-diagonal task k ≡ q (mod Q).
   for (int a = q; a < ntiles; a += Q) {
     {
-      // ---------------- diagonal task (a, a): goal + obstacles + inner pairs
+      // ---------------- diagonal task (a, a): extent + obstacles + inner pairs
       {
         PackedTile<PD, TB> A;
         A.load(X, Y, Z, a * TB);
         uint64_t NA[TB / 2];
+        float xlo = lo_f(A.x[0]), xhi = xlo;
 #pragma unroll
         for (int j = 0; j < TB / 2; ++j) {
           uint64_t n2 = fmul2(A.x[j], A.x[j]);
           n2 = ffma2_sq(A.y[j], n2);
           if constexpr (PD == 3) n2 = ffma2_sq(A.z[j], n2);
           NA[j] = n2;
+          xlo = fminf(xlo, fminf(lo_f(A.x[j]), hi_f(A.x[j])));
+          xhi = fmaxf(xhi, fmaxf(lo_f(A.x[j]), hi_f(A.x[j])));
         }
-        // goal terms (reward.cpp:92-97), direct form
-#pragma unroll
-        for (int j = 0; j < TB / 2; ++j) {
-          const int k = a * TB + 2 * j;
-          const uint64_t gx = *reinterpret_cast<const uint64_t*>(sm.goal + k);
-          const uint64_t gy = *reinterpret_cast<const uint64_t*>(sm.goal + sm.Rp + k);
-          const uint64_t dx = fadd2(A.x[j], gx), dy = fadd2(A.y[j], gy);
-          uint64_t d2 = fmul2(dx, dx);
-          d2 = ffma2_sq(dy, d2);
-          if constexpr (PD == 3) {
-            const uint64_t gz = *reinterpret_cast<const uint64_t*>(sm.goal + 2 * sm.Rp + k);
-            d2 = ffma2_sq(fadd2(A.z[j], gz), d2);
-          }
-          const float2 io0 = *reinterpret_cast<const float2*>(sm.inv + 2 * k);  // (1/‖s−g‖, valid)
-          const float2 io1 = *reinterpret_cast<const float2*>(sm.inv + 2 * k + 2);
-          gacc += fmaf(-sqrt_approx(lo_f(d2)), io0.x, io0.y);
-          gacc += fmaf(-sqrt_approx(hi_f(d2)), io1.x, io1.y);
+        if (cull) {
+          bbp[(2 * a) * bbs] = xlo;
+          bbp[(2 * a + 1) * bbs] = xhi;
         }
-        // obstacle terms (reward.cpp:112-125): obstacles outer, robot pairs inner
+        // obstacle terms (reward.cpp:112-125) over the obstacles whose
+        // x-interval meets [xlo, xhi] for some item of the warp
         uint32_t olo[TB / 2], ohi[TB / 2];
 #pragma unroll
         for (int j = 0; j < TB / 2; ++j) olo[j] = ohi[j] = 0;
-        for (int o = 0; o < n_obs; o += 2) {
+        int ob = 0, oe = n_obs;
+        if (cull && n_obs > 0) {
+          const unsigned am = __activemask();
+          ob = __reduce_min_sync(am, sorted_count<false>(sm.ocl + 1, n_obs, xlo));
+          oe = __reduce_max_sync(am, sorted_count<true>(sm.ocl, n_obs, xhi));
+        }
+        for (int o = ob; o < oe; o += 2) {
           const float4 b0 = *reinterpret_cast<const float4*>(sm.obs + 4 * o);      // −2c, |c|²−L²↑
-          const float4 b1 = *reinterpret_cast<const float4*>(sm.obs + 4 * o + 4);  // padded: never hits
+          const float4 b1 = *reinterpret_cast<const float4*>(sm.obs + 4 * o + 4);  // row O: never hits
 #pragma unroll
           for (int j = 0; j < TB / 2; ++j) {
             uint64_t t0 = fadd2_b(b0.w, NA[j]);
@@ -302,6 +334,7 @@ __device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int t
     }
   }
   const int n_off = ntiles * (ntiles - 1) / 2;
+  if (cull && Q > 1 && n_off > 0) __syncwarp(__activemask());  // tile extents written by the item's other lanes
   for (int k = q; k < n_off; k += Q) {
     // ---------------- off-diagonal task k → (a, b), a < b
     int a = 0, rem = k;
@@ -310,6 +343,11 @@ __device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int t
       ++a;
     }
     const int b = a + 1 + rem;
+    if (cull) {
+      const bool apart = bbp[(2 * a + 1) * bbs] + cmg < bbp[(2 * b) * bbs] ||
+                         bbp[(2 * b + 1) * bbs] + cmg < bbp[(2 * a) * bbs];
+      if (__all_sync(__activemask(), apart)) continue;
+    }
     {
       ColTile<PD, TB> C;
       C.load(X, Y, Z, b * TB, m2u);
@@ -340,7 +378,6 @@ __device__ __forceinline__ float item_f32(const FitSmem<float>& sm, int s, int t
       or_mask<MAXW>(cm, b * TB, sign_mask<TB>(fb));
     }
   }
-  return gacc;
 }
 
 // One (sample, t) item in fp64: the reference's loops (reward.cpp:88-127) on
@@ -400,6 +437,28 @@ __device__ __forceinline__ double item_f64(const FitSmem<double>& sm, int s, int
 }
 
 // ------------------------------------------------- fp32 fused rollout (phase A)
+// Goal term of reward.cpp:92-97 for the robot a phase-A thread owns:
+// accumulates ‖p − g‖ / ‖start − g‖ (ng = −g, ginv = 1/‖start − g‖).
+template <int PD>
+__device__ __forceinline__ void goal_acc(const float* x, const float* ng, float ginv, float& gsd) {
+  const float dx = x[0] + ng[0], dy = x[1] + ng[1];
+  float d2 = fmaf(dy, dy, dx * dx);
+  if constexpr (PD == 3) {
+    const float dz = x[2] + ng[2];
+    d2 = fmaf(dz, dz, d2);
+  }
+  gsd = fmaf(sqrt_approx(d2), ginv, gsd);
+}
+
+// Chunk sort key of a robot: its x in an order-preserving integer form, low
+// bits replaced by the lane so keys are unique (the order only steers the
+// culling; ties and near-ties may go either way).  Padding lanes sort last.
+__device__ __forceinline__ int chunk_key(float x, int k, int Rp2, bool real) {
+  int i = __float_as_int(x);
+  i ^= (i >> 31) & 0x7fffffff;
+  if (!real) i = 0x7fffffff;
+  return (i & ~(Rp2 - 1)) | k;
+}
 // One robot's `nsteps` steps of a chunk: the block's base+msv loads are issued
 // first, the Philox draws (in registers) hide their latency, z is written once
 // for K5, then the RK4 steps run; positions go to the chunk's shared rows.
@@ -409,7 +468,8 @@ __device__ __forceinline__ double item_f64(const FitSmem<double>& sm, int s, int
 template <int KIND, bool FULL>
 __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, const float* bmp, float* zp, int RDU,
                                             uint64_t m, int kA, uint32_t g0, uint2 key, float* px, float* py, float* pz,
-                                            int RS, float* x, float& eff32, float& chk) {
+                                            int RS, float* x, float& eff32, float& chk, const float* ng, float ginv,
+                                            float& gsd) {
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
   float bq[kPF][DU];
 #pragma unroll
@@ -428,12 +488,18 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
   float nz[kPF * DU];
 #pragma unroll
   for (int g = 0; g < kPF * DU / 4; ++g) {
+#ifdef D4K_EXPERIMENT_CHEAP_RNG
+    const float h = __uint_as_float(((key.x ^ (uint32_t)m * 0x9E3779B9u ^ kA * 0x85EBCA6Bu ^ (g0 + g) * 0xC2B2AE35u) >> 9) | 0x3f800000u) - 1.5f;
+    const float4 v = make_float4(h, -h, 0.5f * h, -0.5f * h);
+#else
     const float4 v = philox_normals(key, m, (uint32_t)kA, g0 + g);
+#endif
     nz[4 * g] = v.x;
     nz[4 * g + 1] = v.y;
     nz[4 * g + 2] = v.z;
     nz[4 * g + 3] = v.w;
   }
+#ifndef D4K_EXPERIMENT_NO_ZSTORE
 #pragma unroll
   for (int j = 0; j < kPF; ++j) {
     if (FULL || j < nb) {
@@ -445,6 +511,7 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
       }
     }
   }
+#endif
 #pragma unroll
   for (int j = 0; j < kPF; ++j) {
     if (FULL || j < nb) {
@@ -461,6 +528,7 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
 #pragma unroll
       for (int q = 1; q < DX; ++q) s += x[q];
       chk = fmaf(s, 0.f, chk);
+      goal_acc<PD>(x, ng, ginv, gsd);
       px[j * RS] = x[0];
       py[j * RS] = x[1];
       if constexpr (PD == 3) pz[j * RS] = x[2];
@@ -470,25 +538,27 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
 
 template <int KIND>
 __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const FitSmem<float>& sm, int sA, int kA,
-                                               int64_t m, int t0, int nsteps, float* x, float* zrow, uint2 key,
-                                               float& eff32) {
+                                               int rA, int64_t m, int t0, int nsteps, float* x, float* zrow, uint2 key,
+                                               float& eff32, const float* ng, float ginv, float& gsd) {
   constexpr int DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
   const int RDU = p.R * DU;
   const int64_t e0 = ((int64_t)t0 * p.R + kA) * DU;
   const float* bmp = p.bm + e0;
   float* zp = zrow + e0;
-  float* px = sm.row(0, sA, 0) + kA;
-  float* py = sm.row(1, sA, 0) + kA;
-  float* pz = PD == 3 ? sm.row(2, sA, 0) + kA : px;
+  float* px = sm.row(0, sA, 0) + rA;
+  float* py = sm.row(1, sA, 0) + rA;
+  float* pz = PD == 3 ? sm.row(2, sA, 0) + rA : px;
   const int RS = sm.RS;
   float chk = 0.f;
   for (int tc = 0; tc < nsteps; tc += kPF) {
     const int nb = nsteps - tc;
     const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
     if (nb >= kPF) {
-      fused_block<KIND, true>(p, kPF, bmp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk);
+      fused_block<KIND, true>(p, kPF, bmp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk, ng,
+                              ginv, gsd);
     } else {
-      fused_block<KIND, false>(p, nb, bmp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk);
+      fused_block<KIND, false>(p, nb, bmp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk, ng,
+                               ginv, gsd);
     }
     bmp += kPF * RDU;
     zp += kPF * RDU;
@@ -538,31 +608,39 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
   sm.TC = TC;
   sm.spc = spc;
   sm.Rp = Rp;
+  sm.nthreads = nthreads;
   sm.pos = reinterpret_cast<S*>(smem_raw);
-  sm.goal = sm.pos + (size_t)PD * spc * TC * sm.RS;
-  sm.inv = sm.goal + (size_t)PD * Rp;
-  sm.obs = sm.inv + 2 * Rp;
   {
-    uintptr_t q = reinterpret_cast<uintptr_t>(sm.obs + 4 * (p.n_obs + 1));
-    q = (q + 15) & ~uintptr_t(15);
-    sm.red = reinterpret_cast<double*>(q);
+    const size_t pos_b = (size_t)PD * spc * TC * sm.RS * sizeof(S);
+    const size_t red_b = 2 * (size_t)nthreads * sizeof(double) + 2 * (size_t)nthreads * sizeof(int);
+    sm.red = reinterpret_cast<double*>(smem_raw);  // aliases pos: used after the last chunk only
     sm.eff = sm.red + nthreads;
     sm.cnt = reinterpret_cast<int*>(sm.eff + nthreads);
+    sm.obs = reinterpret_cast<S*>(smem_raw + (((pos_b > red_b ? pos_b : red_b) + 15) & ~size_t(15)));
   }
-  for (int j = tid; j < PD * Rp; j += nthreads) {
-    const int c = j / Rp, k = j % Rp;
-    const S g = k < R ? p.goals[k * PD + c] : S(0);
-    sm.goal[j] = F32 ? -g : g;
+  if constexpr (F32) {
+    sm.key = reinterpret_cast<int*>(sm.obs + 4 * (p.n_obs + 1));  // 16-B aligned (Rp % 4 == 0)
+    sm.bb = reinterpret_cast<float*>(sm.key + spc * Rp);
+    sm.ocl = sm.bb + 2 * (Rp / TB) * nthreads;
+    sm.goal = sm.inv = nullptr;
+    for (int j = tid; j < 4 * (p.n_obs + 1); j += nthreads) sm.obs[j] = p.obs[j];  // (−2c, |c|²−L²↑), pad row
+    for (int j = tid; j < 2 * (p.n_obs + 1); j += nthreads) sm.ocl[j] = p.obs_cull[j];
+  } else {
+    sm.goal = sm.obs + 4 * (p.n_obs + 1);
+    sm.inv = sm.goal + (size_t)PD * Rp;
+    sm.ocl = nullptr;
+    sm.key = nullptr;
+    sm.bb = nullptr;
+    for (int j = tid; j < PD * Rp; j += nthreads) {
+      const int c = j / Rp, k = j % Rp;
+      sm.goal[j] = k < R ? p.goals[k * PD + c] : S(0);
+    }
+    for (int k = tid; k < Rp; k += nthreads) {  // interleaved (‖s−g‖, valid)
+      sm.inv[2 * k] = k < R ? p.inv_dstart[k] : S(1);
+      sm.inv[2 * k + 1] = k < R ? S(1) : S(0);
+    }
+    for (int j = tid; j < 4 * p.n_obs; j += nthreads) sm.obs[j] = p.obs[j];  // (c, L²)
   }
-  for (int k = tid; k < Rp; k += nthreads) {  // interleaved (1/‖s−g‖ | ‖s−g‖, valid)
-    sm.inv[2 * k] = k < R ? p.inv_dstart[k] : (F32 ? S(0) : S(1));
-    sm.inv[2 * k + 1] = k < R ? S(1) : S(0);
-  }
-  for (int j = tid; j < 4 * p.n_obs; j += nthreads) {
-    const S v = p.obs[j];
-    sm.obs[j] = v;  // fp32: (−2c, |c|²−L²↑) precomputed on the host; fp64: (c, L²)
-  }
-  if (F32 && (p.n_obs & 1) && tid < 4) sm.obs[4 * p.n_obs + tid] = tid == 3 ? S(1.0e30) : S(0);  // never-hit pad
 
   // ---- phase-A identity: (sample sA, robot kA)
   const int sA = tid / Rp, kA = tid % Rp;
@@ -588,6 +666,16 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
   double effort = 0.0;
   float eff32 = 0.f;
   bool bad = false;
+  // fp32: the robot's goal term is accumulated here (Σ ‖p−g‖/‖s−g‖ per chunk)
+  float ng[3] = {0.f, 0.f, 0.f}, ginv = 0.f;
+  double goalA = 0.0;
+  if (F32 && robotA) {
+#pragma unroll
+    for (int c = 0; c < PD; ++c) ng[c] = -(float)p.goals[kA * PD + c];
+    ginv = (float)p.inv_dstart[kA];
+  }
+  int Rp2 = 1;
+  while (Rp2 < Rp) Rp2 <<= 1;
 
   // NOISE == 0: prefetch ring over the HBM noise stream + base/mean-scaled
   // variable (L2-resident).  NOISE == 1: the noise is drawn here in registers
@@ -627,6 +715,23 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
   __syncthreads();
 
   for (int t0 = 0; t0 < T; t0 += TC) {
+    // ===== fp32: rank the sample's robots by x at the chunk start; a robot's
+    // positions go to column rA, so TB-robot tiles are x-strips (culling)
+    int rA = kA;
+    if (F32 && p.cull) {
+      if (liveA) sm.key[tid] = chunk_key((float)x[0], kA, Rp2, robotA);
+      __syncthreads();
+      if (robotA) {
+        const int me = sm.key[tid];
+        const int4* kv = reinterpret_cast<const int4*>(sm.key + sA * Rp);
+        int r = 0;
+        for (int j = 0; j < Rp / 4; ++j) {
+          const int4 v = kv[j];
+          r += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
+        }
+        rA = r;
+      }
+    }
     // ===== phase A: integrate TC steps
     if constexpr (NOISE == 1) {
       if (robotA) {
@@ -634,10 +739,14 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
         float x0[DX];
 #pragma unroll
         for (int q = 0; q < DX; ++q) x0[q] = x[q];
-        const float chk = rollout_fused<KIND>(p, sm, sA, kA, p.m_global0 + mA, t0, nsteps, x, zst, key, eff32);
+        float gsd = 0.f;
+        const float chk = rollout_fused<KIND>(p, sm, sA, kA, rA, p.m_global0 + mA, t0, nsteps, x, zst, key, eff32,
+                                              ng, ginv, gsd);
+        goalA += (double)nsteps - (double)gsd;
         if (!(chk == 0.f)) rollout_check<KIND>(p, kA, p.m_global0 + mA, t0, nsteps, x0, zst);
       }
     } else if (robotA) {
+      float gsd = 0.f;
       const int t_end = t0 + TC < T ? t0 + TC : T;
 #pragma unroll
       for (int j = 0; j < kPF; ++j) fetch(t0 + j, t_end, j);
@@ -674,9 +783,10 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
                                              ((unsigned long long)kA << 10) | (unsigned long long)(t + 1);
               atomicMin(p.err, key);
             }
-            sm.row(0, sA, tc + j)[kA] = x[0];
-            sm.row(1, sA, tc + j)[kA] = x[1];
-            if constexpr (PD == 3) sm.row(2, sA, tc + j)[kA] = x[2];
+            if constexpr (F32) goal_acc<PD>(x, ng, ginv, gsd);
+            sm.row(0, sA, tc + j)[rA] = x[0];
+            sm.row(1, sA, tc + j)[rA] = x[1];
+            if constexpr (PD == 3) sm.row(2, sA, tc + j)[rA] = x[2];
             if (NOISE == 0 && p.states_out) {
               S* so = p.states_out + (mA * (int64_t)(T + 1) + t + 1) * R * DX + (int64_t)kA * DX;
 #pragma unroll
@@ -690,6 +800,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
           }
         }
       }
+      if constexpr (F32) goalA += (double)(t_end - t0) - (double)gsd;
     }
     effort += (double)eff32;  // per-chunk fp32 partial → fp64 accumulator
     eff32 = 0.f;
@@ -708,7 +819,8 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
           uint32_t cm[MAXW];
 #pragma unroll
           for (int w = 0; w < MAXW; ++w) cm[w] = 0;
-          gsum += (double)item_f32<PD, TB, MAXW>(sm, sB, tc, R, p.n_obs, p.margin_sq, qB, Q, cm, &nobs);
+          item_f32<PD, TB, MAXW>(sm, sB, tc, R, p.n_obs, p.margin_sq, p.cull != 0, p.cull_margin, qB, Q,
+                                 sm.bb + (tid - qB), cm, &nobs);
           // merge the Q lanes' conflict flags (adjacent lanes, same item)
           for (int off = 1; off < Q; off <<= 1) {
 #pragma unroll
@@ -730,7 +842,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
   }
 
   // ---- per-sample deterministic reduction
-  sm.red[tid] = liveB ? gsum : 0.0;
+  sm.red[tid] = (liveB ? gsum : 0.0) + (robotA ? goalA : 0.0);  // fp32 goal terms come from phase A
   sm.eff[tid] = robotA ? effort : 0.0;
   sm.cnt[2 * tid] = liveB ? nconf : 0;
   sm.cnt[2 * tid + 1] = liveB ? nobs : 0;
