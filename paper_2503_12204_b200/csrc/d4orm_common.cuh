@@ -67,6 +67,14 @@ __device__ __forceinline__ void deriv(const S* x, const S* u, S* f) {
 template <int KIND, typename S>
 __device__ __forceinline__ void rk4(S* x, const S* u, S dt, S half_dt, S dt6) {
   constexpr int DX = ModelDims<KIND>::DX;
+  if constexpr (std::is_same<S, float>::value && (KIND == HOLO2D_VEL || KIND == HOLO3D_VEL)) {
+    // fp32 throughput path, velocity-input models: the derivative is u at all
+    // four stages, so RK4 is x + dt·u (one FFMA; equal in exact arithmetic to
+    // the staged expression the fp64 path evaluates).
+#pragma unroll
+    for (int j = 0; j < DX; ++j) x[j] = fmaf(dt, u[j], x[j]);
+    return;
+  }
   S k1[DX], k2[DX], k3[DX], k4[DX], tmp[DX];
   deriv<KIND>(x, u, k1);
 #pragma unroll
@@ -159,11 +167,15 @@ __device__ __forceinline__ float u01_open(uint32_t x) {
   return __uint_as_float((x >> 9) | 0x3f800000u) - 0.99999994039535522461f;
 }
 
+// Box-Muller on the MUFU unit: r = √(−2 ln u) as √(−2 ln2 · log2 u), and the
+// angle 2π·u folded into one FFMA on the [1, 2) bit pattern.
 __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
-  const float v = -2.0f * __logf(u01_open(a));  // > 0
-  const float r = v * rsqrtf(v);
+  float l2;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u01_open(a)));
+  const float r = sqrt_approx(l2 * -1.38629436111989061883f);  // −2 ln u > 0
+  const float f = __uint_as_float((b >> 9) | 0x3f800000u);     // 1 + k·2^-23
   float s, c;
-  __sincosf(6.28318530717958647692f * u01_open(b), &s, &c);
+  __sincosf(fmaf(f, 6.28318530717958647692f, -6.28318530717958647692f), &s, &c);  // 2π·k·2^-23
   return make_float2(r * c, r * s);
 }
 
