@@ -309,3 +309,19 @@ def test_nccl_protocol_on_one_rank():
     assert ta == tb
     a.close()
     b.close()
+
+
+def test_philox_noise_matches_cpu_model(gpu):
+    """K1 / the fused draw against the numpy model (tests/philox_model.py,
+    itself pinned to the Philox4x32-10 known-answer vectors): the integer stream
+    is exact, so the normals agree to the MUFU approximations (~1e-6)."""
+    import philox_model
+    for case, seed, step, m0, count in [("C2", 123, 50, 0, 64), ("C4", 9, 1, 1000, 16), ("C3", 2**63 + 5, 99, 2**33, 8)]:
+        p = CASES[case]()
+        gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX)
+        gpu.set_problem(p)
+        z = gpu.philox_noise(seed, step, m0, count).reshape(count, p.horizon, p.robots, p.du)
+        ref = philox_model.normals(seed, step, m0, count, p.robots, p.horizon, p.du)
+        err = np.abs(z.astype(np.float64) - ref)
+        assert err.max() < 5e-5 * (1 + np.abs(ref).max()), (case, err.max())
+        assert np.median(err) < 1e-6
