@@ -120,6 +120,41 @@ int d4orm_cuda_set_noise_fn(d4orm_cuda_ctx* ctx, d4orm_noise_fn fn, void* user);
 int d4orm_cuda_run_denoising(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* config,
                              double* out_variable, d4orm_trace_rec* trace);
 
+/* ---- the caller of the path: the anytime loop solve (optimizer.cpp:49-102) --
+ * Every iteration runs on the device: seed and key table (K7), the denoising
+ * steps, the final fp64 rollout of base + delta, total_reward / objective /
+ * check_success and best-trajectory tracking (K6).  Philox mode replays one
+ * CUDA graph per iteration; the host reads back one record per iteration
+ * (stop_on_success and the deadline are decided as in optimizer.cpp:91-92).
+ * Replaces d4orm::solve (optimizer.hpp:31-32) for its caller run_trial
+ * (bench.cpp:61) / cmd_solve (tools/main.cpp:338). */
+typedef int (*d4orm_iteration_fn)(void* user, int iteration, uint64_t seed_it);
+typedef struct {
+  int max_iterations;               /* OptimizerConfig::max_iterations (>= 1) */
+  int stop_on_success;              /* OptimizerConfig::stop_on_success */
+  double deadline_seconds;          /* <= 0: no deadline */
+  d4orm_denoiser_config denoiser;   /* mode is forced to Deformation (optimizer.cpp:23) */
+  /* optional, called before iteration it (1-based) with seed_it =
+   * mix_seed(denoiser.seed, it): host-noise providers reseed here.  Non-zero
+   * aborts the solve. */
+  d4orm_iteration_fn on_iteration;
+  void* on_iteration_user;
+} d4orm_solve_config;
+
+/* IterationStats (result.hpp) */
+typedef struct {
+  double reward, objective;
+  int success;
+  double elapsed;                   /* seconds since the solve started */
+} d4orm_iteration_rec;
+
+/* best_states: (R*dx) x (T+1); best_controls: (R*du) x (T+1) (column T zero);
+ * per_iteration: max_iterations records; traces: max_iterations x steps
+ * records (may be NULL).  *success = check_success(best trajectory). */
+int d4orm_cuda_solve(d4orm_cuda_ctx* ctx, const d4orm_solve_config* config, double* best_states,
+                     double* best_controls, d4orm_iteration_rec* per_iteration, d4orm_trace_rec* traces,
+                     int* iterations_used, double* best_reward, int* success);
+
 /* ---- per-stage entry points (parity) -------------------------------------- */
 /* One denoising step i (loop body denoiser.cpp:152-180) from a given variable;
  * noise (batch x elems, fp64) or NULL for Philox. Outputs may be NULL. */

@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -25,6 +26,7 @@
 
 #include "../../include/d4orm_cuda.h"
 #include "d4orm_kernels.cuh"
+#include "k_outcome.cuh"
 
 namespace d4k {
 template <typename S, int KIND>
@@ -147,10 +149,19 @@ struct d4orm_cuda_ctx {
   std::string graph_key;
   std::vector<StepGraph> graphs;
 
+  // solve (K6/K7): trajectory buffers, device state, one graph per iteration
+  DevBuf<double> sv;
+  DevBuf<unsigned char> sst;
+  std::string iter_key;
+  cudaGraphExec_t iter_exec = nullptr;
+
   ~d4orm_cuda_ctx() {
     cudaSetDevice(device);
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (iter_exec) cudaGraphExecDestroy(iter_exec);
+    sv.release();
+    sst.release();
     for (auto* b : {&z[0], &z[1], &base, &msv, &bm, &starts_d, &goals_d, &inv_d, &obs_d, &ocl_d, &partial, &roots,
                     &states_out, &controls_out})
       b->release();
@@ -631,9 +642,17 @@ int prologue(d4orm_cuda_ctx* ctx, const RunShape& rs, const double* base_host, c
 }
 
 std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
-  char b[512];
-  snprintf(b, sizeof b, "%lld/%d/%.17g/%.17g/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p", (long long)rs.M, rs.N,
-           rs.abf, rs.lambda, ctx->precision, rs.mode, (void*)ctx->z[0].p, (void*)ctx->z[1].p, (void*)ctx->partial.p,
+  // the per-step constants (std, update scale) come from the schedule: key on
+  // its values, not only on (N, alpha_bar_final), since callers may pass their own
+  uint64_t h = 1469598103934665603ull;
+  for (double a : ctx->ab) {
+    uint64_t v;
+    std::memcpy(&v, &a, sizeof v);
+    h = (h ^ v) * 1099511628211ull;
+  }
+  char b[600];
+  snprintf(b, sizeof b, "%llx/%lld/%d/%.17g/%.17g/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p",
+           (unsigned long long)h, (long long)rs.M, rs.N, rs.abf, rs.lambda, ctx->precision, rs.mode, (void*)ctx->z[0].p, (void*)ctx->z[1].p, (void*)ctx->partial.p,
            (void*)ctx->base.p, (void*)ctx->msv.p, (void*)ctx->var.p, (void*)ctx->rewards.p, (void*)ctx->w64.p,
            (void*)ctx->w32.p, (void*)ctx->trace.p, (void*)ctx->keys.p, (void*)ctx->errw.p, (void*)ctx->roots.p);
   return b;
@@ -678,12 +697,17 @@ int run_steps(d4orm_cuda_ctx* ctx, const RunShape& rs, bool philox, int i_begin,
   return D4ORM_OK;
 }
 
+constexpr int kOutcomeKey = 0xFFE;  // K6 error key: the final rollout of an iteration
+
 int check_err(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   unsigned long long e = 0;
   CU(cudaMemcpy(&e, ctx->errw.p, sizeof e, cudaMemcpyDeviceToHost));
   if (e == ~0ull) return D4ORM_OK;
   if (e == 0xFFFFFFFFFFFFFFFEull) return fail(ctx, D4ORM_E_RUNTIME, "score_weights: non-finite reward");
   const int step_key = (int)(e >> 52);
+  if (step_key == kOutcomeKey)  // dynamics.cpp:81-84, thrown by rollout in iterate_impl (optimizer.cpp:28)
+    return fail(ctx, D4ORM_E_RUNTIME, "rollout: non-finite state for robot %d at step %d", (int)((e >> 10) & 1023),
+                (int)(e & 1023));
   const long long m = (long long)((e >> 20) & 0xFFFFFFFFull);
   const int k = (int)((e >> 10) & 1023), t = (int)(e & 1023);
   return fail(ctx, D4ORM_E_RUNTIME, "run_denoising: sample %lld at step %d: rollout: non-finite state for robot %d at step %d",
@@ -710,6 +734,213 @@ int run_denoising_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoise
     CU(cudaMemcpy(t.data(), ctx->trace.p, sizeof(double) * t.size(), cudaMemcpyDeviceToHost));
     for (int s = 0; s < rs.N; ++s) trace[s] = {(int)t[4 * s], t[4 * s + 1], t[4 * s + 2], t[4 * s + 3]};
   }
+  return D4ORM_OK;
+}
+
+// ------------------------------------------------------------------ solve
+// fp64 buffers of the device-side anytime loop (one allocation, `sv`) and its
+// state (`sst`, d4k::SolveState).
+struct SolveLayout {
+  size_t cur, states, vals, best_states, best_ctrl, rec, starts, goals, obsc, obsr, total;
+};
+SolveLayout solve_layout(const d4orm_problem& p, int max_it) {
+  SolveLayout L{};
+  const size_t E = (size_t)p.robots * p.du * p.horizon, NS = (size_t)(p.horizon + 1) * p.robots * p.dx;
+  L.cur = 0;
+  L.states = L.cur + E;
+  L.vals = L.states + NS;
+  L.best_states = L.vals + (size_t)p.horizon * p.robots;
+  L.best_ctrl = L.best_states + NS;
+  L.rec = L.best_ctrl + (size_t)(p.horizon + 1) * p.robots * p.du;
+  L.starts = L.rec + 4 * (size_t)max_it;
+  L.goals = L.starts + (size_t)p.robots * p.dx;
+  L.obsc = L.goals + (size_t)p.robots * p.pdim;
+  L.obsr = L.obsc + (size_t)p.n_obstacles * p.pdim;
+  L.total = L.obsr + (size_t)p.n_obstacles + 1;
+  return L;
+}
+
+template <typename S>
+cudaError_t launch_iter_begin(d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  const bool f64 = std::is_same<S, double>::value;
+  d4k::IterBeginParams<S> ip{};
+  ip.cur_ctrl = ctx->sv.p;  // SolveLayout::cur == 0
+  ip.base = (S*)ctx->base.p;
+  ip.msv = (S*)ctx->msv.p;
+  ip.bm = f64 ? nullptr : (S*)ctx->bm.p;
+  ip.var = ctx->var.p;
+  ip.E = rs.E;
+  ip.keys = ctx->keys.p;
+  ip.N = rs.N;
+  ip.st = reinterpret_cast<const d4k::SolveState*>(ctx->sst.p);
+  ip.err = ctx->errw.p;
+  const int64_t need = std::max<int64_t>(rs.E, rs.N + 1);
+  const unsigned g = (unsigned)std::min<int64_t>((need + 255) / 256, 148 * 8);
+  d4k::k_iter_begin<S><<<g, 256, 0, ctx->s_main>>>(ip);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_outcome(d4orm_cuda_ctx* ctx, int max_it) {
+  const d4orm_problem& p = ctx->prob;
+  const SolveLayout L = solve_layout(p, max_it);
+  double* sv = ctx->sv.p;
+  d4k::OutcomeParams op{};
+  op.ctrl = sv + L.cur;
+  op.var = ctx->var.p;
+  op.starts = sv + L.starts;
+  op.goals = sv + L.goals;
+  op.obs_c = sv + L.obsc;
+  op.obs_r = sv + L.obsr;
+  for (int d = 0; d < 3; ++d) {
+    op.lower[d] = p.lower[d];
+    op.upper[d] = p.upper[d];
+  }
+  op.dt = p.dt;
+  op.R = p.robots;
+  op.T = p.horizon;
+  op.O = p.n_obstacles;
+  op.w_t = p.w_t;
+  op.epsilon = p.epsilon;
+  op.robot_radius = p.robot_radius;
+  op.goal_tol = p.goal_tolerance;
+  op.w_o = p.obstacle_weight;
+  op.w_e = p.effort_weight;
+  op.states = sv + L.states;
+  op.vals = sv + L.vals;
+  op.best_states = sv + L.best_states;
+  op.best_ctrl = sv + L.best_ctrl;
+  op.rec = sv + L.rec;
+  op.st = reinterpret_cast<d4k::SolveState*>(ctx->sst.p);
+  op.step_key = kOutcomeKey;
+  op.err = ctx->errw.p;
+  switch (p.kind) {
+    case 0: d4k::k_outcome<0><<<1, 256, 0, ctx->s_main>>>(op); break;
+    case 1: d4k::k_outcome<1><<<1, 256, 0, ctx->s_main>>>(op); break;
+    case 2: d4k::k_outcome<2><<<1, 256, 0, ctx->s_main>>>(op); break;
+    case 3: d4k::k_outcome<3><<<1, 256, 0, ctx->s_main>>>(op); break;
+    case 4: d4k::k_outcome<4><<<1, 256, 0, ctx->s_main>>>(op); break;
+    default: d4k::k_outcome<5><<<1, 256, 0, ctx->s_main>>>(op); break;
+  }
+  return cudaGetLastError();
+}
+
+// One iteration: K7, the N denoising steps, K6.
+template <typename S>
+int enqueue_iteration(d4orm_cuda_ctx* ctx, const RunShape& rs, const d4orm_solve_config* sc, bool philox) {
+  CU(launch_iter_begin<S>(ctx, rs));
+  if (philox) {
+    for (int i = rs.N; i >= 1; --i)
+      if (int r = enqueue_step<S>(ctx, rs, i, true, false)) return r;
+  } else {
+    if (int r = run_steps<S>(ctx, rs, false, rs.N, 1, nullptr)) return r;
+  }
+  CU(launch_outcome(ctx, sc->max_iterations));
+  return D4ORM_OK;
+}
+
+template <typename S>
+int ensure_iter_graph(d4orm_cuda_ctx* ctx, const RunShape& rs, const d4orm_solve_config* sc) {
+  char extra[160];
+  snprintf(extra, sizeof extra, "|solve/%d/%p/%p", sc->max_iterations, (void*)ctx->sv.p, (void*)ctx->sst.p);
+  const std::string key = graph_key_of(ctx, rs) + extra;
+  if (ctx->iter_exec && key == ctx->iter_key) return D4ORM_OK;
+  if (ctx->iter_exec) cudaGraphExecDestroy(ctx->iter_exec);
+  ctx->iter_exec = nullptr;
+  cudaGraph_t g;
+  CU(cudaStreamBeginCapture(ctx->s_main, cudaStreamCaptureModeThreadLocal));
+  int r = enqueue_iteration<S>(ctx, rs, sc, true);
+  cudaError_t e = cudaStreamEndCapture(ctx->s_main, &g);
+  if (r) return r;
+  CU(e);
+  CU(cudaGraphInstantiate(&ctx->iter_exec, g, 0));
+  CU(cudaGraphDestroy(g));
+  ctx->iter_key = key;
+  return D4ORM_OK;
+}
+
+template <typename S>
+int solve_t(d4orm_cuda_ctx* ctx, const d4orm_solve_config* sc, double* best_states, double* best_controls,
+            d4orm_iteration_rec* per_it, d4orm_trace_rec* traces, int* used, double* best_reward, int* success) {
+  if (!ctx->has_problem) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: set_problem not called");
+  if (sc->max_iterations < 1) return fail(ctx, D4ORM_E_INVALID, "solve: max_iterations must be >= 1");
+  if (ctx->prob.horizon < 2) return fail(ctx, D4ORM_E_INVALID, "solve: horizon must be >= 2");
+  if (!(ctx->prob.dt > 0.0)) return fail(ctx, D4ORM_E_INVALID, "solve: dt must be positive");
+  const auto t0 = std::chrono::steady_clock::now();
+  auto elapsed = [&t0] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+  d4orm_denoiser_config dc = sc->denoiser;
+  dc.mode = D4ORM_DEFORMATION;  // optimizer.cpp:23
+  RunShape rs;
+  if (int r = check_config(ctx, &dc, &rs)) return r;
+  const bool philox = ctx->noise_source == D4ORM_NOISE_PHILOX;
+  if (!philox && !ctx->noise_fn)
+    return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: host noise selected but no noise fn set");
+  if (int r = ensure_buffers(ctx, rs, false)) return r;
+  const d4orm_problem& p = ctx->prob;
+  const SolveLayout L = solve_layout(p, sc->max_iterations);
+  CU(ctx->sv.ensure(L.total));
+  CU(ctx->sst.ensure(sizeof(d4k::SolveState)));
+  {
+    // problem constants (fp64) and the initial trajectory's executed controls:
+    // rollout of zero controls (optimizer.cpp:64-68) executes clamp(0)
+    std::vector<double> h(L.total - L.cur, 0.0);
+    for (int t = 0; t < p.horizon; ++t)
+      for (int k = 0; k < p.robots; ++k)
+        for (int d = 0; d < p.du; ++d) {
+          double v = 0.0;
+          v = (v < p.lower[d]) ? p.lower[d] : v;
+          v = (p.upper[d] < v) ? p.upper[d] : v;
+          h[((size_t)t * p.robots + k) * p.du + d] = v;
+        }
+    std::copy(ctx->starts.begin(), ctx->starts.end(), h.begin() + L.starts);
+    std::copy(ctx->goals.begin(), ctx->goals.end(), h.begin() + L.goals);
+    std::copy(ctx->obs_c.begin(), ctx->obs_c.end(), h.begin() + L.obsc);
+    std::copy(ctx->obs_r.begin(), ctx->obs_r.end(), h.begin() + L.obsr);
+    CU(cudaMemcpyAsync(ctx->sv.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, ctx->s_main));
+    const d4k::SolveState st0{0, -1, 0, 0, -INFINITY, sc->denoiser.seed};
+    CU(cudaMemcpyAsync(ctx->sst.p, &st0, sizeof st0, cudaMemcpyHostToDevice, ctx->s_main));
+    CU(cudaStreamSynchronize(ctx->s_main));
+  }
+  const bool graphs = philox && ctx->use_graphs;
+  if (graphs) {
+    if (int r = ensure_iter_graph<S>(ctx, rs, sc)) return r;
+  }
+  int it_used = 0;
+  std::vector<double> rec(4), tr((size_t)4 * rs.N);
+  for (int it = 1; it <= sc->max_iterations; ++it) {
+    const uint64_t seed_it = mix_seed(sc->denoiser.seed, (uint64_t)it);
+    if (sc->on_iteration && sc->on_iteration(sc->on_iteration_user, it, seed_it) != 0)
+      return fail(ctx, D4ORM_E_RUNTIME, "solve: iteration callback failed at iteration %d", it);
+    if (graphs) {
+      CU(cudaGraphLaunch(ctx->iter_exec, ctx->s_main));
+    } else {
+      if (int r = enqueue_iteration<S>(ctx, rs, sc, philox)) return r;
+    }
+    CU(cudaStreamSynchronize(ctx->s_main));
+    if (int r = check_err(ctx, rs)) return r;
+    CU(cudaMemcpy(rec.data(), ctx->sv.p + L.rec + 4 * (size_t)(it - 1), sizeof(double) * 4, cudaMemcpyDeviceToHost));
+    if (traces) {
+      CU(cudaMemcpy(tr.data(), ctx->trace.p, sizeof(double) * tr.size(), cudaMemcpyDeviceToHost));
+      for (int s = 0; s < rs.N; ++s)
+        traces[(size_t)(it - 1) * rs.N + s] = {(int)tr[4 * s], tr[4 * s + 1], tr[4 * s + 2], tr[4 * s + 3]};
+    }
+    const bool ok = rec[2] != 0.0;
+    if (per_it) per_it[it - 1] = {rec[0], rec[1], ok ? 1 : 0, elapsed()};
+    it_used = it;
+    if (sc->stop_on_success && ok) break;
+    if (sc->deadline_seconds > 0 && elapsed() >= sc->deadline_seconds) break;
+  }
+  d4k::SolveState st{};
+  CU(cudaMemcpy(&st, ctx->sst.p, sizeof st, cudaMemcpyDeviceToHost));
+  if (best_states)
+    CU(cudaMemcpy(best_states, ctx->sv.p + L.best_states, sizeof(double) * (L.best_ctrl - L.best_states),
+                  cudaMemcpyDeviceToHost));
+  if (best_controls)
+    CU(cudaMemcpy(best_controls, ctx->sv.p + L.best_ctrl, sizeof(double) * (L.rec - L.best_ctrl),
+                  cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(rec.data(), ctx->sv.p + L.rec + 4 * (size_t)st.best_iter, sizeof(double) * 4, cudaMemcpyDeviceToHost));
+  if (used) *used = it_used;
+  if (best_reward) *best_reward = st.best_reward;
+  if (success) *success = rec[2] != 0.0 ? 1 : 0;  // check_success of the best trajectory (optimizer.cpp:97)
   return D4ORM_OK;
 }
 
@@ -846,6 +1077,18 @@ int d4orm_cuda_run_denoising(d4orm_cuda_ctx* ctx, const double* base, const d4or
   CU(cudaSetDevice(ctx->device));
   return ctx->precision == D4ORM_PREC_F64 ? run_denoising_t<double>(ctx, base, config, out_variable, trace)
                                           : run_denoising_t<float>(ctx, base, config, out_variable, trace);
+}
+
+int d4orm_cuda_solve(d4orm_cuda_ctx* ctx, const d4orm_solve_config* config, double* best_states,
+                     double* best_controls, d4orm_iteration_rec* per_iteration, d4orm_trace_rec* traces,
+                     int* iterations_used, double* best_reward, int* success) {
+  CU(cudaSetDevice(ctx->device));
+  if (!config) return fail(ctx, D4ORM_E_INVALID, "solve: null config");
+  return ctx->precision == D4ORM_PREC_F64
+             ? solve_t<double>(ctx, config, best_states, best_controls, per_iteration, traces, iterations_used,
+                               best_reward, success)
+             : solve_t<float>(ctx, config, best_states, best_controls, per_iteration, traces, iterations_used,
+                              best_reward, success);
 }
 
 extern "C++" template <typename S>

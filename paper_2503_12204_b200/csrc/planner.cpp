@@ -664,6 +664,17 @@ JointTrajectory iterate(const JointTrajectory& base, const Scenario& scenario, c
   return iterate_impl(base, scenario, model, schedule, config.denoiser, base.dt).trajectory;
 }
 
+namespace {
+int reseed_host_noise(void* user, int, std::uint64_t seed_it) {  // seed of iteration it (optimizer.cpp:76)
+  static_cast<HostNoise*>(user)->seed = seed_it;
+  return 0;
+}
+}  // namespace
+
+// The anytime loop on the device (d4orm_cuda_solve): every iteration's
+// denoising, final rollout, total_reward / objective / check_success and best
+// tracking run in one CUDA graph; the host reads one record per iteration and
+// decides stop_on_success / the deadline exactly where optimizer.cpp:91-92 does.
 SolveResult solve(const Scenario& scenario, const DynamicsModel& model, const OptimizerConfig& config) {
   if (config.max_iterations < 1) throw std::invalid_argument("solve: max_iterations must be >= 1");
   if (config.horizon < 2) throw std::invalid_argument("solve: horizon must be >= 2");
@@ -672,35 +683,55 @@ SolveResult solve(const Scenario& scenario, const DynamicsModel& model, const Op
   check_model(scenario, model);
   const NoiseSchedule schedule = make_schedule(config.denoiser.steps, config.denoiser.alpha_bar_final);
   const auto t0 = std::chrono::steady_clock::now();
-  const auto elapsed = [&t0] {
-    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-  };
-  JointTrajectory current = rollout(model, scenario.starts,
-                                    JointControls::zeros(scenario.robots, model.control_dim, config.horizon), config.dt);
-  SolveResult result;
-  int best_iteration = -1;
-  for (int it = 1; it <= config.max_iterations; ++it) {
-    DenoiserConfig dc = config.denoiser;
-    dc.seed = mix_seed(config.denoiser.seed, static_cast<std::uint64_t>(it));
-    IterateOutcome out = iterate_impl(current, scenario, model, schedule, dc, config.dt);
-    current = std::move(out.trajectory);
-    const double reward = total_reward(current, scenario);
-    const double quality = objective(current, scenario);
-    const SuccessReport report = check_success(current, scenario);
-    result.per_iteration.push_back({reward, quality, report.success, elapsed()});
-    result.traces.push_back(std::move(out.trace));
-    if (best_iteration < 0 || reward > result.best_reward) {
-      result.best_reward = reward;
-      result.best_trajectory = current;
-      best_iteration = it;
-    }
-    if (config.stop_on_success && report.success) break;
-    if (config.deadline_seconds && elapsed() >= *config.deadline_seconds) break;
+  const DenoiserConfig& dcfg = config.denoiser;
+  if (dcfg.batch < 2) throw std::invalid_argument("run_denoising: batch must be >= 2");
+  if (!(dcfg.lambda > 0.0)) throw std::invalid_argument("run_denoising: lambda must be > 0");
+  const ProblemArrays pa = make_problem(scenario, model, config.horizon, config.dt);
+  const bool host = g_opts.host_noise;
+  d4orm_cuda_ctx* c = gpu(0, pa, g_opts.precision, host ? D4ORM_NOISE_HOST : D4ORM_NOISE_PHILOX, g_opts.graphs);
+  if (host) {
+    g_noise = {dcfg.seed, dcfg.workers};
+    throw_for(d4orm_cuda_set_noise_fn(c, host_noise_fn, &g_noise), d4orm_cuda_last_error(c));
   }
-  result.iterations_used = static_cast<int>(result.per_iteration.size());
-  result.total_denoise_steps = static_cast<long long>(result.iterations_used) * config.denoiser.steps;
-  result.success = check_success(result.best_trajectory, scenario).success;
-  result.wall_time = elapsed();
+  d4orm_solve_config sc{};
+  sc.max_iterations = config.max_iterations;
+  sc.stop_on_success = config.stop_on_success ? 1 : 0;
+  sc.deadline_seconds = config.deadline_seconds ? *config.deadline_seconds : 0.0;
+  sc.denoiser.steps = dcfg.steps;
+  sc.denoiser.batch = dcfg.batch;
+  sc.denoiser.lambda = dcfg.lambda;
+  sc.denoiser.alpha_bar_final = dcfg.alpha_bar_final;
+  sc.denoiser.seed = dcfg.seed;
+  sc.denoiser.mode = D4ORM_DEFORMATION;
+  sc.denoiser.alpha_bar = schedule.alpha_bar.data();
+  sc.on_iteration = host ? reseed_host_noise : nullptr;
+  sc.on_iteration_user = &g_noise;
+  const int R = scenario.robots, H = config.horizon;
+  SolveResult result;
+  result.best_trajectory = {R, model.state_dim, model.control_dim, config.dt,
+                            Matrix(static_cast<Index>(R) * model.state_dim, H + 1),
+                            Matrix(static_cast<Index>(R) * model.control_dim, H + 1)};
+  std::vector<d4orm_iteration_rec> recs(static_cast<size_t>(config.max_iterations));
+  std::vector<d4orm_trace_rec> tr(static_cast<size_t>(config.max_iterations) * dcfg.steps);
+  int used = 0, ok = 0;
+  double best = 0.0;
+  throw_for(d4orm_cuda_solve(c, &sc, result.best_trajectory.states.data(), result.best_trajectory.controls.data(),
+                             recs.data(), tr.data(), &used, &best, &ok),
+            d4orm_cuda_last_error(c));
+  for (int it = 0; it < used; ++it) {
+    result.per_iteration.push_back({recs[it].reward, recs[it].objective, recs[it].success != 0, recs[it].elapsed});
+    DenoiseTrace t;
+    for (int s = 0; s < dcfg.steps; ++s) {
+      const d4orm_trace_rec& r = tr[static_cast<size_t>(it) * dcfg.steps + s];
+      t.steps.push_back({r.step, r.best_reward, r.mean_reward, r.weight_entropy});
+    }
+    result.traces.push_back(std::move(t));
+  }
+  result.best_reward = best;
+  result.success = ok != 0;
+  result.iterations_used = used;
+  result.total_denoise_steps = static_cast<long long>(used) * dcfg.steps;
+  result.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return result;
 }
 

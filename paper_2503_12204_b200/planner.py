@@ -7,7 +7,7 @@ reference's operators with the same argument meaning and error behaviour:
   denoise_step    one loop body        denoiser.cpp:152-180 (teacher-forced)
   rollout_fitness rollout + total_reward  dynamics.cpp:122-169, reward.cpp:67-130
   score_weights   denoiser.cpp:50-90 (+ weight_entropy :24-30)
-  solve           optimizer.cpp:48-102 (anytime loop; per-iteration outcome on GPU)
+  solve           optimizer.cpp:48-102 (anytime loop, every iteration on the device)
 
 Arrays use the reference's layouts: a joint control sequence is (T, R, du)
 C-contiguous == Eigen (R*du) x T column-major.
@@ -194,39 +194,49 @@ class GpuDenoiser:
 
     # ---------------------------------------------------------- anytime loop
     def solve(self, cfg: DenoiserConfig, max_iterations: int = 10, stop_on_success: bool = True,
-              deadline_seconds: float | None = None):
-        """solve (optimizer.cpp:48-102): zero-control start, per-iteration seed
-        mix_seed(seed, it), denoise a deformation, roll out base+Δ, keep the
-        best-reward iterate.  Outcome per iteration via the GPU rollout."""
-        from .scenarios import mix_seed
-        from .outcome import check_success, objective
+              deadline_seconds: float | None = None, on_iteration=None):
+        """solve (optimizer.cpp:48-102) on the device (d4orm_cuda_solve): zero-
+        control start, per-iteration seed mix_seed(seed, it), denoise a
+        deformation, fp64 rollout of base+Δ, total_reward / objective /
+        check_success and best tracking in K6; one CUDA graph per iteration in
+        Philox mode.  on_iteration(it, seed_it) runs before each iteration (host
+        noise providers reseed there)."""
         if max_iterations < 1:
             raise ValueError("solve: max_iterations must be >= 1")
         p = self.problem
+        sc = _lib.SolveConfig_C()
+        sc.max_iterations = max_iterations
+        sc.stop_on_success = int(stop_on_success)
+        sc.deadline_seconds = float(deadline_seconds) if deadline_seconds is not None else 0.0
+        sc.denoiser = cfg.c()
+        cb = None
+        if on_iteration is not None:
+            def _cb(user, it, seed_it):
+                try:
+                    on_iteration(it, seed_it)
+                    return 0
+                except Exception:
+                    return 1
+            cb = _lib.ITER_FN(_cb)
+            sc.on_iteration = cb
+        best_states = np.empty((p.horizon + 1, p.robots, p.dx))
+        best_controls = np.empty((p.horizon + 1, p.robots, p.du))
+        recs = (_lib.IterationRec_C * max_iterations)()
+        traces = (TraceRec_C * (max_iterations * cfg.steps))()
+        used, ok = C.c_int(), C.c_int()
+        best = C.c_double()
         t0 = time.perf_counter()
-        states, controls, rw, _ = self.rollout_fitness(np.zeros((1,) + self._shape()))
-        current_controls = controls[0, :p.horizon]
+        self._check(self._L.d4orm_cuda_solve(self._h, C.byref(sc), dptr(best_states), dptr(best_controls), recs,
+                                             traces, C.byref(used), C.byref(best), C.byref(ok)))
         result = SolveResult()
-        best_it = -1
-        for it in range(1, max_iterations + 1):
-            c = DenoiserConfig(cfg.steps, cfg.batch, cfg.lam, cfg.alpha_bar_final, mix_seed(cfg.seed, it), DEFORMATION)
-            delta, trace = self.run_denoising(current_controls, c)
-            states, controls, rw, _ = self.rollout_fitness((current_controls + delta)[None])
-            current_controls = controls[0, :p.horizon]
-            reward = float(rw[0])
-            ok, msg = check_success(p, states[0])
-            result.per_iteration.append((reward, objective(p, states[0]), ok, time.perf_counter() - t0))
-            result.traces.append(trace)
-            if best_it < 0 or reward > result.best_reward:
-                result.best_reward, result.best_states, result.best_controls = reward, states[0], controls[0]
-                best_it = it
-            if stop_on_success and ok:
-                break
-            if deadline_seconds is not None and time.perf_counter() - t0 >= deadline_seconds:
-                break
-        result.iterations_used = len(result.per_iteration)
-        result.total_denoise_steps = result.iterations_used * cfg.steps
-        result.success = check_success(p, result.best_states)[0]
+        result.iterations_used = used.value
+        result.total_denoise_steps = used.value * cfg.steps
+        result.per_iteration = [(r.reward, r.objective, bool(r.success), r.elapsed) for r in recs[: used.value]]
+        result.traces = [[(t.step, t.best_reward, t.mean_reward, t.weight_entropy)
+                          for t in traces[i * cfg.steps:(i + 1) * cfg.steps]] for i in range(used.value)]
+        result.best_reward = best.value
+        result.best_states, result.best_controls = best_states, best_controls
+        result.success = bool(ok.value)
         result.wall_time = time.perf_counter() - t0
         return result
 

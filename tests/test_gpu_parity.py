@@ -325,3 +325,53 @@ def test_philox_noise_matches_cpu_model(gpu):
         err = np.abs(z.astype(np.float64) - ref)
         assert err.max() < 5e-5 * (1 + np.abs(ref).max()), (case, err.max())
         assert np.median(err) < 1e-6
+
+
+@pytest.mark.parametrize("case", ["holo2d", "C2", "C3"])
+def test_device_solve_matches_oracle(gpu, oracle, case):
+    """The anytime loop on the device (K7 + steps + K6 per iteration) against
+    the oracle's solve (optimizer.cpp:49-102) in correctness mode: same noise,
+    fp64; the final rollout, total_reward, objective and check_success are
+    computed in the reference's own order, so they agree to the Δ parity."""
+    p = CASES[case]()
+    N, M, seed, its = 6, 256, 7, 3
+    cfg = d4.DenoiserConfig(steps=N, batch=M, seed=seed)
+    cur = {"seed": None}
+    gpu.set_options(d4.PREC_F64, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    gpu.set_noise_provider(lambda step, m0, count, elems: oracle.step_noise(cur["seed"], step, m0, count, elems))
+    res = gpu.solve(cfg, max_iterations=its, stop_on_success=False,
+                    on_iteration=lambda it, seed_it: cur.__setitem__("seed", seed_it))
+    ref = oracle.solve(p, make_config(N, M, seed=seed), max_iterations=its, stop_on_success=False)
+    assert res.iterations_used == ref["iterations"] == its
+    for a, b in zip(res.per_iteration, ref["per_iteration"]):
+        assert abs(a[0] - b[0]) < 1e-9 and a[1] == b[1] and a[2] == b[2]
+    assert abs(res.best_reward - ref["best_reward"]) < 1e-9
+    assert res.success == ref["success"]
+    np.testing.assert_allclose(res.best_states, ref["states"], rtol=1e-9, atol=1e-9)
+    np.testing.assert_allclose(res.best_controls, ref["controls"], rtol=1e-9, atol=1e-9)
+    assert len(res.traces) == its and len(res.traces[0]) == N
+
+
+def test_device_solve_philox_stops_on_success(gpu):
+    """Throughput mode: Philox noise, one graph per iteration.  Deterministic
+    for a seed; stop_on_success ends the loop at the first collision-free,
+    goal-reaching iterate (C1-style swap that is reachable)."""
+    p = S.antipodal_circle(4, 4.0, S.HOLO2D_VEL, robot_radius=0.1, horizon=48, lower=[-1, -1], upper=[1, 1])
+    cfg = d4.DenoiserConfig(steps=40, batch=1024, seed=3)
+    gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX)
+    gpu.set_problem(p)
+    r1 = gpu.solve(cfg, max_iterations=8, stop_on_success=True)
+    r2 = gpu.solve(cfg, max_iterations=8, stop_on_success=True)
+    assert r1.iterations_used == r2.iterations_used
+    assert r1.best_reward == r2.best_reward
+    np.testing.assert_array_equal(r1.best_states, r2.best_states)
+    rewards = [it[0] for it in r1.per_iteration]
+    assert r1.best_reward == max(rewards)
+    if r1.success:
+        assert r1.per_iteration[-1][2] and not any(it[2] for it in r1.per_iteration[:-1])
+    # the device outcome equals the host restatement on the returned trajectory
+    from paper_2503_12204_b200.outcome import check_success, objective
+    assert check_success(p, r1.best_states)[0] == r1.success
+    best_it = rewards.index(r1.best_reward)
+    assert objective(p, r1.best_states) == r1.per_iteration[best_it][1]
