@@ -15,6 +15,8 @@ value    rollouts+fitness evaluations/s with inputs resident in HBM (device
          CUDA-event timing of exactly K steps, max over ranks)
 e2e      the same metric through the public C-ABI call d4orm_cuda_run_denoising
          with host buffers (H2D base, D2H variable+trace inside the region)
+solve    the same metric through d4orm_cuda_solve (the anytime loop, every
+         iteration on the device), the config's iteration count
 roofline dominant kernel K2+K3 (rollout+fitness), FP32-bound: algorithmic
          FLOPs per launch / its CUDA-event launch time, against the
          FP32 peak measured live on this GPU (d4orm_cuda_fp32_peak)
@@ -251,6 +253,21 @@ def main():
                "step": f"one run_denoising call = {cfg.steps} denoising steps, host base in, host variable+trace out",
                "ms_per_call": dt * 1e3}
 
+    # the anytime loop (solve, optimizer.cpp:49-102) on the device: every
+    # iteration's denoising + final rollout/outcome in one graph per iteration
+    solve = None
+    if not args.no_e2e:
+        g.solve(cfg, max_iterations=rc.iterations, stop_on_success=False)  # graph build (untimed)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        sr = g.solve(cfg, max_iterations=rc.iterations, stop_on_success=False)
+        dt = reduce_max(dist, time.perf_counter() - t0)
+        solve = {"value": M * cfg.steps * sr.iterations_used / dt, "unit": UNIT, "iterations": sr.iterations_used,
+                 "wall_ms": dt * 1e3, "best_reward": sr.best_reward, "success": sr.success,
+                 "call": "d4orm_cuda_solve: max_iterations=%d, stop_on_success=false (SURVEY 8d throughput runs)"
+                         % rc.iterations}
+
     F = algorithmic_flops_per_eval(p)
     k23_ms = kms[1]
     achieved = Ml * F / (k23_ms * 1e-3) / 1e12
@@ -277,6 +294,8 @@ def main():
     }
     if e2e:
         line["e2e"] = e2e
+    if solve:
+        line["solve"] = solve
     if rank == 0 and world == 1 and not args.no_cpu:
         ref, kind, what = reference_checker()
         batch, t = size_cpu_sample(ref, p, M, 2.0)
