@@ -148,12 +148,44 @@ typedef struct {
   double elapsed;                   /* seconds since the solve started */
 } d4orm_iteration_rec;
 
+/* ---- the paper's baselines on the same kernels (baselines.cpp:99-173) ------
+ * MPPI: samples mean + sigma*z, softmax weights (score_weights), mc_average;
+ * CEM: samples mean + std.*z, the elite fraction by a stable descending sort
+ * of the rewards (select_elites), diagonal Gaussian refit with a std floor.
+ * Every iteration (one CUDA graph in Philox mode) ends with K6 on the mean:
+ * fp64 rollout, total_reward / objective / check_success, best tracking.
+ * Host noise: the provider's `step` is the iteration (stream
+ * mix_seed(seed, it, m)).  Replace mppi_solve / cem_solve (baselines.hpp:46-50). */
+typedef struct {                    /* MppiConfig (baselines.hpp:16-27); horizon/dt from the problem */
+  int64_t batch;
+  double lambda, sigma;
+  int iterations;
+  uint64_t seed;
+  int stop_on_success;
+  double deadline_seconds;          /* <= 0: none */
+} d4orm_mppi_config;
+
+typedef struct {                    /* CemConfig (baselines.hpp:31-43) */
+  int64_t batch;
+  double elite_fraction, initial_std, min_std;
+  int iterations;
+  uint64_t seed;
+  int stop_on_success;
+  double deadline_seconds;
+} d4orm_cem_config;
+
 /* best_states: (R*dx) x (T+1); best_controls: (R*du) x (T+1) (column T zero);
  * per_iteration: max_iterations records; traces: max_iterations x steps
  * records (may be NULL).  *success = check_success(best trajectory). */
 int d4orm_cuda_solve(d4orm_cuda_ctx* ctx, const d4orm_solve_config* config, double* best_states,
                      double* best_controls, d4orm_iteration_rec* per_iteration, d4orm_trace_rec* traces,
                      int* iterations_used, double* best_reward, int* success);
+int d4orm_cuda_mppi_solve(d4orm_cuda_ctx* ctx, const d4orm_mppi_config* config, double* best_states,
+                          double* best_controls, d4orm_iteration_rec* per_iteration, int* iterations_used,
+                          double* best_reward, int* success);
+int d4orm_cuda_cem_solve(d4orm_cuda_ctx* ctx, const d4orm_cem_config* config, double* best_states,
+                         double* best_controls, d4orm_iteration_rec* per_iteration, int* iterations_used,
+                         double* best_reward, int* success);
 
 /* ---- per-stage entry points (parity) -------------------------------------- */
 /* One denoising step i (loop body denoiser.cpp:152-180) from a given variable;

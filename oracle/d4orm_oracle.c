@@ -747,3 +747,215 @@ out:
   free(delta);
   return rc;
 }
+
+/* ------------------------------------------------------------ baselines */
+/* MPPI and CEM in the joint control space (baselines.cpp:19-173): the same
+ * rollout / total_reward / score_weights / mc_average pieces, no schedule. */
+
+typedef struct {
+  const or_problem* p;
+  const double* mean;
+  const double* stdv;   /* CEM: per-element std; NULL → MPPI scalar sigma */
+  double sigma;
+  uint64_t seed;
+  int it;
+  int64_t elems;
+  double* samples;      /* batch x elems */
+  double* rewards;
+  int* failed;
+  char (*errs)[160];
+} base_ctx;
+
+static void base_sample_one(int64_t m, void* c) {
+  base_ctx* b = (base_ctx*)c;
+  double* out = b->samples + m * b->elems;
+  /* normal_matrix with stream mix_seed(seed, iteration, m) (baselines.cpp:116-119,152-155) */
+  or_normal_fill(or_mix_seed3(b->seed, (uint64_t)b->it, (uint64_t)m), out, b->elems);
+  for (int64_t e = 0; e < b->elems; ++e)  /* mean.u + sigma*z | mean.u + std.cwiseProduct(z) */
+    out[e] = b->stdv ? b->mean[e] + b->stdv[e] * out[e] : b->mean[e] + b->sigma * out[e];
+}
+
+static void base_eval_one(int64_t m, void* c) {  /* evaluate_batch (baselines.cpp:30-38) */
+  base_ctx* b = (base_ctx*)c;
+  const or_problem* p = b->p;
+  double* states = (double*)malloc(sizeof(double) * (size_t)p->robots * p->dx * (p->horizon + 1));
+  int br = 0, bs = 0;
+  if (or_rollout(p, b->samples + m * b->elems, states, NULL, &br, &bs) != 0) {
+    b->failed[m] = 1;
+    snprintf(b->errs[m], 160, "rollout: non-finite state for robot %d at step %d", br, bs);
+  } else if (or_total_reward(p, states, &b->rewards[m], NULL, NULL) != 0) {
+    b->failed[m] = 1;
+    snprintf(b->errs[m], 160, "%s", g_err);
+  }
+  free(states);
+}
+
+static int base_evaluate(base_ctx* b, int64_t M, int workers) {
+  parallel_for(M, workers, base_sample_one, b);
+  parallel_for(M, workers, base_eval_one, b);
+  for (int64_t m = 0; m < M; ++m)
+    if (b->failed[m]) { set_err("%s", b->errs[m]); return 1; }
+  return 0;
+}
+
+/* run_anytime's per-iteration bookkeeping (baselines.cpp:45-75) on `mean`. */
+typedef struct {
+  double* states;
+  double* controls;
+  int best_it, used;
+  double t0;
+} anytime_ctx;
+
+static int anytime_record(const or_problem* p, anytime_ctx* a, const double* mean, int it,
+                          double* best_states, double* best_controls, double* best_reward,
+                          or_iteration_stats* per_it, int* ok_out) {
+  const size_t ns = (size_t)p->robots * p->dx * (p->horizon + 1), nc = (size_t)p->robots * p->du * (p->horizon + 1);
+  if (or_rollout(p, mean, a->states, a->controls, NULL, NULL)) return 1;
+  double reward;
+  or_total_reward(p, a->states, &reward, NULL, NULL);
+  const double quality = or_objective(p, a->states);
+  const int ok = or_check_success(p, a->states, NULL, 0);
+  if (per_it) per_it[it - 1] = (or_iteration_stats){reward, quality, ok, now_s() - a->t0};
+  a->used = it;
+  if (a->best_it < 0 || reward > *best_reward) {
+    *best_reward = reward;
+    memcpy(best_states, a->states, sizeof(double) * ns);
+    if (best_controls) memcpy(best_controls, a->controls, sizeof(double) * nc);
+    a->best_it = it;
+  }
+  *ok_out = ok;
+  return 0;
+}
+
+static int check_base_problem(const or_problem* p, int64_t batch, const char* what) {
+  if (p->horizon < 2) { set_err("%s: horizon must be >= 2", what); return 1; }
+  if (!(p->dt > 0.0)) { set_err("%s: dt must be positive", what); return 1; }
+  if (batch < 2) { set_err("%s: batch must be >= 2", what); return 1; }
+  return 0;
+}
+
+static const double* g_elite_r;
+static int elite_cmp(const void* a, const void* b) {  /* reward descending, index ascending */
+  const int i = *(const int*)a, j = *(const int*)b;
+  const double ri = g_elite_r[i], rj = g_elite_r[j];
+  if (ri > rj) return -1;
+  if (rj > ri) return 1;
+  return (i > j) - (i < j);
+}
+static int int_cmp(const void* a, const void* b) {
+  const int i = *(const int*)a, j = *(const int*)b;
+  return (i > j) - (i < j);
+}
+
+/* select_elites (baselines.cpp:86-97): stable sort by reward descending (ties →
+ * lower index first), keep `count`, return them in ascending index order. */
+int or_select_elites(const double* rewards, int64_t m, int count, int* out) {
+  if (count < 1 || count > m) { set_err("select_elites: elite count out of range"); return 1; }
+  int* order = (int*)malloc(sizeof(int) * (size_t)m);
+  for (int64_t i = 0; i < m; ++i) order[i] = (int)i;
+  g_elite_r = rewards;  /* not re-entrant: test infrastructure */
+  qsort(order, (size_t)m, sizeof(int), elite_cmp);
+  qsort(order, (size_t)count, sizeof(int), int_cmp);
+  memcpy(out, order, sizeof(int) * (size_t)count);
+  free(order);
+  return 0;
+}
+
+/* mppi_solve (baselines.cpp:99-129) */
+int or_mppi_solve(const or_problem* p, const or_mppi_config* c, double* best_states, double* best_controls,
+                  double* best_reward, int* success, or_iteration_stats* per_it) {
+  if (check_base_problem(p, c->batch, "mppi_solve")) return -1;
+  if (!(c->sigma > 0.0)) { set_err("mppi_solve: sigma must be positive"); return -1; }
+  if (c->iterations < 1) { set_err("mppi_solve: iterations must be >= 1"); return -1; }
+  const int64_t M = c->batch, E = (int64_t)p->robots * p->du * p->horizon;
+  double* mean = (double*)calloc((size_t)E, sizeof(double));
+  double* w = (double*)malloc(sizeof(double) * (size_t)M);
+  base_ctx b = {p, mean, NULL, c->sigma, c->seed, 0, E, (double*)malloc(sizeof(double) * (size_t)(M * E)),
+                (double*)malloc(sizeof(double) * (size_t)M), (int*)calloc((size_t)M, sizeof(int)),
+                (char (*)[160])calloc((size_t)M, 160)};
+  anytime_ctx a = {(double*)malloc(sizeof(double) * (size_t)p->robots * p->dx * (p->horizon + 1)),
+                   (double*)malloc(sizeof(double) * (size_t)p->robots * p->du * (p->horizon + 1)), -1, 0, now_s()};
+  int rc = 0;
+  for (int it = 1; it <= c->iterations; ++it) {
+    b.it = it;
+    if (base_evaluate(&b, M, c->workers)) { rc = -1; break; }
+    if (or_score_weights(b.rewards, M, c->lambda, w)) { rc = -1; break; }
+    double sum = 0.0;  /* mc_average (denoiser.cpp:92-108) */
+    for (int64_t m = 0; m < M; ++m) sum += w[m];
+    if (fabs(sum - 1.0) > 1e-9) { set_err("mc_average: weights must sum to 1"); rc = -1; break; }
+    memset(mean, 0, sizeof(double) * (size_t)E);
+    for (int64_t m = 0; m < M; ++m)
+      for (int64_t e = 0; e < E; ++e) mean[e] = mean[e] + w[m] * b.samples[m * E + e];
+    int ok = 0;
+    if (anytime_record(p, &a, mean, it, best_states, best_controls, best_reward, per_it, &ok)) { rc = -1; break; }
+    if (c->stop_on_success && ok) break;
+    if (c->deadline_seconds > 0 && now_s() - a.t0 >= c->deadline_seconds) break;
+  }
+  if (rc == 0) {
+    *success = or_check_success(p, best_states, NULL, 0);
+    rc = a.used;
+  }
+  free(mean); free(w); free(b.samples); free(b.rewards); free(b.failed); free(b.errs);
+  free(a.states); free(a.controls);
+  return rc;
+}
+
+/* cem_solve (baselines.cpp:131-173) */
+int or_cem_solve(const or_problem* p, const or_cem_config* c, double* best_states, double* best_controls,
+                 double* best_reward, int* success, or_iteration_stats* per_it) {
+  if (check_base_problem(p, c->batch, "cem_solve")) return -1;
+  if (!(c->elite_fraction > 0.0) || !(c->elite_fraction < 1.0)) {
+    set_err("cem_solve: elite_fraction must lie in (0, 1)");
+    return -1;
+  }
+  const int k = (int)(c->elite_fraction * (double)c->batch);
+  if (k < 1) { set_err("cem_solve: elite_fraction * batch must be >= 1"); return -1; }
+  if (!(c->initial_std > 0.0) || !(c->min_std > 0.0)) { set_err("cem_solve: stds must be positive"); return -1; }
+  if (c->iterations < 1) { set_err("cem_solve: iterations must be >= 1"); return -1; }
+  const int64_t M = c->batch, E = (int64_t)p->robots * p->du * p->horizon;
+  double* mean = (double*)calloc((size_t)E, sizeof(double));
+  double* stdv = (double*)malloc(sizeof(double) * (size_t)E);
+  double* nm = (double*)malloc(sizeof(double) * (size_t)E);
+  double* var = (double*)malloc(sizeof(double) * (size_t)E);
+  int* el = (int*)malloc(sizeof(int) * (size_t)k);
+  for (int64_t e = 0; e < E; ++e) stdv[e] = c->initial_std;
+  base_ctx b = {p, mean, stdv, 0.0, c->seed, 0, E, (double*)malloc(sizeof(double) * (size_t)(M * E)),
+                (double*)malloc(sizeof(double) * (size_t)M), (int*)calloc((size_t)M, sizeof(int)),
+                (char (*)[160])calloc((size_t)M, 160)};
+  anytime_ctx a = {(double*)malloc(sizeof(double) * (size_t)p->robots * p->dx * (p->horizon + 1)),
+                   (double*)malloc(sizeof(double) * (size_t)p->robots * p->du * (p->horizon + 1)), -1, 0, now_s()};
+  int rc = 0;
+  for (int it = 1; it <= c->iterations; ++it) {
+    b.it = it;
+    if (base_evaluate(&b, M, c->workers)) { rc = -1; break; }
+    if (or_select_elites(b.rewards, M, k, el)) { rc = -1; break; }
+    memset(nm, 0, sizeof(double) * (size_t)E);
+    for (int j = 0; j < k; ++j)
+      for (int64_t e = 0; e < E; ++e) nm[e] = nm[e] + b.samples[(int64_t)el[j] * E + e];
+    for (int64_t e = 0; e < E; ++e) nm[e] = nm[e] / (double)k;
+    memset(var, 0, sizeof(double) * (size_t)E);
+    for (int j = 0; j < k; ++j)
+      for (int64_t e = 0; e < E; ++e) {
+        const double d = b.samples[(int64_t)el[j] * E + e] - nm[e];
+        var[e] = var[e] + d * d;
+      }
+    for (int64_t e = 0; e < E; ++e) {
+      var[e] = var[e] / (double)k;
+      const double s = sqrt(var[e]);
+      stdv[e] = s < c->min_std ? c->min_std : s;  /* cwiseSqrt().cwiseMax(min_std) */
+    }
+    memcpy(mean, nm, sizeof(double) * (size_t)E);
+    int ok = 0;
+    if (anytime_record(p, &a, mean, it, best_states, best_controls, best_reward, per_it, &ok)) { rc = -1; break; }
+    if (c->stop_on_success && ok) break;
+    if (c->deadline_seconds > 0 && now_s() - a.t0 >= c->deadline_seconds) break;
+  }
+  if (rc == 0) {
+    *success = or_check_success(p, best_states, NULL, 0);
+    rc = a.used;
+  }
+  free(mean); free(stdv); free(nm); free(var); free(el);
+  free(b.samples); free(b.rewards); free(b.failed); free(b.errs);
+  free(a.states); free(a.controls);
+  return rc;
+}

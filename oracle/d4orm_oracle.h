@@ -149,6 +149,36 @@ int or_solve(const or_problem* p, const or_denoiser_config* dcfg, const or_optim
              double* best_states, double* best_controls, double* best_reward, int* success,
              or_iteration_stats* per_iteration, or_trace_rec* traces);
 
+/* ---- baselines.cpp (MPPI / CEM in the joint control space) ---- */
+typedef struct {           /* MppiConfig (baselines.hpp:16-27); horizon/dt from the problem */
+  int64_t batch;
+  double lambda, sigma;
+  int iterations;
+  uint64_t seed;
+  int stop_on_success;
+  double deadline_seconds; /* <= 0: none */
+  int workers;
+} or_mppi_config;
+
+typedef struct {           /* CemConfig (baselines.hpp:31-43) */
+  int64_t batch;
+  double elite_fraction, initial_std, min_std;
+  int iterations;
+  uint64_t seed;
+  int stop_on_success;
+  double deadline_seconds;
+  int workers;
+} or_cem_config;
+
+/* select_elites (baselines.cpp:86-97): `count` indices, ascending. */
+int or_select_elites(const double* rewards, int64_t m, int count, int* out);
+/* mppi_solve / cem_solve (baselines.cpp:99-173).  Same outputs as or_solve;
+ * returns iterations used (> 0) or -1. */
+int or_mppi_solve(const or_problem* p, const or_mppi_config* c, double* best_states, double* best_controls,
+                  double* best_reward, int* success, or_iteration_stats* per_it);
+int or_cem_solve(const or_problem* p, const or_cem_config* c, double* best_states, double* best_controls,
+                 double* best_reward, int* success, or_iteration_stats* per_it);
+
 const char* or_last_error(void);
 
 #ifdef __cplusplus

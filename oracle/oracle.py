@@ -52,6 +52,28 @@ class OrIterStats(C.Structure):
                 ("wall_seconds", C.c_double)]
 
 
+class OrMppiConfig(C.Structure):
+    _fields_ = [("batch", C.c_int64), ("lambda_", C.c_double), ("sigma", C.c_double), ("iterations", C.c_int),
+                ("seed", C.c_uint64), ("stop_on_success", C.c_int), ("deadline_seconds", C.c_double),
+                ("workers", C.c_int)]
+
+
+class OrCemConfig(C.Structure):
+    _fields_ = [("batch", C.c_int64), ("elite_fraction", C.c_double), ("initial_std", C.c_double),
+                ("min_std", C.c_double), ("iterations", C.c_int), ("seed", C.c_uint64), ("stop_on_success", C.c_int),
+                ("deadline_seconds", C.c_double), ("workers", C.c_int)]
+
+
+def mppi_config(batch, lam=0.1, sigma=1.0, iterations=10, seed=0, stop_on_success=True, workers=0):
+    return OrMppiConfig(batch, lam, sigma, iterations, seed & ((1 << 64) - 1), int(stop_on_success), 0.0, workers)
+
+
+def cem_config(batch, elite_fraction=0.1, initial_std=1.0, min_std=0.05, iterations=10, seed=0,
+               stop_on_success=True, workers=0):
+    return OrCemConfig(batch, elite_fraction, initial_std, min_std, iterations, seed & ((1 << 64) - 1),
+                       int(stop_on_success), 0.0, workers)
+
+
 def _dp(a):
     if a is None:
         return None
@@ -128,6 +150,11 @@ class Oracle(_Base):
         L.or_run_denoising.argtypes = [C.POINTER(OrProblem), dp, C.POINTER(OrConfig), dp, C.POINTER(OrTrace)]
         L.or_solve.argtypes = [C.POINTER(OrProblem), C.POINTER(OrConfig), C.POINTER(OrOptConfig), dp, dp, dp,
                                C.POINTER(C.c_int), C.POINTER(OrIterStats), C.POINTER(OrTrace)]
+        L.or_select_elites.argtypes = [dp, i64, C.c_int, C.POINTER(C.c_int)]
+        L.or_mppi_solve.argtypes = [C.POINTER(OrProblem), C.POINTER(OrMppiConfig), dp, dp, dp, C.POINTER(C.c_int),
+                                    C.POINTER(OrIterStats)]
+        L.or_cem_solve.argtypes = [C.POINTER(OrProblem), C.POINTER(OrCemConfig), dp, dp, dp, C.POINTER(C.c_int),
+                                   C.POINTER(OrIterStats)]
         L.or_last_error.restype = C.c_char_p
 
     def err(self):
@@ -254,6 +281,33 @@ class Oracle(_Base):
                                                     for j in range(used)])
 
 
+    def select_elites(self, rewards, count):
+        r = np.ascontiguousarray(rewards, dtype=np.float64)
+        out = (C.c_int * count)()
+        if self.L.or_select_elites(_dp(r), len(r), count, out):
+            raise ValueError(self.err())
+        return list(out)
+
+    def _baseline(self, fn, p, cfg, iterations):
+        s, keep = make_problem(p)
+        states = np.empty((p.horizon + 1, p.robots, p.dx))
+        controls = np.empty((p.horizon + 1, p.robots, p.du))
+        best = C.c_double()
+        ok = C.c_int()
+        its = (OrIterStats * iterations)()
+        used = fn(C.byref(s), C.byref(cfg), _dp(states), _dp(controls), C.byref(best), C.byref(ok), its)
+        if used < 0:
+            raise RuntimeError(self.err())
+        return dict(states=states, controls=controls, best_reward=best.value, success=bool(ok.value),
+                    iterations=used, per_iteration=[(its[j].reward, its[j].objective, bool(its[j].success))
+                                                    for j in range(used)])
+
+    def mppi_solve(self, p, cfg: OrMppiConfig):
+        return self._baseline(self.L.or_mppi_solve, p, cfg, cfg.iterations)
+
+    def cem_solve(self, p, cfg: OrCemConfig):
+        return self._baseline(self.L.or_cem_solve, p, cfg, cfg.iterations)
+
 class Reference(_Base):
     """The reference's own library (proj/src, unchanged) behind ref_* C entry points."""
 
@@ -282,6 +336,11 @@ class Reference(_Base):
         L.ref_run_denoising.argtypes = [C.POINTER(OrProblem), dp, C.POINTER(OrConfig), dp, C.POINTER(OrTrace)]
         L.ref_solve.argtypes = [C.POINTER(OrProblem), C.POINTER(OrConfig), C.POINTER(OrOptConfig), dp, dp,
                                 C.POINTER(C.c_int), C.POINTER(OrIterStats)]
+        L.ref_select_elites.argtypes = [dp, i64, C.c_int, C.POINTER(C.c_int)]
+        L.ref_mppi_solve.argtypes = [C.POINTER(OrProblem), C.POINTER(OrMppiConfig), dp, dp, C.POINTER(C.c_int),
+                                     C.POINTER(OrIterStats)]
+        L.ref_cem_solve.argtypes = [C.POINTER(OrProblem), C.POINTER(OrCemConfig), dp, dp, C.POINTER(C.c_int),
+                                    C.POINTER(OrIterStats)]
         L.ref_antipodal_circle.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, dp, dp]
         L.ref_antipodal_sphere.argtypes = [C.c_int, C.c_double, C.c_double, dp, dp]
         L.ref_random_square.argtypes = [C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_double, dp, dp]
@@ -384,6 +443,31 @@ class Reference(_Base):
             raise RuntimeError(self.err())
         return dict(states=states, best_reward=best.value, success=bool(ok.value), iterations=used,
                     per_iteration=[(its[j].reward, its[j].objective, bool(its[j].success)) for j in range(used)])
+
+    def select_elites(self, rewards, count):
+        r = np.ascontiguousarray(rewards, dtype=np.float64)
+        out = (C.c_int * count)()
+        if self.L.ref_select_elites(_dp(r), len(r), count, out):
+            raise ValueError(self.err())
+        return list(out)
+
+    def _baseline(self, fn, p, cfg, iterations):
+        s, keep = make_problem(p)
+        states = np.empty((p.horizon + 1, p.robots, p.dx))
+        best = C.c_double()
+        ok = C.c_int()
+        its = (OrIterStats * iterations)()
+        used = fn(C.byref(s), C.byref(cfg), _dp(states), C.byref(best), C.byref(ok), its)
+        if used < 0:
+            raise RuntimeError(self.err())
+        return dict(states=states, best_reward=best.value, success=bool(ok.value), iterations=used,
+                    per_iteration=[(its[j].reward, its[j].objective, bool(its[j].success)) for j in range(used)])
+
+    def mppi_solve(self, p, cfg: OrMppiConfig):
+        return self._baseline(self.L.ref_mppi_solve, p, cfg, cfg.iterations)
+
+    def cem_solve(self, p, cfg: OrCemConfig):
+        return self._baseline(self.L.ref_cem_solve, p, cfg, cfg.iterations)
 
     def antipodal_circle(self, robots, diameter, kind, robot_radius):
         dx = 4

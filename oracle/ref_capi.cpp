@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../oracle/d4orm_oracle.h"
+#include "d4orm/baselines.hpp"
 #include "d4orm/denoiser.hpp"
 #include "d4orm/dynamics.hpp"
 #include "d4orm/optimizer.hpp"
@@ -449,6 +450,179 @@ int ref_solve(const or_problem* p, const or_denoiser_config* dc, const or_optimi
     std::memcpy(best_states, best.states.data(), sizeof(double) * best.states.size());
     *success = check_success(best, sc).success ? 1 : 0;
     return used;
+  } catch (const std::exception& ex) {
+    g_ref_err = ex.what();
+    return -1;
+  }
+}
+
+// ------------------------------------------------------------- baselines
+// mppi_solve / cem_solve (baselines.cpp:99-173): native kinds call the
+// reference functions; the extension kinds run the same statements with the
+// rollout swapped (any_rollout), every other piece the reference's own.
+int ref_select_elites(const double* r, int64_t m, int count, int* out) {
+  try {
+    Vector rw(m);
+    for (int64_t i = 0; i < m; ++i) rw[i] = r[i];
+    const std::vector<int> e = select_elites(rw, count);
+    std::memcpy(out, e.data(), sizeof(int) * e.size());
+    return 0;
+  } catch (const std::exception& ex) {
+    g_ref_err = ex.what();
+    return 1;
+  }
+}
+
+}  // extern "C"
+
+namespace {
+template <class Update>
+int ext_anytime(const or_problem* p, const DynamicsModel& model, const Scenario& sc, int iterations,
+                bool stop_on_success, double* best_states, double* best_reward, int* success,
+                or_iteration_stats* per_it, Update&& update) {
+  JointTrajectory best;
+  int best_it = -1, used = 0;
+  for (int it = 1; it <= iterations; ++it) {
+    const JointControls& mean = update(it);
+    const JointTrajectory traj = any_rollout(p, model, sc, mean);
+    const double reward = total_reward(traj, sc);
+    const double quality = objective(traj, sc);
+    const bool ok = check_success(traj, sc).success;
+    if (per_it) per_it[it - 1] = {reward, quality, ok ? 1 : 0, 0.0};
+    used = it;
+    if (best_it < 0 || reward > *best_reward) {
+      *best_reward = reward;
+      best = traj;
+      best_it = it;
+    }
+    if (stop_on_success && ok) break;
+  }
+  std::memcpy(best_states, best.states.data(), sizeof(double) * best.states.size());
+  *success = check_success(best, sc).success ? 1 : 0;
+  return used;
+}
+
+Vector ext_evaluate(const or_problem* p, const DynamicsModel& model, const Scenario& sc,
+                    const std::vector<JointControls>& samples, int workers) {
+  Vector rewards(static_cast<Eigen::Index>(samples.size()));
+  parallel_for(static_cast<int>(samples.size()), workers, [&](int m) {
+    const JointTrajectory traj = any_rollout(p, model, sc, samples[m]);
+    rewards[m] = total_reward(traj, sc, sc.reward);
+  });
+  return rewards;
+}
+
+Matrix ext_normal_matrix(Eigen::Index rows, Eigen::Index cols, std::uint64_t stream_seed) {
+  Matrix z(rows, cols);
+  NormalStream stream(stream_seed);
+  stream.fill(z.data(), z.size());
+  return z;
+}
+}  // namespace
+
+extern "C" {
+
+int ref_mppi_solve(const or_problem* p, const or_mppi_config* c, double* best_states, double* best_reward,
+                   int* success, or_iteration_stats* per_it) {
+  try {
+    const DynamicsModel model = make_model(p);
+    Scenario sc = make_scenario(p);
+    MppiConfig cfg;
+    cfg.batch = static_cast<int>(c->batch);
+    cfg.lambda = c->lambda;
+    cfg.sigma = c->sigma;
+    cfg.iterations = c->iterations;
+    cfg.seed = c->seed;
+    cfg.horizon = p->horizon;
+    cfg.dt = p->dt;
+    cfg.stop_on_success = c->stop_on_success != 0;
+    cfg.workers = c->workers;
+    if (native(p->kind)) {
+      const SolveResult r = mppi_solve(sc, model, cfg);
+      std::memcpy(best_states, r.best_trajectory.states.data(), sizeof(double) * r.best_trajectory.states.size());
+      *best_reward = r.best_reward;
+      *success = r.success ? 1 : 0;
+      if (per_it)
+        for (size_t i = 0; i < r.per_iteration.size(); ++i)
+          per_it[i] = {r.per_iteration[i].reward, r.per_iteration[i].objective,
+                       r.per_iteration[i].success ? 1 : 0, r.per_iteration[i].wall_seconds};
+      return r.iterations_used;
+    }
+    JointControls mean = JointControls::zeros(p->robots, p->du, p->horizon);
+    std::vector<JointControls> samples(static_cast<std::size_t>(cfg.batch));
+    return ext_anytime(p, model, sc, cfg.iterations, cfg.stop_on_success, best_states, best_reward, success, per_it,
+                       [&](int iteration) -> const JointControls& {
+                         parallel_for(cfg.batch, cfg.workers, [&](int m) {
+                           const Matrix z = ext_normal_matrix(mean.u.rows(), mean.u.cols(),
+                                                              mix_seed(cfg.seed, static_cast<std::uint64_t>(iteration),
+                                                                       static_cast<std::uint64_t>(m)));
+                           samples[m] = {mean.robots, mean.control_dim, mean.u + cfg.sigma * z};
+                         });
+                         const Vector rewards = ext_evaluate(p, model, sc, samples, cfg.workers);
+                         const Vector weights = score_weights(rewards, cfg.lambda);
+                         mean = mc_average(samples, weights);
+                         return mean;
+                       });
+  } catch (const std::exception& ex) {
+    g_ref_err = ex.what();
+    return -1;
+  }
+}
+
+int ref_cem_solve(const or_problem* p, const or_cem_config* c, double* best_states, double* best_reward,
+                  int* success, or_iteration_stats* per_it) {
+  try {
+    const DynamicsModel model = make_model(p);
+    Scenario sc = make_scenario(p);
+    CemConfig cfg;
+    cfg.batch = static_cast<int>(c->batch);
+    cfg.elite_fraction = c->elite_fraction;
+    cfg.initial_std = c->initial_std;
+    cfg.min_std = c->min_std;
+    cfg.iterations = c->iterations;
+    cfg.seed = c->seed;
+    cfg.horizon = p->horizon;
+    cfg.dt = p->dt;
+    cfg.stop_on_success = c->stop_on_success != 0;
+    cfg.workers = c->workers;
+    if (native(p->kind)) {
+      const SolveResult r = cem_solve(sc, model, cfg);
+      std::memcpy(best_states, r.best_trajectory.states.data(), sizeof(double) * r.best_trajectory.states.size());
+      *best_reward = r.best_reward;
+      *success = r.success ? 1 : 0;
+      if (per_it)
+        for (size_t i = 0; i < r.per_iteration.size(); ++i)
+          per_it[i] = {r.per_iteration[i].reward, r.per_iteration[i].objective,
+                       r.per_iteration[i].success ? 1 : 0, r.per_iteration[i].wall_seconds};
+      return r.iterations_used;
+    }
+    const int elite_count = static_cast<int>(cfg.elite_fraction * cfg.batch);
+    JointControls mean = JointControls::zeros(p->robots, p->du, p->horizon);
+    Matrix std_dev = Matrix::Constant(mean.u.rows(), mean.u.cols(), cfg.initial_std);
+    std::vector<JointControls> samples(static_cast<std::size_t>(cfg.batch));
+    return ext_anytime(p, model, sc, cfg.iterations, cfg.stop_on_success, best_states, best_reward, success, per_it,
+                       [&](int iteration) -> const JointControls& {
+                         parallel_for(cfg.batch, cfg.workers, [&](int m) {
+                           const Matrix z = ext_normal_matrix(mean.u.rows(), mean.u.cols(),
+                                                              mix_seed(cfg.seed, static_cast<std::uint64_t>(iteration),
+                                                                       static_cast<std::uint64_t>(m)));
+                           samples[m] = {mean.robots, mean.control_dim, mean.u + std_dev.cwiseProduct(z)};
+                         });
+                         const Vector rewards = ext_evaluate(p, model, sc, samples, cfg.workers);
+                         const std::vector<int> elites = select_elites(rewards, elite_count);
+                         Matrix new_mean = Matrix::Zero(mean.u.rows(), mean.u.cols());
+                         for (const int m : elites) new_mean += samples[static_cast<std::size_t>(m)].u;
+                         new_mean /= static_cast<double>(elite_count);
+                         Matrix variance = Matrix::Zero(mean.u.rows(), mean.u.cols());
+                         for (const int m : elites) {
+                           const Matrix d = samples[static_cast<std::size_t>(m)].u - new_mean;
+                           variance += d.cwiseProduct(d);
+                         }
+                         variance /= static_cast<double>(elite_count);
+                         std_dev = variance.cwiseSqrt().cwiseMax(cfg.min_std);
+                         mean.u = new_mean;
+                         return mean;
+                       });
   } catch (const std::exception& ex) {
     g_ref_err = ex.what();
     return -1;

@@ -25,7 +25,7 @@ EXPORTS = (
     "d4orm_cuda_version", "d4orm_cuda_set_problem", "d4orm_cuda_set_options", "d4orm_cuda_set_noise_fn",
     "d4orm_cuda_run_denoising", "d4orm_cuda_denoise_step", "d4orm_cuda_rollout_fitness",
     "d4orm_cuda_score_weights", "d4orm_cuda_philox_noise", "d4orm_cuda_bench_steps",
-    "d4orm_cuda_launches_per_step", "d4orm_cuda_solve",
+    "d4orm_cuda_launches_per_step", "d4orm_cuda_solve", "d4orm_cuda_mppi_solve", "d4orm_cuda_cem_solve",
 )
 
 
@@ -64,6 +64,17 @@ class IterationRec_C(C.Structure):
     _fields_ = [("reward", C.c_double), ("objective", C.c_double), ("success", C.c_int), ("elapsed", C.c_double)]
 
 
+class MppiConfig_C(C.Structure):
+    _fields_ = [("batch", C.c_int64), ("lambda_", C.c_double), ("sigma", C.c_double), ("iterations", C.c_int),
+                ("seed", C.c_uint64), ("stop_on_success", C.c_int), ("deadline_seconds", C.c_double)]
+
+
+class CemConfig_C(C.Structure):
+    _fields_ = [("batch", C.c_int64), ("elite_fraction", C.c_double), ("initial_std", C.c_double),
+                ("min_std", C.c_double), ("iterations", C.c_int), ("seed", C.c_uint64),
+                ("stop_on_success", C.c_int), ("deadline_seconds", C.c_double)]
+
+
 NOISE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_double))
 
 _lib = None
@@ -97,6 +108,10 @@ def lib() -> C.CDLL:
     L.d4orm_cuda_philox_noise.argtypes = [vp, C.c_uint64, i32, i64, i64, C.POINTER(C.c_float)]
     L.d4orm_cuda_bench_steps.argtypes = [vp, dp, C.POINTER(DenoiserConfig_C), i32, i32, dp, dp]
     L.d4orm_cuda_launches_per_step.argtypes = [vp]
+    L.d4orm_cuda_mppi_solve.argtypes = [vp, C.POINTER(MppiConfig_C), dp, dp, C.POINTER(IterationRec_C),
+                                        C.POINTER(i32), dp, C.POINTER(i32)]
+    L.d4orm_cuda_cem_solve.argtypes = [vp, C.POINTER(CemConfig_C), dp, dp, C.POINTER(IterationRec_C),
+                                       C.POINTER(i32), dp, C.POINTER(i32)]
     L.d4orm_cuda_solve.argtypes = [vp, C.POINTER(SolveConfig_C), dp, dp, C.POINTER(IterationRec_C),
                                    C.POINTER(TraceRec_C), C.POINTER(i32), dp, C.POINTER(i32)]
     _lib = L

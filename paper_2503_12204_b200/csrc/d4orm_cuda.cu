@@ -28,6 +28,8 @@
 #include "d4orm_kernels.cuh"
 #include "k_outcome.cuh"
 
+#include <cub/device/device_radix_sort.cuh>
+
 namespace d4k {
 template <typename S, int KIND>
 cudaError_t launch_k23(int tb, int maxw, int noise, dim3 grid, int threads, size_t smem, cudaStream_t st,
@@ -154,14 +156,25 @@ struct d4orm_cuda_ctx {
   DevBuf<unsigned char> sst;
   std::string iter_key;
   cudaGraphExec_t iter_exec = nullptr;
+  // MPPI / CEM: per-element std and new mean (S, fp64), sort buffers
+  DevBuf<unsigned char> bl_s, cub_tmp;
+  DevBuf<double> bl_d;
+  DevBuf<int> bl_i;
+  std::string bl_key;
+  cudaGraphExec_t bl_exec = nullptr;
 
   ~d4orm_cuda_ctx() {
     cudaSetDevice(device);
     for (auto& g : graphs)
       if (g.exec) cudaGraphExecDestroy(g.exec);
     if (iter_exec) cudaGraphExecDestroy(iter_exec);
+    if (bl_exec) cudaGraphExecDestroy(bl_exec);
     sv.release();
     sst.release();
+    bl_s.release();
+    cub_tmp.release();
+    bl_d.release();
+    bl_i.release();
     for (auto* b : {&z[0], &z[1], &base, &msv, &bm, &starts_d, &goals_d, &inv_d, &obs_d, &ocl_d, &partial, &roots,
                     &states_out, &controls_out})
       b->release();
@@ -498,95 +511,153 @@ int host_noise(d4orm_cuda_ctx* ctx, const RunShape& rs, int step, int64_t m0, in
   return D4ORM_OK;
 }
 
-// Enqueue one denoising step i.  philox: fp32 draws the noise inside K2+K3
-// (fused, z written once for K5); fp64 runs K1 first.  !philox: z for step i
-// is already in z[0] (host noise).
+// Per-step constants.  Denoising step i: sd = √(1/ᾱ_i − 1), update scale
+// √ᾱ_{i−1}, next mean scale 1/√ᾱ_{i−1}, Philox keys[i], trace slot N − i.
+// MPPI / CEM iterations reuse the same kernels with sd = σ, unit scales and
+// keys[0] (re-derived on the device per iteration).
+struct StepConsts {
+  double sd = 1.0, sab = 1.0, next_ms = 1.0;
+  int key_i = 0;        // Philox key index (FitParams::step, K1 step)
+  int err_key = 0;      // error key of the step (check_err)
+  int trace_off = 0;    // K4 trace record slot
+  int trace_step = 0;   // step number recorded in the trace
+  const void* sdv = nullptr;  // CEM: per-element std (S), else the scalar sd
+};
+
+StepConsts denoise_consts(const d4orm_cuda_ctx* ctx, const RunShape& rs, int i) {
+  StepConsts c;
+  c.sd = std::sqrt(1.0 / ctx->ab[i] - 1.0);
+  c.sab = std::sqrt(ctx->ab[i - 1]);
+  c.next_ms = i > 1 ? 1.0 / std::sqrt(ctx->ab[i - 1]) : 0.0;
+  c.key_i = i;
+  c.err_key = rs.N - i;
+  c.trace_off = rs.N - i;
+  c.trace_step = i;
+  return c;
+}
+
+// K2+K3 (+ K1 on the fp64 Philox path) and the reward all-gather.
 template <typename S>
-int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, bool philox, bool timing) {
-  const double ab_i = ctx->ab[i];
-  const double sd = std::sqrt(1.0 / ab_i - 1.0);
-  const double sab = std::sqrt(ctx->ab[i - 1]);
-  const double next_ms = i > 1 ? 1.0 / std::sqrt(ctx->ab[i - 1]) : 0.0;
+int enqueue_fitness(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc, bool philox, bool timing) {
   const bool f64 = std::is_same<S, double>::value;
   const bool fused = philox && !f64;
   const int TC = f64 ? ctx->TC64 : ctx->TC32;
   const size_t smem = f64 ? ctx->smem64 : ctx->smem32;
-  auto mark = [&](int k) -> int {
-    if (timing) CU(cudaEventRecord(ctx->ev_k[k], ctx->s_main));
-    return D4ORM_OK;
-  };
   if (philox && !fused) {
-    if (int r = launch_noise<S>(ctx, ctx->s_main, rs.Ml, rs.m0, i, ctx->z[0].p)) return r;
+    if (int r = launch_noise<S>(ctx, ctx->s_main, rs.Ml, rs.m0, sc.key_i, ctx->z[0].p)) return r;
   }
-  if (int r = mark(0)) return r;
-  d4k::FitParams<S> f = fit_params<S>(ctx, (const S*)ctx->z[0].p, (const S*)ctx->base.p, (const S*)ctx->msv.p, sd,
-                                      rs.Ml, rs.m0, rs.N - i, ctx->rewards.p + rs.m0, nullptr, nullptr, nullptr, TC);
+  if (timing) CU(cudaEventRecord(ctx->ev_k[0], ctx->s_main));
+  d4k::FitParams<S> f = fit_params<S>(ctx, (const S*)ctx->z[0].p, (const S*)ctx->base.p, (const S*)ctx->msv.p, sc.sd,
+                                      rs.Ml, rs.m0, sc.err_key, ctx->rewards.p + rs.m0, nullptr, nullptr, nullptr, TC);
   f.keys = ctx->keys.p;
-  f.step = i;
+  f.step = sc.key_i;
   f.z_store = (S*)ctx->z[0].p;
+  f.sdv = (const S*)sc.sdv;
   CU(launch_fit<S>(ctx, f, smem, fused));
-  if (int r = mark(1)) return r;
+  if (timing) CU(cudaEventRecord(ctx->ev_k[1], ctx->s_main));
   if (ctx->comm) {
     NC(g_nccl.AllGather(ctx->rewards.p + rs.m0, ctx->rewards.p, (size_t)rs.Ml, ncclFloat64, ctx->comm, ctx->s_main));
   }
-  d4k::WeightParams wp{ctx->rewards.p, rs.M, rs.lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p + 4 * (rs.N - i), i,
-                       ctx->errw.p};
-  {
-    // 2 rewards per thread (16 beyond 148·2048 samples) held in registers;
-    // one CTA → plain launch, several → cooperative launch (grid.sync)
-    const bool big = rs.M > 148LL * d4k::kWThreads * 2;
-    const int64_t per_cta = (int64_t)d4k::kWThreads * (big ? 16 : 2);
-    const unsigned g = (unsigned)((rs.M + per_cta - 1) / per_cta);
-    if (g > 148) return fail(ctx, D4ORM_E_UNSUPPORTED, "score_weights: batch %lld too large", (long long)rs.M);
-    double* scratch = ctx->wscratch.p;
-    const void* fn = big ? (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 16>
-                         : (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 2>;
-    void* args[] = {(void*)&wp, (void*)&scratch};
-    if (g == 1) {
-      CU(cudaLaunchKernel(fn, dim3(1), dim3(d4k::kWThreads), args, 0, ctx->s_main));
-    } else {
-      CU(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(d4k::kWThreads), args, 0, ctx->s_main));
-    }
+  return D4ORM_OK;
+}
+
+// K4: z-scored softmax weights over all M rewards.
+int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc) {
+  d4k::WeightParams wp{ctx->rewards.p, rs.M, rs.lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p + 4 * sc.trace_off,
+                       sc.trace_step, ctx->errw.p};
+  // 2 rewards per thread (16 beyond 148·2048 samples) held in registers;
+  // one CTA → plain launch, several → cooperative launch (grid.sync)
+  const bool big = rs.M > 148LL * d4k::kWThreads * 2;
+  const int64_t per_cta = (int64_t)d4k::kWThreads * (big ? 16 : 2);
+  const unsigned g = (unsigned)((rs.M + per_cta - 1) / per_cta);
+  if (g > 148) return fail(ctx, D4ORM_E_UNSUPPORTED, "score_weights: batch %lld too large", (long long)rs.M);
+  double* scratch = ctx->wscratch.p;
+  const void* fn = big ? (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 16>
+                       : (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 2>;
+  void* args[] = {(void*)&wp, (void*)&scratch};
+  if (g == 1) {
+    CU(cudaLaunchKernel(fn, dim3(1), dim3(d4k::kWThreads), args, 0, ctx->s_main));
+  } else {
+    CU(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(d4k::kWThreads), args, 0, ctx->s_main));
   }
-  if (int r = mark(2)) return r;
+  return D4ORM_OK;
+}
+
+// K5: Σ_m w_m·f(sample_m) over this rank's samples (chunk partials), then the
+// deterministic pairwise tree (+ the root all-gather when sharded) and the
+// finalisation `fin` (the denoiser / MPPI update, or the CEM mean / variance).
+template <typename S>
+int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc, int dev_mode,
+                   const d4k::TreeFinal<S>& fin, bool timing) {
+  const bool f64 = std::is_same<S, double>::value;
   static_assert(kChunk == d4k::kChunkSamples, "K5 chunk size");
   auto partial = [&](auto sub_tag) {
     constexpr int SUB = decltype(sub_tag)::value;
     using Sh = d4k::PartShape<SUB>;
     const dim3 pgrid((unsigned)((rs.E + 4 * Sh::GROUPS - 1) / (4 * Sh::GROUPS)), (unsigned)rs.chunks_local);
+    d4k::PartArgs<S> pa{(const S*)ctx->z[0].p, (const S*)ctx->msv.p, (S)sc.sd, (const S*)sc.sdv, fin.nm_in, rs.Ml,
+                        rs.E, (S*)ctx->partial.p};
     if (f64) {
-      d4k::k_wmean_partial<S, double, SUB><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(
-          (const S*)ctx->z[0].p, ctx->w64.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, (S*)ctx->partial.p);
+      if (dev_mode)
+        d4k::k_wmean_partial<S, double, SUB, 1><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w64.p + rs.m0);
+      else
+        d4k::k_wmean_partial<S, double, SUB, 0><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w64.p + rs.m0);
     } else {
-      d4k::k_wmean_partial<S, float, SUB><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(
-          (const S*)ctx->z[0].p, ctx->w32.p + rs.m0, (const S*)ctx->msv.p, (S)sd, rs.Ml, rs.E, (S*)ctx->partial.p);
+      if (dev_mode)
+        d4k::k_wmean_partial<S, float, SUB, 1><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w32.p + rs.m0);
+      else
+        d4k::k_wmean_partial<S, float, SUB, 0><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w32.p + rs.m0);
     }
   };
   if (rs.E >= kPartLargeE) partial(std::integral_constant<int, 1>{});
   else partial(std::integral_constant<int, 16>{});
   CU(cudaGetLastError());
-  if (int r = mark(3)) return r;
+  if (timing) CU(cudaEventRecord(ctx->ev_k[3], ctx->s_main));
   const unsigned tgrid = (unsigned)((rs.E + d4k::kThreads - 1) / d4k::kThreads);
-  S* bm = f64 ? nullptr : (S*)ctx->bm.p;
-  const S* bs = (const S*)ctx->base.p;
   if (!ctx->comm) {
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
-                                                                   sab, next_ms, ctx->var.p, (S*)ctx->msv.p, bs, bm,
-                                                                   nullptr);
+                                                                   fin, nullptr);
   } else {
     S* my_root = (S*)ctx->roots.p + (size_t)ctx->rank * rs.E;
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
-                                                                   sab, next_ms, ctx->var.p, (S*)ctx->msv.p, bs, bm,
-                                                                   my_root);
+                                                                   fin, my_root);
     CU(cudaGetLastError());
     NC(g_nccl.AllGather(my_root, ctx->roots.p, (size_t)rs.E, f64 ? ncclFloat64 : ncclFloat32, ctx->comm, ctx->s_main));
-    d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->roots.p, ctx->world, rs.E, sab,
-                                                                   next_ms, ctx->var.p, (S*)ctx->msv.p, bs, bm,
+    d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->roots.p, ctx->world, rs.E, fin,
                                                                    nullptr);
   }
   CU(cudaGetLastError());
-  if (int r = mark(4)) return r;
+  if (timing) CU(cudaEventRecord(ctx->ev_k[4], ctx->s_main));
   return D4ORM_OK;
+}
+
+template <typename S>
+d4k::TreeFinal<S> update_final(d4orm_cuda_ctx* ctx, const StepConsts& sc) {
+  d4k::TreeFinal<S> fin{};
+  fin.mode = d4k::FIN_UPDATE;
+  fin.scale = sc.sab;
+  fin.next_ms = sc.next_ms;
+  fin.var = ctx->var.p;
+  fin.msv = (S*)ctx->msv.p;
+  fin.base = (const S*)ctx->base.p;
+  fin.bm = std::is_same<S, double>::value ? nullptr : (S*)ctx->bm.p;
+  return fin;
+}
+
+// Enqueue one denoising step i.  philox: fp32 draws the noise inside K2+K3
+// (fused, z written once for K5); fp64 runs K1 first.  !philox: z for step i
+// is already in z[0] (host noise).
+template <typename S>
+int enqueue_step_c(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc, bool philox, bool timing) {
+  if (int r = enqueue_fitness<S>(ctx, rs, sc, philox, timing)) return r;
+  if (int r = enqueue_weights(ctx, rs, sc)) return r;
+  if (timing) CU(cudaEventRecord(ctx->ev_k[2], ctx->s_main));
+  return enqueue_reduce<S>(ctx, rs, sc, 0, update_final<S>(ctx, sc), timing);
+}
+
+template <typename S>
+int enqueue_step(d4orm_cuda_ctx* ctx, const RunShape& rs, int i, bool philox, bool timing) {
+  return enqueue_step_c<S>(ctx, rs, denoise_consts(ctx, rs, i), philox, timing);
 }
 
 template <typename S>
@@ -705,7 +776,7 @@ int check_err(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   if (e == ~0ull) return D4ORM_OK;
   if (e == 0xFFFFFFFFFFFFFFFEull) return fail(ctx, D4ORM_E_RUNTIME, "score_weights: non-finite reward");
   const int step_key = (int)(e >> 52);
-  if (step_key == kOutcomeKey)  // dynamics.cpp:81-84, thrown by rollout in iterate_impl (optimizer.cpp:28)
+  if (step_key == kOutcomeKey || step_key == 0xFFD)  // dynamics.cpp:81-84 thrown by rollout (optimizer.cpp:28, baselines.cpp:34)
     return fail(ctx, D4ORM_E_RUNTIME, "rollout: non-finite state for robot %d at step %d", (int)((e >> 10) & 1023),
                 (int)(e & 1023));
   const long long m = (long long)((e >> 20) & 0xFFFFFFFFull);
@@ -741,7 +812,7 @@ int run_denoising_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoise
 // fp64 buffers of the device-side anytime loop (one allocation, `sv`) and its
 // state (`sst`, d4k::SolveState).
 struct SolveLayout {
-  size_t cur, states, vals, best_states, best_ctrl, rec, starts, goals, obsc, obsr, total;
+  size_t cur, states, vals, best_states, best_ctrl, rec, starts, goals, obsc, obsr, aux, total;
 };
 SolveLayout solve_layout(const d4orm_problem& p, int max_it) {
   SolveLayout L{};
@@ -756,7 +827,8 @@ SolveLayout solve_layout(const d4orm_problem& p, int max_it) {
   L.goals = L.starts + (size_t)p.robots * p.dx;
   L.obsc = L.goals + (size_t)p.robots * p.pdim;
   L.obsr = L.obsc + (size_t)p.n_obstacles * p.pdim;
-  L.total = L.obsr + (size_t)p.n_obstacles + 1;
+  L.aux = L.obsr + (size_t)p.n_obstacles + 1;
+  L.total = L.aux + E;
   return L;
 }
 
@@ -780,12 +852,15 @@ cudaError_t launch_iter_begin(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_outcome(d4orm_cuda_ctx* ctx, int max_it) {
+// baseline: MPPI / CEM — the base is zero (cur region, never written) and the
+// executed controls go to the aux region.
+cudaError_t launch_outcome(d4orm_cuda_ctx* ctx, int max_it, bool baseline = false) {
   const d4orm_problem& p = ctx->prob;
   const SolveLayout L = solve_layout(p, max_it);
   double* sv = ctx->sv.p;
   d4k::OutcomeParams op{};
-  op.ctrl = sv + L.cur;
+  op.ctrl_in = sv + L.cur;
+  op.ctrl = sv + (baseline ? L.aux : L.cur);
   op.var = ctx->var.p;
   op.starts = sv + L.starts;
   op.goals = sv + L.goals;
@@ -944,6 +1019,229 @@ int solve_t(d4orm_cuda_ctx* ctx, const d4orm_solve_config* sc, double* best_stat
   return D4ORM_OK;
 }
 
+// ------------------------------------------------------------ MPPI / CEM
+// baselines.cpp:99-173 on the same kernels: an iteration is one step of the
+// denoiser's machinery with sd = σ (MPPI) or the per-element CEM std, unit
+// scales, the key of mix_seed(seed, it) (K8), then K6 on the mean.
+constexpr int kBaselineKey = 0xFFD;  // error key: a sample rollout of MPPI / CEM
+
+struct BaselineSpec {
+  bool cem = false;
+  int64_t batch = 0;
+  double lambda = 0.1, sigma = 1.0;
+  double elite_fraction = 0.1, initial_std = 1.0, min_std = 0.05;
+  int iterations = 1;
+  uint64_t seed = 0;
+  int stop_on_success = 1;
+  double deadline = 0.0;
+  const char* what = "mppi_solve";
+  int64_t k = 0;  // CEM elite count
+};
+
+template <typename S>
+struct CemBufs {
+  S* sdv;
+  S* nm_s;
+  double* std64;
+  double* nm64;
+  double* keys_in;
+  double* keys_out;
+  int* idx_in;
+  int* idx_out;
+};
+
+template <typename S>
+CemBufs<S> cem_bufs(d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  CemBufs<S> b{};
+  b.sdv = (S*)ctx->bl_s.p;
+  b.nm_s = b.sdv + rs.E;
+  b.std64 = ctx->bl_d.p;
+  b.nm64 = b.std64 + rs.E;
+  b.keys_in = b.nm64 + rs.E;
+  b.keys_out = b.keys_in + rs.M;
+  b.idx_in = ctx->bl_i.p;
+  b.idx_out = b.idx_in + rs.M;
+  return b;
+}
+
+template <typename S>
+int enqueue_baseline_iteration(d4orm_cuda_ctx* ctx, const RunShape& rs, const BaselineSpec& b, bool philox, int it,
+                               int max_it) {
+  const bool f64 = std::is_same<S, double>::value;
+  d4k::k_baseline_begin<<<1, 32, 0, ctx->s_main>>>(ctx->keys.p, reinterpret_cast<const d4k::SolveState*>(ctx->sst.p),
+                                                    ctx->errw.p);
+  CU(cudaGetLastError());
+  if (!philox) {  // host noise of iteration it: NormalStream(mix_seed(seed, it, m))
+    if (int r = host_noise(ctx, rs, it, rs.m0, rs.Ml, nullptr, ctx->z[0].p)) return r;
+  }
+  StepConsts sc;
+  sc.sd = b.sigma;
+  sc.sab = 1.0;
+  sc.next_ms = 1.0;
+  sc.key_i = 0;
+  sc.err_key = kBaselineKey;
+  sc.trace_off = 0;
+  sc.trace_step = 0;
+  CemBufs<S> cb = cem_bufs<S>(ctx, rs);
+  if (b.cem) sc.sdv = cb.sdv;
+  if (int r = enqueue_fitness<S>(ctx, rs, sc, philox, false)) return r;
+  if (!b.cem) {
+    if (int r = enqueue_weights(ctx, rs, sc)) return r;  // score_weights (baselines.cpp:124)
+    if (int r = enqueue_reduce<S>(ctx, rs, sc, 0, update_final<S>(ctx, sc), false)) return r;  // mc_average
+  } else {
+    // select_elites: stable descending sort of all M rewards, first k
+    const unsigned g = (unsigned)((rs.M + 255) / 256);
+    d4k::k_sort_prep<<<g, 256, 0, ctx->s_main>>>(ctx->rewards.p, rs.M, cb.keys_in, cb.idx_in);
+    size_t tmp = ctx->cub_tmp.n;
+    CU(cub::DeviceRadixSort::SortPairsDescending(ctx->cub_tmp.p, tmp, cb.keys_in, cb.keys_out, cb.idx_in, cb.idx_out,
+                                                 (int)rs.M, 0, 64, ctx->s_main));
+    d4k::k_elite_weights<<<g, 256, 0, ctx->s_main>>>(cb.idx_out, rs.M, b.k, ctx->w64.p, ctx->w32.p);
+    CU(cudaGetLastError());
+    d4k::TreeFinal<S> fm{};
+    fm.mode = d4k::FIN_CEM_MEAN;
+    fm.kdiv = (double)b.k;
+    fm.nm64 = cb.nm64;
+    fm.nm_s = cb.nm_s;
+    if (int r = enqueue_reduce<S>(ctx, rs, sc, 0, fm, false)) return r;  // Σ elites / k
+    d4k::TreeFinal<S> fv = fm;
+    fv.mode = d4k::FIN_CEM_VAR;
+    fv.nm_in = cb.nm_s;
+    fv.min_std = b.min_std;
+    fv.std64 = cb.std64;
+    fv.sdv = cb.sdv;
+    fv.var = ctx->var.p;
+    fv.msv = (S*)ctx->msv.p;
+    fv.base = (const S*)ctx->base.p;
+    fv.bm = f64 ? nullptr : (S*)ctx->bm.p;
+    if (int r = enqueue_reduce<S>(ctx, rs, sc, 1, fv, false)) return r;  // Σ elites (u − nm)² / k
+  }
+  CU(launch_outcome(ctx, max_it, true));
+  return D4ORM_OK;
+}
+
+template <typename S>
+int baseline_solve_t(d4orm_cuda_ctx* ctx, BaselineSpec b, double* best_states, double* best_controls,
+                     d4orm_iteration_rec* per_it, int* used, double* best_reward, int* success) {
+  if (!ctx->has_problem) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: set_problem not called");
+  const d4orm_problem& p = ctx->prob;
+  // check_problem (baselines.cpp:19-28) and the per-method checks
+  if (p.horizon < 2) return fail(ctx, D4ORM_E_INVALID, "%s: horizon must be >= 2", b.what);
+  if (!(p.dt > 0.0)) return fail(ctx, D4ORM_E_INVALID, "%s: dt must be positive", b.what);
+  if (b.batch < 2) return fail(ctx, D4ORM_E_INVALID, "%s: batch must be >= 2", b.what);
+  if (!b.cem) {
+    if (!(b.sigma > 0.0)) return fail(ctx, D4ORM_E_INVALID, "mppi_solve: sigma must be positive");
+    if (b.iterations < 1) return fail(ctx, D4ORM_E_INVALID, "mppi_solve: iterations must be >= 1");
+  } else {
+    if (!(b.elite_fraction > 0.0) || !(b.elite_fraction < 1.0))
+      return fail(ctx, D4ORM_E_INVALID, "cem_solve: elite_fraction must lie in (0, 1)");
+    b.k = (int64_t)(int)(b.elite_fraction * (double)b.batch);
+    if (b.k < 1) return fail(ctx, D4ORM_E_INVALID, "cem_solve: elite_fraction * batch must be >= 1");
+    if (!(b.initial_std > 0.0) || !(b.min_std > 0.0)) return fail(ctx, D4ORM_E_INVALID, "cem_solve: stds must be positive");
+    if (b.iterations < 1) return fail(ctx, D4ORM_E_INVALID, "cem_solve: iterations must be >= 1");
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  auto elapsed = [&t0] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+  d4orm_denoiser_config dc{};
+  dc.steps = 1;
+  dc.batch = b.batch;
+  dc.lambda = b.cem ? 1.0 : b.lambda;
+  dc.alpha_bar_final = 0.5;
+  dc.seed = b.seed;
+  dc.mode = D4ORM_DEFORMATION;
+  RunShape rs;
+  if (int r = check_config(ctx, &dc, &rs)) return r;
+  const bool philox = ctx->noise_source == D4ORM_NOISE_PHILOX;
+  if (!philox && !ctx->noise_fn)
+    return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: host noise selected but no noise fn set");
+  if (int r = ensure_buffers(ctx, rs, false)) return r;
+  const SolveLayout L = solve_layout(p, b.iterations);
+  CU(ctx->sv.ensure(L.total));
+  CU(ctx->sst.ensure(sizeof(d4k::SolveState)));
+  const size_t SZ = sizeof(S);
+  if (b.cem) {
+    CU(ctx->bl_s.ensure(2 * (size_t)rs.E * SZ));
+    CU(ctx->bl_d.ensure(2 * (size_t)rs.E + 2 * (size_t)rs.M));
+    CU(ctx->bl_i.ensure(2 * (size_t)rs.M));
+    size_t tmp = 0;
+    CU(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, (const double*)nullptr, (double*)nullptr,
+                                                 (const int*)nullptr, (int*)nullptr, (int)rs.M, 0, 64, ctx->s_main));
+    CU(ctx->cub_tmp.ensure(tmp));
+  }
+  {
+    // mean = zeros (baselines.cpp:107,145); base zero; CEM std = initial_std
+    std::vector<double> h(L.total, 0.0);
+    std::copy(ctx->starts.begin(), ctx->starts.end(), h.begin() + L.starts);
+    std::copy(ctx->goals.begin(), ctx->goals.end(), h.begin() + L.goals);
+    std::copy(ctx->obs_c.begin(), ctx->obs_c.end(), h.begin() + L.obsc);
+    std::copy(ctx->obs_r.begin(), ctx->obs_r.end(), h.begin() + L.obsr);
+    CU(cudaMemcpyAsync(ctx->sv.p, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, ctx->s_main));
+    const d4k::SolveState st0{0, -1, 0, 0, -INFINITY, b.seed};
+    CU(cudaMemcpyAsync(ctx->sst.p, &st0, sizeof st0, cudaMemcpyHostToDevice, ctx->s_main));
+    std::vector<double> zero(rs.E, 0.0);
+    CU((upload_as<S>(ctx->base, zero.data(), rs.E, ctx->s_main)));
+    CU((upload_as<S>(ctx->msv, zero.data(), rs.E, ctx->s_main)));
+    if (!std::is_same<S, double>::value) CU((upload_as<S>(ctx->bm, zero.data(), rs.E, ctx->s_main)));
+    CU(cudaMemcpyAsync(ctx->var.p, zero.data(), sizeof(double) * rs.E, cudaMemcpyHostToDevice, ctx->s_main));
+    if (b.cem) {
+      std::vector<double> sd0(rs.E, b.initial_std);
+      CU((upload_as<S>(ctx->bl_s, sd0.data(), rs.E, ctx->s_main)));
+      CU(cudaMemcpyAsync(ctx->bl_d.p, sd0.data(), sizeof(double) * rs.E, cudaMemcpyHostToDevice, ctx->s_main));
+    }
+    CU(cudaStreamSynchronize(ctx->s_main));
+  }
+  const bool graphs = philox && ctx->use_graphs;
+  if (graphs) {
+    char extra[200];
+    snprintf(extra, sizeof extra, "|baseline/%d/%.17g/%.17g/%lld/%.17g/%d/%p/%p/%p/%p/%p", b.cem ? 1 : 0, b.sigma,
+             b.lambda, (long long)b.k, b.min_std, b.iterations, (void*)ctx->sv.p, (void*)ctx->sst.p,
+             (void*)ctx->bl_s.p, (void*)ctx->bl_d.p, (void*)ctx->cub_tmp.p);
+    const std::string key = graph_key_of(ctx, rs) + extra;
+    if (!ctx->bl_exec || key != ctx->bl_key) {
+      if (ctx->bl_exec) cudaGraphExecDestroy(ctx->bl_exec);
+      ctx->bl_exec = nullptr;
+      cudaGraph_t g;
+      CU(cudaStreamBeginCapture(ctx->s_main, cudaStreamCaptureModeThreadLocal));
+      int r = enqueue_baseline_iteration<S>(ctx, rs, b, true, 0, b.iterations);
+      cudaError_t e = cudaStreamEndCapture(ctx->s_main, &g);
+      if (r) return r;
+      CU(e);
+      CU(cudaGraphInstantiate(&ctx->bl_exec, g, 0));
+      CU(cudaGraphDestroy(g));
+      ctx->bl_key = key;
+    }
+  }
+  int it_used = 0;
+  std::vector<double> rec(4);
+  for (int it = 1; it <= b.iterations; ++it) {
+    if (graphs) {
+      CU(cudaGraphLaunch(ctx->bl_exec, ctx->s_main));
+    } else {
+      if (int r = enqueue_baseline_iteration<S>(ctx, rs, b, philox, it, b.iterations)) return r;
+    }
+    CU(cudaStreamSynchronize(ctx->s_main));
+    if (int r = check_err(ctx, rs)) return r;
+    CU(cudaMemcpy(rec.data(), ctx->sv.p + L.rec + 4 * (size_t)(it - 1), sizeof(double) * 4, cudaMemcpyDeviceToHost));
+    const bool ok = rec[2] != 0.0;
+    if (per_it) per_it[it - 1] = {rec[0], rec[1], ok ? 1 : 0, elapsed()};
+    it_used = it;
+    if (b.stop_on_success && ok) break;
+    if (b.deadline > 0 && elapsed() >= b.deadline) break;
+  }
+  d4k::SolveState st{};
+  CU(cudaMemcpy(&st, ctx->sst.p, sizeof st, cudaMemcpyDeviceToHost));
+  if (best_states)
+    CU(cudaMemcpy(best_states, ctx->sv.p + L.best_states, sizeof(double) * (L.best_ctrl - L.best_states),
+                  cudaMemcpyDeviceToHost));
+  if (best_controls)
+    CU(cudaMemcpy(best_controls, ctx->sv.p + L.best_ctrl, sizeof(double) * (L.rec - L.best_ctrl),
+                  cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(rec.data(), ctx->sv.p + L.rec + 4 * (size_t)st.best_iter, sizeof(double) * 4, cudaMemcpyDeviceToHost));
+  if (used) *used = it_used;
+  if (best_reward) *best_reward = st.best_reward;
+  if (success) *success = rec[2] != 0.0 ? 1 : 0;
+  return D4ORM_OK;
+}
+
 }  // namespace
 
 // =================================================================== C-ABI
@@ -1077,6 +1375,50 @@ int d4orm_cuda_run_denoising(d4orm_cuda_ctx* ctx, const double* base, const d4or
   CU(cudaSetDevice(ctx->device));
   return ctx->precision == D4ORM_PREC_F64 ? run_denoising_t<double>(ctx, base, config, out_variable, trace)
                                           : run_denoising_t<float>(ctx, base, config, out_variable, trace);
+}
+
+int d4orm_cuda_mppi_solve(d4orm_cuda_ctx* ctx, const d4orm_mppi_config* config, double* best_states,
+                          double* best_controls, d4orm_iteration_rec* per_iteration, int* iterations_used,
+                          double* best_reward, int* success) {
+  CU(cudaSetDevice(ctx->device));
+  if (!config) return fail(ctx, D4ORM_E_INVALID, "mppi_solve: null config");
+  BaselineSpec b;
+  b.batch = config->batch;
+  b.lambda = config->lambda;
+  b.sigma = config->sigma;
+  b.iterations = config->iterations;
+  b.seed = config->seed;
+  b.stop_on_success = config->stop_on_success;
+  b.deadline = config->deadline_seconds;
+  b.what = "mppi_solve";
+  return ctx->precision == D4ORM_PREC_F64
+             ? baseline_solve_t<double>(ctx, b, best_states, best_controls, per_iteration, iterations_used,
+                                        best_reward, success)
+             : baseline_solve_t<float>(ctx, b, best_states, best_controls, per_iteration, iterations_used,
+                                       best_reward, success);
+}
+
+int d4orm_cuda_cem_solve(d4orm_cuda_ctx* ctx, const d4orm_cem_config* config, double* best_states,
+                         double* best_controls, d4orm_iteration_rec* per_iteration, int* iterations_used,
+                         double* best_reward, int* success) {
+  CU(cudaSetDevice(ctx->device));
+  if (!config) return fail(ctx, D4ORM_E_INVALID, "cem_solve: null config");
+  BaselineSpec b;
+  b.cem = true;
+  b.batch = config->batch;
+  b.elite_fraction = config->elite_fraction;
+  b.initial_std = config->initial_std;
+  b.min_std = config->min_std;
+  b.iterations = config->iterations;
+  b.seed = config->seed;
+  b.stop_on_success = config->stop_on_success;
+  b.deadline = config->deadline_seconds;
+  b.what = "cem_solve";
+  return ctx->precision == D4ORM_PREC_F64
+             ? baseline_solve_t<double>(ctx, b, best_states, best_controls, per_iteration, iterations_used,
+                                        best_reward, success)
+             : baseline_solve_t<float>(ctx, b, best_states, best_controls, per_iteration, iterations_used,
+                                       best_reward, success);
 }
 
 int d4orm_cuda_solve(d4orm_cuda_ctx* ctx, const d4orm_solve_config* config, double* best_states,

@@ -323,13 +323,28 @@ struct PartShape {
   static constexpr int THREADS = GROUPS * SUB;
 };
 
-template <typename S, typename W, int SUB>
-__global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const S* __restrict__ z,
-                                                                           const W* __restrict__ w,
-                                                                           const S* __restrict__ msv, S sd, int64_t M,
-                                                                           int64_t elems, S* __restrict__ partial) {
+template <typename S>
+struct PartArgs {
+  const S* z;        // [M][E] noise of this rank's samples
+  const S* msv;      // [E] mean-scaled variable (sample = msv + sd·z)
+  S sd;              // scalar std, or
+  const S* sdv;      // [E] per-element std (CEM), else null
+  const S* nm;       // DEV: [E] the new mean (CEM variance pass)
+  int64_t M, elems;
+  S* partial;        // [chunks][E]
+};
+
+// DEV = 0: Σ_m w_m·sample_m (mc_average, denoiser.cpp:92-108; CEM's elite sum
+// with w ∈ {0, 1}).  DEV = 1: Σ_m w_m·(sample_m − nm)² (CEM's variance,
+// baselines.cpp:162-167; zero-weight samples are skipped as the reference only
+// visits the elites).
+template <typename S, typename W, int SUB, int DEV>
+__global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const PartArgs<S> a,
+                                                                           const W* __restrict__ w) {
   constexpr int kPartGroups = PartShape<SUB>::GROUPS, kPartSub = SUB, kPartLanes = PartShape<SUB>::LANES;
   __shared__ S red[kPartSub][kPartGroups][4];
+  const S* __restrict__ z = a.z;
+  const int64_t M = a.M, elems = a.elems;
   const int g = threadIdx.x % kPartGroups, sr = threadIdx.x / kPartGroups;
   const int64_t e0 = ((int64_t)blockIdx.x * kPartGroups + g) * 4;
   const int64_t c = blockIdx.y;
@@ -337,8 +352,22 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
   const int n = e0 < elems ? (elems - e0 < 4 ? (int)(elems - e0) : 4) : 0;
   S acc[4] = {S(0), S(0), S(0), S(0)};
   if (n > 0) {
-    S mv[4] = {S(0), S(0), S(0), S(0)};
-    for (int j = 0; j < n; ++j) mv[j] = msv[e0 + j];
+    S mv[4] = {S(0), S(0), S(0), S(0)}, sv[4], nv[4] = {S(0), S(0), S(0), S(0)};
+    for (int j = 0; j < 4; ++j) sv[j] = a.sd;
+    for (int j = 0; j < n; ++j) {
+      mv[j] = a.msv[e0 + j];
+      if (a.sdv) sv[j] = a.sdv[e0 + j];
+      if (DEV) nv[j] = a.nm[e0 + j];
+    }
+    auto term = [&](S wm, S zv, int j) -> S {  // fp32: fused; the weight multiplies the (squared) sample
+      const S smp = fmaf(sv[j], zv, mv[j]);
+      if constexpr (DEV) {
+        const S d = smp - nv[j];
+        return wm * (d * d);
+      } else {
+        return wm * smp;
+      }
+    };
     bool vec = false;
     if constexpr (std::is_same<S, float>::value) vec = n == 4 && (elems & 3) == 0;
     if (vec) {
@@ -352,10 +381,17 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
           const float4 v = __ldcs(zp);
           zp += stride;
           const float wm = (float)__ldg(w + m);
-          acc[0] = fmaf(wm, fmaf(sd, v.x, mv[0]), acc[0]);
-          acc[1] = fmaf(wm, fmaf(sd, v.y, mv[1]), acc[1]);
-          acc[2] = fmaf(wm, fmaf(sd, v.z, mv[2]), acc[2]);
-          acc[3] = fmaf(wm, fmaf(sd, v.w, mv[3]), acc[3]);
+          if constexpr (DEV) {
+            acc[0] += term(wm, v.x, 0);
+            acc[1] += term(wm, v.y, 1);
+            acc[2] += term(wm, v.z, 2);
+            acc[3] += term(wm, v.w, 3);
+          } else {
+            acc[0] = fmaf(wm, fmaf(sv[0], v.x, mv[0]), acc[0]);
+            acc[1] = fmaf(wm, fmaf(sv[1], v.y, mv[1]), acc[1]);
+            acc[2] = fmaf(wm, fmaf(sv[2], v.z, mv[2]), acc[2]);
+            acc[3] = fmaf(wm, fmaf(sv[3], v.w, mv[3]), acc[3]);
+          }
         }
       } else if constexpr (std::is_same<S, float>::value) {
         for (int q0 = 0; q0 < kPartLanes; q0 += kPartBatch) {
@@ -374,21 +410,35 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
           }
 #pragma unroll
           for (int q = 0; q < kPartBatch; ++q) {
-            acc[0] = fmaf(wv[q], fmaf(sd, v[q].x, mv[0]), acc[0]);
-            acc[1] = fmaf(wv[q], fmaf(sd, v[q].y, mv[1]), acc[1]);
-            acc[2] = fmaf(wv[q], fmaf(sd, v[q].z, mv[2]), acc[2]);
-            acc[3] = fmaf(wv[q], fmaf(sd, v[q].w, mv[3]), acc[3]);
+            if constexpr (DEV) {
+              acc[0] += term(wv[q], v[q].x, 0);
+              acc[1] += term(wv[q], v[q].y, 1);
+              acc[2] += term(wv[q], v[q].z, 2);
+              acc[3] += term(wv[q], v[q].w, 3);
+            } else {
+              acc[0] = fmaf(wv[q], fmaf(sv[0], v[q].x, mv[0]), acc[0]);
+              acc[1] = fmaf(wv[q], fmaf(sv[1], v[q].y, mv[1]), acc[1]);
+              acc[2] = fmaf(wv[q], fmaf(sv[2], v[q].z, mv[2]), acc[2]);
+              acc[3] = fmaf(wv[q], fmaf(sv[3], v[q].w, mv[3]), acc[3]);
+            }
           }
         }
       }
     } else {
+      // reference arithmetic (fp64 parity path; also ragged fp32 tails)
       for (int q = 0; q < kPartLanes; ++q) {
         const int64_t m = mb + q;
         if (m >= M) break;
         const S wm = (S)w[m];
+        if (DEV && wm == S(0)) continue;
         for (int j = 0; j < n; ++j) {
-          const S smp = xadd(mv[j], xmul(sd, z[m * elems + e0 + j]));
-          acc[j] = xadd(acc[j], xmul(wm, smp));
+          const S smp = xadd(mv[j], xmul(sv[j], z[m * elems + e0 + j]));
+          if constexpr (DEV) {
+            const S d = xsub(smp, nv[j]);
+            acc[j] = xadd(acc[j], xmul(wm, xmul(d, d)));
+          } else {
+            acc[j] = xadd(acc[j], xmul(wm, smp));
+          }
         }
       }
     }
@@ -406,21 +456,39 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
     __syncthreads();
   }
   if (sr == 0 && n > 0) {
-    for (int j = 0; j < n; ++j) partial[c * elems + e0 + j] = red[0][g][j];
+    for (int j = 0; j < n; ++j) a.partial[c * elems + e0 + j] = red[0][g][j];
   }
 }
+
+// What the tree does with the total of each element.
+enum { FIN_UPDATE = 0, FIN_CEM_MEAN = 1, FIN_CEM_VAR = 2 };
+template <typename S>
+struct TreeFinal {
+  int mode;
+  // FIN_UPDATE (denoise_step, denoiser.cpp:110-117; MPPI with unit scales):
+  //   var ← scale·avg, msv ← next_ms·var, bm ← base + msv
+  double scale, next_ms;
+  double* var;
+  S* msv;
+  const S* base;
+  S* bm;
+  // CEM (baselines.cpp:157-170): FIN_CEM_MEAN  nm ← total / k;
+  //   FIN_CEM_VAR  std ← max(√(total / k), min_std), mean ← nm
+  double kdiv, min_std;
+  double* nm64;
+  S* nm_s;
+  const S* nm_in;
+  double* std64;
+  S* sdv;
+};
 
 // Pairwise (binary-counter) sum of the chunk partials — a balanced binary tree
 // when the chunk count is a power of two, so a rank owning an aligned block of
 // chunks computes exactly one subtree and results are identical for any GPU
-// count.  Then denoise_step (denoiser.cpp:110-117): var ← √ᾱ_{i−1}·avg, and the
-// next step's mean-scaled variable msv ← mean_scale_{i−1}·var (+ base → bm for
-// the fp32 rollout).
+// count.  Then the finalisation `f` (see TreeFinal).
 template <typename S>
 __global__ void __launch_bounds__(kThreads) k_wmean_tree(const S* __restrict__ partial, int64_t nchunks,
-                                                         int64_t elems, double scale, double next_ms,
-                                                         double* __restrict__ var, S* __restrict__ msv,
-                                                         const S* __restrict__ base, S* __restrict__ bm,
+                                                         int64_t elems, const TreeFinal<S> f,
                                                          S* __restrict__ root_out) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= elems) return;
@@ -449,11 +517,25 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree(const S* __restrict__ p
     root_out[e] = total;
     return;
   }
-  const double nv = scale * (double)total;
-  var[e] = nv;
-  const S m = (S)(next_ms * nv);
-  msv[e] = m;
-  if (bm) bm[e] = base[e] + m;
+  if (f.mode == FIN_UPDATE) {
+    const double nv = f.scale * (double)total;
+    f.var[e] = nv;
+    const S m = (S)(f.next_ms * nv);
+    f.msv[e] = m;
+    if (f.bm) f.bm[e] = f.base[e] + m;
+  } else if (f.mode == FIN_CEM_MEAN) {
+    const double nm = (double)total / f.kdiv;  // new_mean /= elite_count
+    f.nm64[e] = nm;
+    f.nm_s[e] = (S)nm;
+  } else {
+    const double sd = sqrt((double)total / f.kdiv);  // variance /= k; cwiseSqrt
+    const double s = sd < f.min_std ? f.min_std : sd;  // cwiseMax(min_std)
+    f.std64[e] = s;
+    f.sdv[e] = (S)s;
+    f.var[e] = f.nm64[e];  // mean.u = new_mean
+    f.msv[e] = f.nm_s[e];
+    if (f.bm) f.bm[e] = f.base[e] + f.nm_s[e];
+  }
 }
 
 template <typename S>

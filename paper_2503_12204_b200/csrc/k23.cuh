@@ -34,6 +34,7 @@ struct FitParams {
   const S* msv;          // [T][R][du]   mean_scale·variable (fp64 path)
   const S* bm;           // [T][R][du]   base + msv (fp32 path)
   S sd;                  // sampling std of this step
+  const S* sdv;          // CEM: per-element std [T][R][du] (replaces sd), else null
   const S* starts;       // [R][dx]
   const S* goals;        // [R][pd]
   const S* inv_dstart;   // [R]  fp32: 1/‖start−goal‖; fp64: ‖start−goal‖ (divide)
@@ -55,7 +56,7 @@ struct FitParams {
   S* states_out;         // [M][T+1][R][dx] or null
   S* controls_out;       // [M][T+1][R][du] or null
   unsigned long long* err;
-  // fused-noise mode (NOISE == 1): Philox key table, this step, z written for K5
+  // fused-noise mode (NOISE >= 1; 2 = with sdv): Philox key table, this step, z written for K5
   const uint2* keys;
   int step;
   S* z_store;            // [M][T][R][du]
@@ -465,13 +466,14 @@ __device__ __forceinline__ int chunk_key(float x, int k, int Rp2, bool real) {
 // Pointers advance by a stride per step (no per-step 64-bit index math).  The
 // returned value is 0 unless some state went non-finite (NaN/inf propagate
 // through fma(x, 0, acc)); the caller then replays the chunk exactly.
-template <int KIND, bool FULL>
-__device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, const float* bmp, float* zp, int RDU,
+template <int KIND, bool FULL, bool SDV>
+__device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, const float* bmp, const float* sdp,
+                                            float* zp, int RDU,
                                             uint64_t m, int kA, uint32_t g0, uint2 key, float* px, float* py, float* pz,
                                             int RS, float* x, float& eff32, float& chk, const float* ng, float ginv,
                                             float& gsd) {
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
-  float bq[kPF][DU];
+  float bq[kPF][DU], sq[SDV ? kPF : 1][DU];
 #pragma unroll
   for (int j = 0; j < kPF; ++j) {
     if (FULL || j < nb) {
@@ -482,6 +484,10 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
       } else {
 #pragma unroll
         for (int d = 0; d < DU; ++d) bq[j][d] = __ldg(bmp + j * RDU + d);
+      }
+      if constexpr (SDV) {
+#pragma unroll
+        for (int d = 0; d < DU; ++d) sq[j][d] = __ldg(sdp + j * RDU + d);
       }
     }
   }
@@ -520,7 +526,8 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
       for (int d = 0; d < DU; ++d) {
         // base + (mean_scale·var + std·z), clamped; FMNMX equals cwiseMax/Min
         // here because NaN inputs are rejected on the host before launch
-        u[d] = fminf(fmaxf(fmaf(p.sd, nz[j * DU + d], bq[j][d]), p.lower[d]), p.upper[d]);
+        const float sdj = SDV ? sq[SDV ? j : 0][d] : p.sd;
+        u[d] = fminf(fmaxf(fmaf(sdj, nz[j * DU + d], bq[j][d]), p.lower[d]), p.upper[d]);
         eff32 = fmaf(u[d], u[d], eff32);
       }
       rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
@@ -536,7 +543,7 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
   }
 }
 
-template <int KIND>
+template <int KIND, bool SDV>
 __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const FitSmem<float>& sm, int sA, int kA,
                                                int rA, int64_t m, int t0, int nsteps, float* x, float* zrow, uint2 key,
                                                float& eff32, const float* ng, float ginv, float& gsd) {
@@ -544,6 +551,7 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
   const int RDU = p.R * DU;
   const int64_t e0 = ((int64_t)t0 * p.R + kA) * DU;
   const float* bmp = p.bm + e0;
+  const float* sdp = SDV ? p.sdv + e0 : nullptr;
   float* zp = zrow + e0;
   float* px = sm.row(0, sA, 0) + rA;
   float* py = sm.row(1, sA, 0) + rA;
@@ -554,13 +562,14 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
     const int nb = nsteps - tc;
     const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
     if (nb >= kPF) {
-      fused_block<KIND, true>(p, kPF, bmp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk, ng,
+      fused_block<KIND, true, SDV>(p, kPF, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk, ng,
                               ginv, gsd);
     } else {
-      fused_block<KIND, false>(p, nb, bmp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk, ng,
+      fused_block<KIND, false, SDV>(p, nb, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk, ng,
                                ginv, gsd);
     }
     bmp += kPF * RDU;
+    if constexpr (SDV) sdp += kPF * RDU;
     zp += kPF * RDU;
     px += kPF * RS;
     py += kPF * RS;
@@ -582,7 +591,8 @@ __device__ __noinline__ void rollout_check(const FitParams<float>& p, int kA, in
     const int t = t0 + tc;
     const int64_t e = ((int64_t)t * p.R + kA) * DU;
     float u[DU];
-    for (int d = 0; d < DU; ++d) u[d] = fminf(fmaxf(fmaf(p.sd, zrow[e + d], p.bm[e + d]), p.lower[d]), p.upper[d]);
+    for (int d = 0; d < DU; ++d)
+      u[d] = fminf(fmaxf(fmaf(p.sdv ? p.sdv[e + d] : p.sd, zrow[e + d], p.bm[e + d]), p.lower[d]), p.upper[d]);
     rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
     bool fin = true;
     for (int q = 0; q < DX; ++q) fin = fin && isfinite(x[q]);
@@ -681,15 +691,16 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
   // variable (L2-resident).  NOISE == 1: the noise is drawn here in registers
   // (Philox, d4orm_common.cuh) block by block and written once for K5.  Both
   // are chunk-local, so they hold no registers during the fitness phase.
-  S zq[kPF][DU], bq[kPF][DU], mq[kPF][F32 ? 1 : DU];
-  S* zst = NOISE == 1 ? p.z_store + (liveA ? mA : 0) * (int64_t)T * R * DU : nullptr;
-  const uint2 key = NOISE == 1 ? p.keys[p.step] : make_uint2(0u, 0u);
+  S zq[kPF][DU], bq[kPF][DU], mq[kPF][F32 ? 1 : DU], sq[kPF][DU];
+  S* zst = NOISE >= 1 ? p.z_store + (liveA ? mA : 0) * (int64_t)T * R * DU : nullptr;
+  const uint2 key = NOISE >= 1 ? p.keys[p.step] : make_uint2(0u, 0u);
   auto fetch = [&](int t, int t_end, int slot) {
     if (NOISE == 0 && robotA && t < t_end) {
       const int64_t e = ((int64_t)t * R + kA) * DU;
 #pragma unroll
       for (int d = 0; d < DU; ++d) {
         zq[slot][d] = __ldcs(zrow + e + d);
+        sq[slot][d] = p.sdv ? __ldg(p.sdv + e + d) : p.sd;
         if constexpr (F32) {
           bq[slot][d] = __ldg(p.bm + e + d);
         } else {
@@ -733,14 +744,14 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
       }
     }
     // ===== phase A: integrate TC steps
-    if constexpr (NOISE == 1) {
+    if constexpr (NOISE >= 1) {
       if (robotA) {
         const int nsteps = t0 + TC < T ? TC : T - t0;
         float x0[DX];
 #pragma unroll
         for (int q = 0; q < DX; ++q) x0[q] = x[q];
         float gsd = 0.f;
-        const float chk = rollout_fused<KIND>(p, sm, sA, kA, rA, p.m_global0 + mA, t0, nsteps, x, zst, key, eff32,
+        const float chk = rollout_fused<KIND, NOISE == 2>(p, sm, sA, kA, rA, p.m_global0 + mA, t0, nsteps, x, zst, key, eff32,
                                               ng, ginv, gsd);
         goalA += (double)nsteps - (double)gsd;
         if (!(chk == 0.f)) rollout_check<KIND>(p, kA, p.m_global0 + mA, t0, nsteps, x0, zst);
@@ -762,9 +773,9 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
               if constexpr (F32) {
                 // base + (mean_scale·var + std·z), clamped (FMNMX; NaN inputs are
                 // rejected on the host before launch, so this equals cwiseMax/Min)
-                v = fminf(fmaxf(fmaf(p.sd, zq[j][d], bq[j][d]), p.lower[d]), p.upper[d]);
+                v = fminf(fmaxf(fmaf(sq[j][d], zq[j][d], bq[j][d]), p.lower[d]), p.upper[d]);
               } else {
-                v = xadd(bq[j][d], xadd(mq[j][d], xmul(p.sd, zq[j][d])));
+                v = xadd(bq[j][d], xadd(mq[j][d], xmul(sq[j][d], zq[j][d])));
                 v = (v < p.lower[d]) ? p.lower[d] : v;  // cwiseMax(lower), dynamics.cpp:78
                 v = (p.upper[d] < v) ? p.upper[d] : v;  // cwiseMin(upper)
               }

@@ -1,7 +1,8 @@
 // k23_launch.cuh — launch glue for the fused rollout+fitness kernel (K2+K3).
 // Instantiated per model kind in k23_k<kind>.cu so the 6 kinds × {f32,f64} ×
 // robot-tile × noise-source variants compile in parallel.  Fused Philox noise
-// (NOISE=1) exists for fp32 only; the fp64 parity path reads z from HBM.
+// (NOISE=1, and NOISE=2 with CEM's per-element std) exists for fp32 only; the
+// fp64 parity path reads z from HBM.
 #pragma once
 
 #include "d4orm_kernels.cuh"
@@ -36,6 +37,7 @@ template <typename S, int KIND>
 cudaError_t launch_k23(int tb, int maxw, int noise, dim3 grid, int threads, size_t smem, cudaStream_t st,
                        const FitParams<S>& p) {
   if constexpr (std::is_same<S, float>::value) {
+    if (noise && p.sdv) return launch_k23_n<S, KIND, 2>(tb, maxw, grid, threads, smem, st, p);  // CEM
     if (noise) return launch_k23_n<S, KIND, 1>(tb, maxw, grid, threads, smem, st, p);
   } else {
     if (noise) return cudaErrorInvalidValue;

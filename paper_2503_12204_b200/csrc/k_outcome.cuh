@@ -76,7 +76,8 @@ __global__ void k_iter_begin(const IterBeginParams<S> p) {
 }
 
 struct OutcomeParams {
-  double* ctrl;            // [T][R][du] in: base (current executed controls); out: new executed controls
+  const double* ctrl_in;   // [T][R][du] base: current executed controls (solve) | zeros (MPPI / CEM)
+  double* ctrl;            // [T][R][du] out: the new executed controls (may alias ctrl_in)
   const double* var;       // [E] Δ
   const double* starts;    // [R][dx]
   const double* goals;     // [R][pd]
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256) k_outcome(const OutcomeParams p) {
       const size_t e = ((size_t)t * R + k) * DU;
 #pragma unroll
       for (int d = 0; d < DU; ++d) {
-        double v = xadd(p.ctrl[e + d], p.var[e + d]);  // base_controls.u + denoised.variable.u
+        double v = xadd(p.ctrl_in[e + d], p.var[e + d]);  // base_controls.u + denoised.variable.u
         v = (v < p.lower[d]) ? p.lower[d] : v;         // cwiseMax(lower)
         v = (p.upper[d] < v) ? p.upper[d] : v;         // cwiseMin(upper)
         u[d] = v;
@@ -233,6 +234,42 @@ __global__ void __launch_bounds__(256) k_outcome(const OutcomeParams p) {
   if (s_better) {
     for (int e = tid; e < (T + 1) * R * DX; e += nt) p.best_states[e] = p.states[e];
     for (int e = tid; e < (T + 1) * R * DU; e += nt) p.best_ctrl[e] = e < T * R * DU ? p.ctrl[e] : 0.0;
+  }
+}
+
+// K8: start of an MPPI / CEM iteration (baselines.cpp:116-119,152-155): the
+// Philox key of iteration it = mix_seed(seed, it), so sample m's noise is the
+// counter stream (·, m, k) of that key — the analogue of the reference's
+// NormalStream(mix_seed(seed, it, m)).
+__global__ void k_baseline_begin(uint2* keys, const SolveState* st, unsigned long long* err) {
+  if (threadIdx.x == 0) {
+    const uint64_t v = mix_seed_dev(st->seed, (uint64_t)(st->iter + 1));
+    keys[0] = make_uint2((uint32_t)v, (uint32_t)(v >> 32));
+    *err = ~0ull;
+  }
+}
+
+// CEM elite selection (select_elites, baselines.cpp:86-97): `order` is the
+// stable descending sort of the rewards (ties keep the lower index first), so
+// the first k entries are the elites; their weight is 1, every other 0 (the
+// elite sum is divided by k in the tree, as new_mean /= elite_count).
+__global__ void k_elite_weights(const int* __restrict__ order, int64_t M, int64_t k, double* __restrict__ w64,
+                                float* __restrict__ w32) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < M) {
+    const int m = order[j];
+    w64[m] = j < k ? 1.0 : 0.0;
+    w32[m] = j < k ? 1.0f : 0.0f;
+  }
+}
+
+// Sort input: rewards with −0 folded into +0 (the reference's `>` treats them
+// as equal; radix keys would not) and the sample indices.
+__global__ void k_sort_prep(const double* __restrict__ r, int64_t M, double* __restrict__ keys, int* __restrict__ idx) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < M) {
+    keys[j] = r[j] + 0.0;
+    idx[j] = (int)j;
   }
 }
 

@@ -241,6 +241,44 @@ class GpuDenoiser:
         return result
 
 
+    # ---------------------------------------------------------- baselines
+    def _baseline(self, fn, cfg_c, iterations, batch):
+        p = self.problem
+        best_states = np.empty((p.horizon + 1, p.robots, p.dx))
+        best_controls = np.empty((p.horizon + 1, p.robots, p.du))
+        recs = (_lib.IterationRec_C * iterations)()
+        used, ok = C.c_int(), C.c_int()
+        best = C.c_double()
+        t0 = time.perf_counter()
+        self._check(fn(self._h, C.byref(cfg_c), dptr(best_states), dptr(best_controls), recs, C.byref(used),
+                       C.byref(best), C.byref(ok)))
+        result = SolveResult()
+        result.iterations_used = used.value
+        result.total_denoise_steps = used.value
+        result.per_iteration = [(r.reward, r.objective, bool(r.success), r.elapsed) for r in recs[: used.value]]
+        result.best_reward = best.value
+        result.best_states, result.best_controls = best_states, best_controls
+        result.success = bool(ok.value)
+        result.wall_time = time.perf_counter() - t0
+        return result
+
+    def mppi_solve(self, batch: int = 2048, lam: float = 0.1, sigma: float = 1.0, iterations: int = 1000,
+                   seed: int = 0, stop_on_success: bool = True, deadline_seconds: float | None = None):
+        """mppi_solve (baselines.cpp:99-129) on the device; host-noise providers
+        receive the iteration as `step` (stream mix_seed(seed, it, m))."""
+        c = _lib.MppiConfig_C(batch, lam, sigma, iterations, seed & ((1 << 64) - 1), int(stop_on_success),
+                              float(deadline_seconds or 0.0))
+        return self._baseline(self._L.d4orm_cuda_mppi_solve, c, iterations, batch)
+
+    def cem_solve(self, batch: int = 2048, elite_fraction: float = 0.1, initial_std: float = 1.0,
+                  min_std: float = 0.05, iterations: int = 1000, seed: int = 0, stop_on_success: bool = True,
+                  deadline_seconds: float | None = None):
+        """cem_solve (baselines.cpp:131-173) on the device."""
+        c = _lib.CemConfig_C(batch, elite_fraction, initial_std, min_std, iterations, seed & ((1 << 64) - 1),
+                             int(stop_on_success), float(deadline_seconds or 0.0))
+        return self._baseline(self._L.d4orm_cuda_cem_solve, c, iterations, batch)
+
+
 @dataclass
 class SolveResult:
     """SolveResult (result.hpp:20-29)."""

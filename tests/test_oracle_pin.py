@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 from paper_2503_12204_b200 import scenarios as S
-from oracle.oracle import make_config
+from oracle.oracle import cem_config, make_config, mppi_config
 
 GOLDEN = Path(__file__).parent / "golden"
 
@@ -203,6 +203,34 @@ def test_pin_solve(oracle, reference, name):
     b = reference.solve(p, cfg, max_iterations=3, stop_on_success=False)
     np.testing.assert_array_equal(a["states"], b["states"])
     assert a["best_reward"] == b["best_reward"] and a["per_iteration"] == b["per_iteration"]
+
+
+@pytest.mark.parametrize("name", ["holo2d", "C2", "C3"])
+def test_pin_mppi_cem(oracle, reference, name):
+    """MPPI / CEM baselines (baselines.cpp:99-173): the C restatement bitwise
+    against the reference's own mppi_solve / cem_solve (native kinds) or the
+    same statements with the extension rollout."""
+    p = PIN_PROBLEMS[name]()
+    mc = mppi_config(24, sigma=0.7, iterations=3, seed=5, stop_on_success=False)
+    a, b = oracle.mppi_solve(p, mc), reference.mppi_solve(p, mc)
+    np.testing.assert_array_equal(a["states"], b["states"])
+    assert a["best_reward"] == b["best_reward"] and a["per_iteration"] == b["per_iteration"]
+    assert a["iterations"] == b["iterations"] == 3
+    cc = cem_config(40, elite_fraction=0.2, initial_std=0.8, min_std=0.05, iterations=3, seed=9, stop_on_success=False)
+    a, b = oracle.cem_solve(p, cc), reference.cem_solve(p, cc)
+    np.testing.assert_array_equal(a["states"], b["states"])
+    assert a["best_reward"] == b["best_reward"] and a["per_iteration"] == b["per_iteration"]
+
+
+def test_pin_select_elites(oracle, reference):
+    rng = np.random.default_rng(3)
+    for m, k in [(10, 3), (64, 6), (257, 25), (5, 5), (7, 1)]:
+        r = np.round(rng.normal(size=m), 1)  # many ties: lower index wins
+        assert oracle.select_elites(r, k) == reference.select_elites(r, k)
+    with pytest.raises(ValueError, match="elite count out of range"):
+        oracle.select_elites(np.zeros(4), 5)
+    with pytest.raises(ValueError, match="elite count out of range"):
+        reference.select_elites(np.zeros(4), 0)
 
 
 def test_pin_generators(reference):
