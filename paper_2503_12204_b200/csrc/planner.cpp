@@ -1,5 +1,5 @@
 // planner.cpp — the C++ drop-in of the reference planner interface
-// (proj/include/d4orm/{dynamics,reward,schedule,denoiser,optimizer,scenario}.hpp)
+// (proj/include/d4orm/{dynamics,reward,schedule,denoiser,optimizer,scenario,baselines}.hpp)
 // over the B200 C-ABI (include/d4orm_cuda.h).
 //
 //   run_denoising   → d4orm_cuda_run_denoising (the hot path, GPU only)
@@ -24,6 +24,7 @@
 #include <thread>
 #include <vector>
 
+#include "../../include/d4orm/baselines.hpp"
 #include "../../include/d4orm/denoiser.hpp"
 #include "../../include/d4orm/dynamics.hpp"
 #include "../../include/d4orm/gpu.hpp"
@@ -733,6 +734,87 @@ SolveResult solve(const Scenario& scenario, const DynamicsModel& model, const Op
   result.total_denoise_steps = static_cast<long long>(used) * dcfg.steps;
   result.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return result;
+}
+
+// ================================================================= baselines
+std::vector<int> select_elites(const Vector& rewards, int count) {
+  if (count < 1 || count > rewards.size()) throw std::invalid_argument("select_elites: elite count out of range");
+  std::vector<int> order(static_cast<std::size_t>(rewards.size()));
+  for (std::size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+  std::stable_sort(order.begin(), order.end(), [&rewards](int a, int b) { return rewards[a] > rewards[b]; });
+  order.resize(static_cast<std::size_t>(count));
+  std::sort(order.begin(), order.end());
+  return order;
+}
+
+namespace {
+template <class Fn>
+SolveResult baseline_result(const Scenario& scenario, const DynamicsModel& model, int horizon, double dt, int iterations,
+                            std::uint64_t seed, int workers, const char* what, Fn&& call) {
+  validate_scenario(scenario);
+  if (scenario.model_kind != model.kind)
+    throw std::invalid_argument(std::string(what) + ": scenario model kind mismatch");
+  const ProblemArrays pa = make_problem(scenario, model, horizon, dt);
+  const bool host = g_opts.host_noise;
+  d4orm_cuda_ctx* c = gpu(0, pa, g_opts.precision, host ? D4ORM_NOISE_HOST : D4ORM_NOISE_PHILOX, g_opts.graphs);
+  if (host) {  // the provider's step is the iteration: NormalStream(mix_seed(seed, it, m))
+    g_noise = {seed, workers};
+    throw_for(d4orm_cuda_set_noise_fn(c, host_noise_fn, &g_noise), d4orm_cuda_last_error(c));
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  const int R = scenario.robots;
+  SolveResult result;
+  result.best_trajectory = {R, model.state_dim, model.control_dim, dt,
+                            Matrix(static_cast<Index>(R) * model.state_dim, horizon + 1),
+                            Matrix(static_cast<Index>(R) * model.control_dim, horizon + 1)};
+  std::vector<d4orm_iteration_rec> recs(static_cast<size_t>(std::max(iterations, 1)));
+  int used = 0, ok = 0;
+  double best = 0.0;
+  throw_for(call(c, result.best_trajectory.states.data(), result.best_trajectory.controls.data(), recs.data(), &used,
+                 &best, &ok),
+            d4orm_cuda_last_error(c));
+  for (int it = 0; it < used; ++it)
+    result.per_iteration.push_back({recs[it].reward, recs[it].objective, recs[it].success != 0, recs[it].elapsed});
+  result.best_reward = best;
+  result.success = ok != 0;
+  result.iterations_used = used;
+  result.total_denoise_steps = used;
+  result.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return result;
+}
+}  // namespace
+
+SolveResult mppi_solve(const Scenario& scenario, const DynamicsModel& model, const MppiConfig& config) {
+  d4orm_mppi_config mc{};
+  mc.batch = config.batch;
+  mc.lambda = config.lambda;
+  mc.sigma = config.sigma;
+  mc.iterations = config.iterations;
+  mc.seed = config.seed;
+  mc.stop_on_success = config.stop_on_success ? 1 : 0;
+  mc.deadline_seconds = config.deadline_seconds ? *config.deadline_seconds : 0.0;
+  return baseline_result(scenario, model, config.horizon, config.dt, config.iterations, config.seed, config.workers,
+                         "mppi_solve", [&](d4orm_cuda_ctx* c, double* st, double* ct, d4orm_iteration_rec* r, int* u,
+                                           double* b, int* ok) {
+                           return d4orm_cuda_mppi_solve(c, &mc, st, ct, r, u, b, ok);
+                         });
+}
+
+SolveResult cem_solve(const Scenario& scenario, const DynamicsModel& model, const CemConfig& config) {
+  d4orm_cem_config cc{};
+  cc.batch = config.batch;
+  cc.elite_fraction = config.elite_fraction;
+  cc.initial_std = config.initial_std;
+  cc.min_std = config.min_std;
+  cc.iterations = config.iterations;
+  cc.seed = config.seed;
+  cc.stop_on_success = config.stop_on_success ? 1 : 0;
+  cc.deadline_seconds = config.deadline_seconds ? *config.deadline_seconds : 0.0;
+  return baseline_result(scenario, model, config.horizon, config.dt, config.iterations, config.seed, config.workers,
+                         "cem_solve", [&](d4orm_cuda_ctx* c, double* st, double* ct, d4orm_iteration_rec* r, int* u,
+                                          double* b, int* ok) {
+                           return d4orm_cuda_cem_solve(c, &cc, st, ct, r, u, b, ok);
+                         });
 }
 
 }  // namespace d4orm

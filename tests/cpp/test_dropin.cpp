@@ -6,6 +6,7 @@
 #include <stdexcept>
 #include <string>
 
+#include "d4orm/baselines.hpp"
 #include "d4orm/denoiser.hpp"
 #include "d4orm/gpu.hpp"
 #include "d4orm/optimizer.hpp"
@@ -74,6 +75,35 @@ int main() {
   std::printf("\"solve_best\": %.17g, \"solve_iters\": %d, \"solve_success\": %d,\n", sr.best_reward, sr.iterations_used,
               sr.success ? 1 : 0);
   print_matrix("solve_states", sr.best_trajectory.states);
+  // 4b. MPPI / CEM baselines in correctness mode
+  {
+    MppiConfig mc;
+    mc.batch = 200;
+    mc.sigma = 0.6;
+    mc.iterations = 3;
+    mc.seed = 4;
+    mc.horizon = H;
+    mc.stop_on_success = false;
+    SolveResult mr = mppi_solve(bc.scenario, bc.model, mc);
+    std::printf("\"mppi_best\": %.17g, \"mppi_iters\": %d,\n", mr.best_reward, mr.iterations_used);
+    print_matrix("mppi_states", mr.best_trajectory.states);
+    CemConfig cc;
+    cc.batch = 200;
+    cc.elite_fraction = 0.1;
+    cc.initial_std = 0.7;
+    cc.iterations = 3;
+    cc.seed = 4;
+    cc.horizon = H;
+    cc.stop_on_success = false;
+    SolveResult cr = cem_solve(bc.scenario, bc.model, cc);
+    std::printf("\"cem_best\": %.17g, \"cem_iters\": %d,\n", cr.best_reward, cr.iterations_used);
+    print_matrix("cem_states", cr.best_trajectory.states);
+    Vector rw(7);
+    const double vals[7] = {0.5, 0.9, 0.5, -1.0, 0.9, 0.2, 0.9};
+    for (int j = 0; j < 7; ++j) rw[j] = vals[j];
+    const std::vector<int> el = select_elites(rw, 3);
+    std::printf("\"elites\": [%d, %d, %d],\n", el[0], el[1], el[2]);
+  }
   // 5. throughput mode (fp32 + Philox) runs and is deterministic
   o.precision = D4ORM_PREC_F32;
   o.host_noise = false;

@@ -32,7 +32,8 @@ def test_library_exports_all_symbols():
     syms = subprocess.run(["nm", "-DC", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     for fn in ("d4orm::run_denoising(", "d4orm::solve(", "d4orm::iterate(", "d4orm::rollout(", "d4orm::batch_rollout(",
                "d4orm::score_weights(", "d4orm::make_schedule(", "d4orm::validate_scenario(", "d4orm::antipodal_circle(",
-               "d4orm::total_reward(", "d4orm::check_success("):
+               "d4orm::total_reward(", "d4orm::check_success(", "d4orm::mppi_solve(", "d4orm::cem_solve(",
+               "d4orm::select_elites("):
         assert fn in syms, fn
 
 

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 from paper_2503_12204_b200 import scenarios as S
-from oracle.oracle import make_config
+from oracle.oracle import cem_config, make_config, mppi_config
 
 ROOT = Path(__file__).resolve().parents[1]
 pytestmark = pytest.mark.gpu
@@ -65,3 +65,18 @@ def test_solve_correctness_mode(dropin, oracle):
 def test_throughput_mode_deterministic_and_errors(dropin):
     assert dropin["f32_repeat_maxdiff"] == 0.0
     assert dropin["err_batch"] == "run_denoising: batch must be >= 2"
+
+
+def test_baselines_correctness_mode(dropin, oracle):
+    """mppi_solve / cem_solve through the C++ drop-in (baselines.hpp) vs the oracle."""
+    p = S.baseline_config(2).problem.with_horizon(16)
+    r = oracle.mppi_solve(p, mppi_config(200, sigma=0.6, iterations=3, seed=4, stop_on_success=False))
+    assert dropin["mppi_iters"] == r["iterations"] == 3
+    assert abs(dropin["mppi_best"] - r["best_reward"]) < 1e-9
+    np.testing.assert_allclose(np.array(dropin["mppi_states"]), r["states"].ravel(), rtol=1e-9, atol=1e-9)
+    r = oracle.cem_solve(p, cem_config(200, elite_fraction=0.1, initial_std=0.7, iterations=3, seed=4,
+                                       stop_on_success=False))
+    assert dropin["cem_iters"] == r["iterations"] == 3
+    assert abs(dropin["cem_best"] - r["best_reward"]) < 1e-9
+    np.testing.assert_allclose(np.array(dropin["cem_states"]), r["states"].ravel(), rtol=1e-9, atol=1e-9)
+    assert dropin["elites"] == oracle.select_elites(np.array([0.5, 0.9, 0.5, -1.0, 0.9, 0.2, 0.9]), 3) == [1, 4, 6]
