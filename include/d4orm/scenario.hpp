@@ -1,7 +1,7 @@
 #pragma once
-// Drop-in for proj/include/d4orm/scenario.hpp:17-57 (problem setup).  JSON
-// I/O (scenario_to_json / scenario_from_json) is not part of the hot path and
-// is left to the caller.
+// Drop-in for proj/include/d4orm/scenario.hpp:17-61 (problem setup and the
+// scenario JSON schema v1; the JSON functions are declared when nlohmann's
+// single header json.hpp is on the include path, as in the reference build).
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -58,5 +58,19 @@ struct BaselineConfig {
 };
 /// BASELINE.json configs[index-1], index 1..5.
 BaselineConfig baseline_config(int index);
+
+}  // namespace d4orm
+
+#if __has_include(<json.hpp>)
+#include <json.hpp>
+namespace d4orm {
+/// Scenario JSON schema v1 (scenario.cpp:296-378); "model" accepts the
+/// extension kinds too, and the state dimension follows the kind.
+nlohmann::json scenario_to_json(const Scenario& scenario);
+Scenario scenario_from_json(const nlohmann::json& j);
+}  // namespace d4orm
+#endif
+
+namespace d4orm {
 
 }  // namespace d4orm

@@ -22,6 +22,7 @@
 
 #include "../oracle/d4orm_oracle.h"
 #include "d4orm/baselines.hpp"
+#include "d4orm/bench.hpp"
 #include "d4orm/denoiser.hpp"
 #include "d4orm/dynamics.hpp"
 #include "d4orm/optimizer.hpp"
@@ -626,6 +627,64 @@ int ref_cem_solve(const or_problem* p, const or_cem_config* c, double* best_stat
   } catch (const std::exception& ex) {
     g_ref_err = ex.what();
     return -1;
+  }
+}
+
+// ------------------------------------------------- trial harness / scenario I/O
+// (bench.cpp:46-260, scenario.cpp:296-378) for pinning the drop-in's host logic.
+static int copy_out(const std::string& v, char* out, int cap) {
+  if (static_cast<int>(v.size()) + 1 > cap) {
+    g_ref_err = "output buffer too small";
+    return 1;
+  }
+  std::memcpy(out, v.c_str(), v.size() + 1);
+  return 0;
+}
+
+/* read_trial_csv on each path, aggregate, aggregate_to_json().dump() */
+int ref_aggregate_csv(const char** paths, int n, char* out, int cap) {
+  try {
+    std::vector<TrialRecord> recs;
+    for (int i = 0; i < n; ++i) recs.push_back(read_trial_csv(paths[i]));
+    return copy_out(aggregate_to_json(aggregate(recs)).dump(), out, cap);
+  } catch (const std::exception& ex) {
+    g_ref_err = ex.what();
+    return 2;
+  }
+}
+
+/* read_trial_csv then write_trial_csv (the reference's own CSV text) */
+int ref_csv_roundtrip(const char* in_path, const char* out_path) {
+  try {
+    write_trial_csv(read_trial_csv(in_path), out_path);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_ref_err = ex.what();
+    return 2;
+  }
+}
+
+/* scenario_to_json(scenario_from_json(text)).dump(): the reference's parser
+ * and writer (native model kinds only) */
+int ref_scenario_json_roundtrip(const char* text, char* out, int cap) {
+  try {
+    return copy_out(scenario_to_json(scenario_from_json(nlohmann::json::parse(text))).dump(), out, cap);
+  } catch (const std::exception& ex) {
+    g_ref_err = ex.what();
+    return 2;
+  }
+}
+
+/* scenario_to_json(antipodal_circle(robots, diameter, kind)).dump() */
+int ref_antipodal_circle_json(int robots, double diameter, int kind, char* out, int cap) {
+  try {
+    return copy_out(
+        scenario_to_json(antipodal_circle(robots, diameter, kind == 0 ? ModelKind::DiffDrive : ModelKind::Holo2D))
+            .dump(),
+        out, cap);
+  } catch (const std::exception& ex) {
+    g_ref_err = ex.what();
+    return 2;
   }
 }
 

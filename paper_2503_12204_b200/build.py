@@ -21,8 +21,19 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "build"
 LIB = PKG / "libd4orm_b200.so"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _json_dir() -> list[str]:
+    """nlohmann json.hpp (header-only, shipped in the image's cudnn_frontend
+    package) for the scenario / trajectory / trial I/O of the C++ drop-in — the
+    same single header the reference vendors (proj/CMakeLists.txt:5)."""
+    for sp in sys.path:
+        d = Path(sp) / "include" / "cudnn_frontend" / "thirdparty" / "nlohmann"
+        if (d / "json.hpp").exists():
+            return [f"-I{d}"]
+    return []
+
+
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-              f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+              f"-I{ROOT / 'include'}", f"-I{CSRC}", *_json_dir()]
 
 
 def _nvcc() -> str:
