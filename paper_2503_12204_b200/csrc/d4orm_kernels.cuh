@@ -49,6 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_philox_noise(S* __restrict__ z, in
 }
 
 // ------------------------------------------------------------ K4 weights
+constexpr double kW32Floor = 3.5527136788005009e-15;  // 2^-48: relative weight below which w32 = 0
 struct WeightParams {
   const double* reward;  // [M] all samples (global)
   int64_t M;
@@ -214,7 +215,10 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
     if (j < p.M) {
       const double w = e[q] * rsum;
       p.w64[j] = w;
-      p.w32[j] = (float)w;
+      // fp32 weights drive the fp32 weighted mean (K5): a sample whose weight
+      // is below 2^-48 of the largest cannot move an fp32 sum (even M = 2^18
+      // of them add < 1e-9 of the total) and its z row is not read at all
+      p.w32[j] = e[q] >= kW32Floor ? (float)w : 0.f;
       if (w > 0.0) h -= w * (r[q] - lsum);
     }
   }
@@ -352,12 +356,16 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
   const int n = e0 < elems ? (elems - e0 < 4 ? (int)(elems - e0) : 4) : 0;
   S acc[4] = {S(0), S(0), S(0), S(0)};
   if (n > 0) {
+    // (constant-index loops with predication keep these in registers)
     S mv[4] = {S(0), S(0), S(0), S(0)}, sv[4], nv[4] = {S(0), S(0), S(0), S(0)};
-    for (int j = 0; j < 4; ++j) sv[j] = a.sd;
-    for (int j = 0; j < n; ++j) {
-      mv[j] = a.msv[e0 + j];
-      if (a.sdv) sv[j] = a.sdv[e0 + j];
-      if (DEV) nv[j] = a.nm[e0 + j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sv[j] = a.sd;
+      if (j < n) {
+        mv[j] = a.msv[e0 + j];
+        if (a.sdv) sv[j] = a.sdv[e0 + j];
+        if (DEV) nv[j] = a.nm[e0 + j];
+      }
     }
     auto term = [&](S wm, S zv, int j) -> S {  // fp32: fused; the weight multiplies the (squared) sample
       const S smp = fmaf(sv[j], zv, mv[j]);
@@ -377,10 +385,10 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
         const int64_t stride = elems / 4;
         const int64_t me = mb + kPartLanes < M ? mb + kPartLanes : M;
 #pragma unroll 4
-        for (int64_t m = mb; m < me; ++m) {
-          const float4 v = __ldcs(zp);
-          zp += stride;
+        for (int64_t m = mb; m < me; ++m, zp += stride) {
           const float wm = (float)__ldg(w + m);
+          if (wm == 0.f) continue;  // uniform across the CTA: zero-weight rows are not read
+          const float4 v = __ldcs(zp);
           if constexpr (DEV) {
             acc[0] += term(wm, v.x, 0);
             acc[1] += term(wm, v.y, 1);
@@ -400,6 +408,8 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
 #pragma unroll
           for (int q = 0; q < kPartBatch; ++q) {
             const int64_t m = mb + q0 + q;
+            // (small E: L2-resident, so loads are issued unconditionally — a
+            // weight-dependent load would serialise two round trips)
             if (m < M) {
               v[q] = __ldcs(reinterpret_cast<const float4*>(z + m * elems + e0));
               wv[q] = (float)__ldg(w + m);
@@ -431,7 +441,9 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
         if (m >= M) break;
         const S wm = (S)w[m];
         if (DEV && wm == S(0)) continue;
-        for (int j = 0; j < n; ++j) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j >= n) break;
           const S smp = xadd(mv[j], xmul(sv[j], z[m * elems + e0 + j]));
           if constexpr (DEV) {
             const S d = xsub(smp, nv[j]);
@@ -456,7 +468,9 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
     __syncthreads();
   }
   if (sr == 0 && n > 0) {
-    for (int j = 0; j < n; ++j) a.partial[c * elems + e0 + j] = red[0][g][j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < n) a.partial[c * elems + e0 + j] = red[0][g][j];
   }
 }
 
