@@ -673,12 +673,15 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
     for (int j = 0; j < DX; ++j) so[j] = x[j];
   }
   const S* zrow = p.z + (liveA ? mA : 0) * (int64_t)T * R * DU;
-  double effort = 0.0;
+  // per-robot accumulators across chunks: fp32 on the throughput path (no
+  // fp64 adds, no spills in the chunk loop), fp64 on the parity path
+  using Acc = typename std::conditional<F32, float, double>::type;
+  Acc effort = Acc(0);
   float eff32 = 0.f;
   bool bad = false;
   // fp32: the robot's goal term is accumulated here (Σ ‖p−g‖/‖s−g‖ per chunk)
   float ng[3] = {0.f, 0.f, 0.f}, ginv = 0.f;
-  double goalA = 0.0;
+  Acc goalA = Acc(0);
   if (F32 && robotA) {
 #pragma unroll
     for (int c = 0; c < PD; ++c) ng[c] = -(float)p.goals[kA * PD + c];
@@ -753,7 +756,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
         float gsd = 0.f;
         const float chk = rollout_fused<KIND, NOISE == 2>(p, sm, sA, kA, rA, p.m_global0 + mA, t0, nsteps, x, zst, key, eff32,
                                               ng, ginv, gsd);
-        goalA += (double)nsteps - (double)gsd;
+        goalA += (Acc)nsteps - (Acc)gsd;
         if (!(chk == 0.f)) rollout_check<KIND>(p, kA, p.m_global0 + mA, t0, nsteps, x0, zst);
       }
     } else if (robotA) {
@@ -811,9 +814,9 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
           }
         }
       }
-      if constexpr (F32) goalA += (double)(t_end - t0) - (double)gsd;
+      if constexpr (F32) goalA += (Acc)(t_end - t0) - (Acc)gsd;
     }
-    effort += (double)eff32;  // per-chunk fp32 partial → fp64 accumulator
+    effort += (Acc)eff32;  // per-chunk fp32 partial → the cross-chunk accumulator
     eff32 = 0.f;
     __syncthreads();
 
@@ -853,8 +856,8 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
   }
 
   // ---- per-sample deterministic reduction
-  sm.red[tid] = (liveB ? gsum : 0.0) + (robotA ? goalA : 0.0);  // fp32 goal terms come from phase A
-  sm.eff[tid] = robotA ? effort : 0.0;
+  sm.red[tid] = (liveB ? gsum : 0.0) + (robotA ? (double)goalA : 0.0);  // fp32 goal terms come from phase A
+  sm.eff[tid] = robotA ? (double)effort : 0.0;
   sm.cnt[2 * tid] = liveB ? nconf : 0;
   sm.cnt[2 * tid + 1] = liveB ? nobs : 0;
   __syncthreads();
