@@ -104,40 +104,55 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
 // the same fixed order — bitwise reproducible and identical on every rank.
 constexpr int kWThreads = 1024;  // PER (rewards per thread) is 2 or 16, see the launch
 
-__device__ __forceinline__ double grid_fold(double v, double* sh, double* scratch, int slot, bool is_max) {
+// N reductions with one grid barrier: v[i] is summed, or max-ed where MAXMASK
+// has bit i.  Fixed fold order (warp tree, CTA tree, CTAs in index order).
+template <int N, int MAXMASK>
+__device__ __forceinline__ void grid_fold_n(double* v, double* sh, double* scratch, int slot) {
   namespace cg = cooperative_groups;
   const int tid = threadIdx.x;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double u = __shfl_xor_sync(0xffffffffu, v, o);
-    v = is_max ? fmax(v, u) : v + u;
-  }
-  if ((tid & 31) == 0) sh[tid >> 5] = v;
-  __syncthreads();
-  if (tid < 32) {
-    double r = sh[tid];
+  for (int i = 0; i < N; ++i) {
+    const bool mx = (MAXMASK >> i) & 1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const double u = __shfl_xor_sync(0xffffffffu, r, o);
-      r = is_max ? fmax(r, u) : r + u;
+      const double u = __shfl_xor_sync(0xffffffffu, v[i], o);
+      v[i] = mx ? fmax(v[i], u) : v[i] + u;
     }
-    if (tid == 0) scratch[slot * gridDim.x + blockIdx.x] = r;
+    if ((tid & 31) == 0) sh[i * 32 + (tid >> 5)] = v[i];
+  }
+  __syncthreads();
+  if (tid < 32) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const bool mx = (MAXMASK >> i) & 1;
+      double r = sh[i * 32 + tid];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, r, o);
+        r = mx ? fmax(r, u) : r + u;
+      }
+      if (tid == 0) scratch[(slot + i) * gridDim.x + blockIdx.x] = r;
+    }
   }
   if (gridDim.x > 1) cg::this_grid().sync();  // cooperative launch only when G > 1
   else __syncthreads();
-  double r = scratch[slot * gridDim.x];
-  for (unsigned b = 1; b < gridDim.x; ++b) {
-    const double u = scratch[slot * gridDim.x + b];
-    r = is_max ? fmax(r, u) : r + u;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const bool mx = (MAXMASK >> i) & 1;
+    double r = scratch[(slot + i) * gridDim.x];
+    for (unsigned b = 1; b < gridDim.x; ++b) {
+      const double u = scratch[(slot + i) * gridDim.x + b];
+      r = mx ? fmax(r, u) : r + u;
+    }
+    v[i] = r;
   }
   __syncthreads();
-  return r;
 }
 
 template <int NT, int kWPer>
 __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p, double* scratch) {
   static_assert(NT == kWThreads, "k_score_weights_grid block size");
-  __shared__ double sh[32];
+  __shared__ double sh[3 * 32];
   const int64_t stride = (int64_t)gridDim.x * kWThreads;
   const int64_t g0 = (int64_t)blockIdx.x * kWThreads + threadIdx.x;
   double r[kWPer];
@@ -156,13 +171,16 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
       best = fmax(best, r[q]);
     }
   }
-  const double nf = grid_fold(finite ? 0.0 : 1.0, sh, scratch, 0, false);
+  // three grid barriers in all: {non-finite count, Σr, max r}, {Σ(r−mean)²}, {Σe, Σe·s}
+  double f3[3] = {finite ? 0.0 : 1.0, s, best};
+  grid_fold_n<3, 4>(f3, sh, scratch, 0);
+  const double nf = f3[0];
   if (nf != 0.0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(p.err, 0xFFFFFFFFFFFFFFFEull);
     return;
   }
-  const double mean = grid_fold(s, sh, scratch, 1, false) / (double)p.M;
-  best = grid_fold(best, sh, scratch, 2, true);
+  const double mean = f3[1] / (double)p.M;
+  best = f3[2];
   double v = 0.0;
 #pragma unroll
   for (int q = 0; q < kWPer; ++q) {
@@ -171,7 +189,9 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
       v += d * d;
     }
   }
-  const double std_dev = sqrt(grid_fold(v, sh, scratch, 3, false) / (double)p.M);
+  double f1[1] = {v};
+  grid_fold_n<1, 0>(f1, sh, scratch, 3);
+  const double std_dev = sqrt(f1[0] / (double)p.M);
   const bool head = blockIdx.x == 0 && threadIdx.x == 0;
   if (std_dev < 1e-8) {  // degenerate batch → uniform (denoiser.cpp:74-77)
     const double u = 1.0 / (double)p.M;
@@ -196,7 +216,7 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
   const double inv = 1.0 / (std_dev * p.lambda);
   const double max_scaled = (best - mean) * inv;
   double e[kWPer];
-  double sum = 0.0;
+  double sum = 0.0, es = 0.0;
 #pragma unroll
   for (int q = 0; q < kWPer; ++q) {
     e[q] = 0.0;
@@ -204,11 +224,16 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
       r[q] = (r[q] - mean) * inv - max_scaled;  // now the shifted exponent
       e[q] = exp(r[q]);
       sum += e[q];
+      es += e[q] * r[q];
     }
   }
-  sum = grid_fold(sum, sh, scratch, 4, false);
+  double f2[2] = {sum, es};
+  grid_fold_n<2, 0>(f2, sh, scratch, 4);
+  sum = f2[0];
   const double rsum = 1.0 / sum, lsum = log(sum);
-  double h = 0.0;
+  // entropy −Σ w·log w with log w = s − log Σe: log Σe − Σe·s / Σe (terms with
+  // e = 0 contribute 0, as the w > 0 guard of denoiser.cpp:24-30)
+  const double h = lsum - f2[1] / sum;
 #pragma unroll
   for (int q = 0; q < kWPer; ++q) {
     const int64_t j = g0 + q * stride;
@@ -219,10 +244,8 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
       // is below 2^-48 of the largest cannot move an fp32 sum (even M = 2^18
       // of them add < 1e-9 of the total) and its z row is not read at all
       p.w32[j] = e[q] >= kW32Floor ? (float)w : 0.f;
-      if (w > 0.0) h -= w * (r[q] - lsum);
     }
   }
-  h = grid_fold(h, sh, scratch, 5, false);
   if (head) {
     p.trace[0] = p.step;
     p.trace[1] = best;
