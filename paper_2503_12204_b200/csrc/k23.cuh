@@ -228,9 +228,10 @@ __device__ __forceinline__ int sorted_count(const float* a, int n, float v) {
 // the strip's extent (warp union) are tested.  The slack in cull_margin and
 // in the obstacle intervals exceeds the expanded form's rounding error, so the
 // skipped tests are ones that would have come out negative anyway.
-template <int PD, int TB, int MAXW>
+template <int PD, int TB, int MAXW, bool CULL>
 __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc, int R, int n_obs, float m2u,
-                                         bool cull, float cmg, int q, int Q, float* bbp, uint32_t* cm, int* nobs) {
+                                         float cmg, int q, int Q, float* bbp, uint32_t* cm, int* nobs) {
+  constexpr bool cull = CULL;
   const float* X = sm.row(0, s, tc);
   const float* Y = sm.row(1, s, tc);
   const float* Z = PD == 3 ? sm.row(2, s, tc) : X;
@@ -356,9 +357,17 @@ __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc
 #pragma unroll
       for (int k = 0; k < TB; ++k) fb[k] = 0;
       uint32_t ma = 0;
+      // row culling: a row pair whose x lies outside tile b's extent ± margin
+      // (for every item of the warp) cannot conflict with any column
+      const float blo = cull ? bbp[(2 * b) * bbs] - cmg : -INFINITY;
+      const float bhi = cull ? bbp[(2 * b + 1) * bbs] + cmg : INFINITY;
 #pragma unroll 2
       for (int i = 0; i < TB / 2; ++i) {
         const float2 ax = *reinterpret_cast<const float2*>(X + a * TB + 2 * i);
+        if (cull) {
+          const bool far = (ax.x < blo || ax.x > bhi) && (ax.y < blo || ax.y > bhi);
+          if (__all_sync(__activemask(), far)) continue;
+        }
         const float2 ay = *reinterpret_cast<const float2*>(Y + a * TB + 2 * i);
         const float2 az = PD == 3 ? *reinterpret_cast<const float2*>(Z + a * TB + 2 * i) : make_float2(0.f, 0.f);
         const float n0 = fmaf(ax.x, ax.x, fmaf(ay.x, ay.x, az.x * az.x));
@@ -833,8 +842,12 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
           uint32_t cm[MAXW];
 #pragma unroll
           for (int w = 0; w < MAXW; ++w) cm[w] = 0;
-          item_f32<PD, TB, MAXW>(sm, sB, tc, R, p.n_obs, p.margin_sq, p.cull != 0, p.cull_margin, qB, Q,
-                                 sm.bb + (tid - qB), cm, &nobs);
+          if (p.cull)
+            item_f32<PD, TB, MAXW, true>(sm, sB, tc, R, p.n_obs, p.margin_sq, p.cull_margin, qB, Q,
+                                         sm.bb + (tid - qB), cm, &nobs);
+          else
+            item_f32<PD, TB, MAXW, false>(sm, sB, tc, R, p.n_obs, p.margin_sq, p.cull_margin, qB, Q,
+                                          sm.bb + (tid - qB), cm, &nobs);
           // merge the Q lanes' conflict flags (adjacent lanes, same item)
           for (int off = 1; off < Q; off <<= 1) {
 #pragma unroll
