@@ -308,8 +308,8 @@ int upload_problem(d4orm_cuda_ctx* ctx) {
       ord[o] = o;
     }
     std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return left[a] < left[b]; });
-    std::vector<double> ocl((size_t)2 * (O + 1), 1e30);
-    double pmax = -1e30;
+    std::vector<double> pmax(O);
+    double run = -1e30;
     for (int i = 0; i < O; ++i) {
       const int o = ord[i];
       const double lim = ctx->obs_r[o] + p.robot_radius;
@@ -320,12 +320,33 @@ int upload_problem(d4orm_cuda_ctx* ctx) {
         c2 += c * c;
       }
       obs[4 * i + 3] = c2 - (double)std::nextafter((float)(lim * lim), INFINITY);
-      pmax = std::max(pmax, right[o]);
-      ocl[2 * i] = std::nextafter((float)left[o], -INFINITY);   // rounded outward
-      ocl[2 * i + 1] = std::nextafter((float)pmax, INFINITY);
+      run = std::max(run, right[o]);
+      pmax[i] = run;
     }
+    // x-bucket table over [min left, max right]: bucket b covers
+    // [x0 + b·w, x0 + (b+1)·w); first[b] = obstacles (prefix) whose prefix-max
+    // right end lies below bucket b−1, last[b] = obstacles (prefix) whose left
+    // end lies at or before the end of bucket b+1 (one bucket of slack each side)
+    const int NB = d4k::kObsBuckets;
+    double x0 = O ? left[ord[0]] : 0.0, x1 = O ? pmax[O - 1] : 1.0;
+    if (!(x1 > x0)) x1 = x0 + 1.0;
+    const double w = (x1 - x0) / NB;
+    std::vector<float> tab(4 + 2 * NB, 0.f);
+    tab[0] = (float)x0;
+    tab[1] = (float)(1.0 / w);
+    int32_t* ti = reinterpret_cast<int32_t*>(tab.data() + 4);
+    for (int bkt = 0; bkt < NB; ++bkt) {
+      const double lo_edge = x0 + (bkt - 1) * w, hi_edge = x0 + (bkt + 2) * w;
+      int f = 0, l = 0;
+      while (f < O && pmax[f] < lo_edge) ++f;
+      while (l < O && left[ord[l]] <= hi_edge) ++l;
+      ti[2 * bkt] = f;
+      ti[2 * bkt + 1] = l;
+    }
+    CU(ctx->ocl_d.ensure(tab.size() * sizeof(float)));
+    CU(cudaMemcpyAsync(ctx->ocl_d.p, tab.data(), tab.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->s_main));
+    CU(cudaStreamSynchronize(ctx->s_main));
     obs[4 * O + 3] = 1e30;  // pad row: |p|² + 1e30 > 0
-    CU((upload_as<S>(ctx->ocl_d, ocl.data(), ocl.size(), ctx->s_main)));
   }
   CU((upload_as<S>(ctx->obs_d, obs.data(), obs.size(), ctx->s_main)));
   return D4ORM_OK;

@@ -25,6 +25,7 @@
 namespace d4k {
 
 constexpr int kFitMaxThreads = 128;
+constexpr int kObsBuckets = 64;  // x-buckets of the obstacle culling table
 constexpr int kPF = 8;  // rollout prefetch depth (time steps)
 
 template <typename S>
@@ -39,7 +40,7 @@ struct FitParams {
   const S* goals;        // [R][pd]
   const S* inv_dstart;   // [R]  fp32: 1/‖start−goal‖; fp64: ‖start−goal‖ (divide)
   const S* obs;          // [O+1][4] fp32: −2c, |c|²−(r+R_a)²↑ (row O: never-hit pad) | fp64: c, (r+R_a)²
-  const S* obs_cull;     // fp32: [O+1][2] x-interval (left end, prefix-max right end), obstacles sorted by left end
+  const S* obs_cull;     // fp32: obstacle x-bucket table (kObsBuckets, see upload_problem), obstacles sorted by left end
   S cull_margin;         // fp32: separation (m) beyond which a pair cannot be in conflict, with rounding slack
   int cull;              // fp32: rank robots by x per chunk and cull tile pairs / obstacles (≥ 3 tiles)
   int n_obs;
@@ -68,7 +69,7 @@ struct FitSmem {
   S* goal;    // fp64: [PD][Rp] goal
   S* inv;     // fp64: [2·Rp] (‖s−g‖, valid)
   S* obs;     // [O+1][4]
-  S* ocl;     // fp32: [O+1][2] obstacle x-intervals (FitParams::obs_cull)
+  S* ocl;     // fp32: obstacle x-bucket table (FitParams::obs_cull): {x0, 1/w, -, -} + [kObsBuckets][2] int
   int* key;   // fp32: [spc][Rp] chunk sort keys (x order)
   float* bb;  // fp32: [2·ntiles][nthreads] per-item tile x-extent (lo, hi)
   // the final reduction arrays alias `pos` (dead after the last chunk)
@@ -91,7 +92,7 @@ __host__ __device__ inline size_t fit_smem_bytes(int PD, int spc, int TC, int Rp
   if (sizeof(S) == 8) {
     b += (size_t)PD * Rp * sizeof(S) + 2 * (size_t)Rp * sizeof(S);
   } else {
-    b += (size_t)2 * (nobs + 1) * sizeof(float) + (size_t)spc * Rp * sizeof(int) +
+    b += (size_t)(4 + 2 * kObsBuckets) * sizeof(float) + (size_t)spc * Rp * sizeof(int) +
          (size_t)2 * (Rp / TB) * nthreads * sizeof(float);
   }
   return (b + 15) & ~size_t(15);
@@ -192,20 +193,15 @@ __device__ __forceinline__ void or_mask(uint32_t* cm, int k0, uint32_t bits) {
     if (q == w) cm[q] |= bits << sh;
 }
 
-// Number of leading entries of the ascending sequence a[0], a[2], … a[2(n−1)]
-// that are < v (STRICT = false) or <= v (STRICT = true).  Branch-free with a
-// trip count that depends on n only, so the lanes of a warp stay converged.
-template <bool STRICT>
-__device__ __forceinline__ int sorted_count(const float* a, int n, float v) {
-  int base = 0, len = n;
-  while (len > 1) {
-    const int half = len >> 1;
-    const float e = a[2 * (base + half)];
-    base = (STRICT ? e <= v : e < v) ? base + half : base;
-    len -= half;
-  }
-  const float e = a[2 * base];
-  return base + ((STRICT ? e <= v : e < v) ? 1 : 0);
+// Obstacle index range [ob, oe) that can meet the x-range [xlo, xhi]: two
+// lookups in the host-built bucket table (obstacles sorted by the left end of
+// their culling interval; each entry keeps one bucket of slack on both sides,
+// so float rounding of the bucket index cannot drop an obstacle).
+__device__ __forceinline__ void obstacle_range(const float* ocl, int n_obs, float xlo, float xhi, int* ob, int* oe) {
+  const int* tab = reinterpret_cast<const int*>(ocl + 4);
+  const float fl = (xlo - ocl[0]) * ocl[1], fh = (xhi - ocl[0]) * ocl[1];
+  *ob = !(fl >= 1.0f) ? 0 : tab[2 * min((int)fl, kObsBuckets - 1)];
+  *oe = !(fh < (float)(kObsBuckets - 1)) ? n_obs : tab[2 * max((int)fh, 0) + 1];
 }
 
 // One (sample, t) item in fp32, shared by Q threads: thread q takes the tasks
@@ -268,8 +264,10 @@ __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc
         int ob = 0, oe = n_obs;
         if (cull && n_obs > 0) {
           const unsigned am = __activemask();
-          ob = __reduce_min_sync(am, sorted_count<false>(sm.ocl + 1, n_obs, xlo));
-          oe = __reduce_max_sync(am, sorted_count<true>(sm.ocl, n_obs, xhi));
+          int b0, e0;
+          obstacle_range(sm.ocl, n_obs, xlo, xhi, &b0, &e0);
+          ob = __reduce_min_sync(am, b0);
+          oe = __reduce_max_sync(am, e0);
         }
         for (int o = ob; o < oe; o += 2) {
           const float4 b0 = *reinterpret_cast<const float4*>(sm.obs + 4 * o);      // −2c, |c|²−L²↑
@@ -643,7 +641,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
     sm.ocl = sm.bb + 2 * (Rp / TB) * nthreads;
     sm.goal = sm.inv = nullptr;
     for (int j = tid; j < 4 * (p.n_obs + 1); j += nthreads) sm.obs[j] = p.obs[j];  // (−2c, |c|²−L²↑), pad row
-    for (int j = tid; j < 2 * (p.n_obs + 1); j += nthreads) sm.ocl[j] = p.obs_cull[j];
+    for (int j = tid; j < 4 + 2 * kObsBuckets; j += nthreads) sm.ocl[j] = p.obs_cull[j];
   } else {
     sm.goal = sm.obs + 4 * (p.n_obs + 1);
     sm.inv = sm.goal + (size_t)PD * Rp;
