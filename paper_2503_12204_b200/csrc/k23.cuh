@@ -242,51 +242,67 @@ __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc
         PackedTile<PD, TB> A;
         A.load(X, Y, Z, a * TB);
         uint64_t NA[TB / 2];
-        float xlo = lo_f(A.x[0]), xhi = xlo;
+        // x-extent of each half tile (robot pairs [h·JH, (h+1)·JH)) and of the tile
+        constexpr int JH = TB / 4 > 0 ? TB / 4 : 1;
+        float hlo[2], hhi[2];
+        hlo[0] = hlo[1] = INFINITY;
+        hhi[0] = hhi[1] = -INFINITY;
 #pragma unroll
         for (int j = 0; j < TB / 2; ++j) {
           uint64_t n2 = fmul2(A.x[j], A.x[j]);
           n2 = ffma2_sq(A.y[j], n2);
           if constexpr (PD == 3) n2 = ffma2_sq(A.z[j], n2);
           NA[j] = n2;
-          xlo = fminf(xlo, fminf(lo_f(A.x[j]), hi_f(A.x[j])));
-          xhi = fmaxf(xhi, fmaxf(lo_f(A.x[j]), hi_f(A.x[j])));
+          const int h = j < JH ? 0 : 1;
+          hlo[h] = fminf(hlo[h], fminf(lo_f(A.x[j]), hi_f(A.x[j])));
+          hhi[h] = fmaxf(hhi[h], fmaxf(lo_f(A.x[j]), hi_f(A.x[j])));
         }
+        const float xlo = fminf(hlo[0], hlo[1]), xhi = fmaxf(hhi[0], hhi[1]);
         if (cull) {
           bbp[(2 * a) * bbs] = xlo;
           bbp[(2 * a + 1) * bbs] = xhi;
         }
-        // obstacle terms (reward.cpp:112-125) over the obstacles whose
-        // x-interval meets [xlo, xhi] for some item of the warp
+        // obstacle terms (reward.cpp:112-125).  Culling: per half tile, only the
+        // obstacles whose x-interval meets the half's extent (warp union).
         uint32_t olo[TB / 2], ohi[TB / 2];
 #pragma unroll
         for (int j = 0; j < TB / 2; ++j) olo[j] = ohi[j] = 0;
-        int ob = 0, oe = n_obs;
-        if (cull && n_obs > 0) {
-          const unsigned am = __activemask();
-          int b0, e0;
-          obstacle_range(sm.ocl, n_obs, xlo, xhi, &b0, &e0);
-          ob = __reduce_min_sync(am, b0);
-          oe = __reduce_max_sync(am, e0);
-        }
-        for (int o = ob; o < oe; o += 2) {
-          const float4 b0 = *reinterpret_cast<const float4*>(sm.obs + 4 * o);      // −2c, |c|²−L²↑
-          const float4 b1 = *reinterpret_cast<const float4*>(sm.obs + 4 * o + 4);  // row O: never hits
+        auto obstacle_block = [&](int ob, int oe, auto j0_tag, auto jn_tag) {
+          constexpr int J0 = decltype(j0_tag)::value, JN = decltype(jn_tag)::value;
+          for (int o = ob; o < oe; o += 2) {
+            const float4 b0 = *reinterpret_cast<const float4*>(sm.obs + 4 * o);      // −2c, |c|²−L²↑
+            const float4 b1 = *reinterpret_cast<const float4*>(sm.obs + 4 * o + 4);  // row O: never hits
 #pragma unroll
-          for (int j = 0; j < TB / 2; ++j) {
-            uint64_t t0 = fadd2_b(b0.w, NA[j]);
-            uint64_t t1 = fadd2_b(b1.w, NA[j]);
-            t0 = ffma2(A.x[j], pack2(b0.x, b0.x), t0);
-            t1 = ffma2(A.x[j], pack2(b1.x, b1.x), t1);
-            t0 = ffma2(A.y[j], pack2(b0.y, b0.y), t0);
-            t1 = ffma2(A.y[j], pack2(b1.y, b1.y), t1);
-            if constexpr (PD == 3) {
-              t0 = ffma2(A.z[j], pack2(b0.z, b0.z), t0);
-              t1 = ffma2(A.z[j], pack2(b1.z, b1.z), t1);
+            for (int j = J0; j < JN; ++j) {
+              uint64_t t0 = fadd2_b(b0.w, NA[j]);
+              uint64_t t1 = fadd2_b(b1.w, NA[j]);
+              t0 = ffma2(A.x[j], pack2(b0.x, b0.x), t0);
+              t1 = ffma2(A.x[j], pack2(b1.x, b1.x), t1);
+              t0 = ffma2(A.y[j], pack2(b0.y, b0.y), t0);
+              t1 = ffma2(A.y[j], pack2(b1.y, b1.y), t1);
+              if constexpr (PD == 3) {
+                t0 = ffma2(A.z[j], pack2(b0.z, b0.z), t0);
+                t1 = ffma2(A.z[j], pack2(b1.z, b1.z), t1);
+              }
+              olo[j] |= lo32(t0) | lo32(t1);
+              ohi[j] |= hi32(t0) | hi32(t1);
             }
-            olo[j] |= lo32(t0) | lo32(t1);
-            ohi[j] |= hi32(t0) | hi32(t1);
           }
+        };
+        if constexpr (CULL) {
+          if (n_obs > 0) {
+            const unsigned am = __activemask();
+            int b0, e0, b1, e1;
+            obstacle_range(sm.ocl, n_obs, hlo[0], hhi[0], &b0, &e0);
+            obstacle_range(sm.ocl, n_obs, hlo[1], hhi[1], &b1, &e1);
+            obstacle_block(__reduce_min_sync(am, b0), __reduce_max_sync(am, e0), std::integral_constant<int, 0>{},
+                           std::integral_constant<int, JH>{});
+            if constexpr (TB / 2 > JH)
+              obstacle_block(__reduce_min_sync(am, b1), __reduce_max_sync(am, e1), std::integral_constant<int, JH>{},
+                             std::integral_constant<int, TB / 2>{});
+          }
+        } else {
+          obstacle_block(0, n_obs, std::integral_constant<int, 0>{}, std::integral_constant<int, TB / 2>{});
         }
         uint32_t om = 0;
 #pragma unroll
