@@ -26,7 +26,10 @@ namespace d4k {
 
 constexpr int kFitMaxThreads = 128;
 constexpr int kObsBuckets = 64;  // x-buckets of the obstacle culling table
-constexpr int kPF = 8;  // rollout prefetch depth (time steps)
+#ifndef D4K_KPF
+#define D4K_KPF 8
+#endif
+constexpr int kPF = D4K_KPF;  // rollout block depth (time steps): Philox draws in flight per thread
 
 template <typename S>
 struct FitParams {
