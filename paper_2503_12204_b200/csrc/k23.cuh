@@ -246,21 +246,34 @@ __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc
         A.load(X, Y, Z, a * TB);
         uint64_t NA[TB / 2];
         // x-extent of each half tile (robot pairs [h·JH, (h+1)·JH)) and of the tile
-        constexpr int JH = TB / 4 > 0 ? TB / 4 : 1;
-        float hlo[2], hhi[2];
-        hlo[0] = hlo[1] = INFINITY;
-        hhi[0] = hhi[1] = -INFINITY;
+#ifndef D4K_OBS_PARTS
+#define D4K_OBS_PARTS 2
+#endif
+        // obstacle culling parts per tile: NPART groups of JH robot pairs
+        constexpr int NPART = (TB / 2) >= D4K_OBS_PARTS ? D4K_OBS_PARTS : (TB / 2);
+        constexpr int JH = (TB / 2) / NPART;
+        float hlo[NPART], hhi[NPART];
+#pragma unroll
+        for (int h = 0; h < NPART; ++h) {
+          hlo[h] = INFINITY;
+          hhi[h] = -INFINITY;
+        }
 #pragma unroll
         for (int j = 0; j < TB / 2; ++j) {
           uint64_t n2 = fmul2(A.x[j], A.x[j]);
           n2 = ffma2_sq(A.y[j], n2);
           if constexpr (PD == 3) n2 = ffma2_sq(A.z[j], n2);
           NA[j] = n2;
-          const int h = j < JH ? 0 : 1;
+          const int h = j / JH;
           hlo[h] = fminf(hlo[h], fminf(lo_f(A.x[j]), hi_f(A.x[j])));
           hhi[h] = fmaxf(hhi[h], fmaxf(lo_f(A.x[j]), hi_f(A.x[j])));
         }
-        const float xlo = fminf(hlo[0], hlo[1]), xhi = fmaxf(hhi[0], hhi[1]);
+        float xlo = hlo[0], xhi = hhi[0];
+#pragma unroll
+        for (int h = 1; h < NPART; ++h) {
+          xlo = fminf(xlo, hlo[h]);
+          xhi = fmaxf(xhi, hhi[h]);
+        }
         if (cull) {
           bbp[(2 * a) * bbs] = xlo;
           bbp[(2 * a + 1) * bbs] = xhi;
@@ -295,14 +308,20 @@ __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc
         if constexpr (CULL) {
           if (n_obs > 0) {
             const unsigned am = __activemask();
-            int b0, e0, b1, e1;
-            obstacle_range(sm.ocl, n_obs, hlo[0], hhi[0], &b0, &e0);
-            obstacle_range(sm.ocl, n_obs, hlo[1], hhi[1], &b1, &e1);
-            obstacle_block(__reduce_min_sync(am, b0), __reduce_max_sync(am, e0), std::integral_constant<int, 0>{},
-                           std::integral_constant<int, JH>{});
-            if constexpr (TB / 2 > JH)
-              obstacle_block(__reduce_min_sync(am, b1), __reduce_max_sync(am, e1), std::integral_constant<int, JH>{},
-                             std::integral_constant<int, TB / 2>{});
+            int ob[NPART], oe[NPART];
+#pragma unroll
+            for (int h = 0; h < NPART; ++h) {
+              obstacle_range(sm.ocl, n_obs, hlo[h], hhi[h], &ob[h], &oe[h]);
+              ob[h] = __reduce_min_sync(am, ob[h]);
+              oe[h] = __reduce_max_sync(am, oe[h]);
+            }
+            obstacle_block(ob[0], oe[0], std::integral_constant<int, 0>{}, std::integral_constant<int, JH>{});
+            if constexpr (NPART > 1)
+              obstacle_block(ob[1], oe[1], std::integral_constant<int, JH>{}, std::integral_constant<int, 2 * JH>{});
+            if constexpr (NPART > 2)
+              obstacle_block(ob[2], oe[2], std::integral_constant<int, 2 * JH>{}, std::integral_constant<int, 3 * JH>{});
+            if constexpr (NPART > 3)
+              obstacle_block(ob[3], oe[3], std::integral_constant<int, 3 * JH>{}, std::integral_constant<int, 4 * JH>{});
           }
         } else {
           obstacle_block(0, n_obs, std::integral_constant<int, 0>{}, std::integral_constant<int, TB / 2>{});
