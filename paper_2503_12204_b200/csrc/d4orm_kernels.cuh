@@ -377,6 +377,35 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
   const int64_t c = blockIdx.y;
   const int64_t mb = c * (kPartSub * kPartLanes) + (int64_t)sr * kPartLanes;
   const int n = e0 < elems ? (elems - e0 < 4 ? (int)(elems - e0) : 4) : 0;
+  // large E (fp32): the CTA first compacts its chunk's non-zero weights (in
+  // ascending sample order, so the sum is the same) into shared memory; the
+  // walk then issues only the z loads that count, back to back
+  __shared__ int s_idx[SUB == 1 ? kPartLanes : 1];
+  __shared__ float s_w[SUB == 1 ? kPartLanes : 1];
+  __shared__ int s_cnt[SUB == 1 ? kPartLanes / 32 + 1 : 1];
+  if constexpr (SUB == 1 && std::is_same<S, float>::value) {
+    static_assert(PartShape<SUB>::THREADS == kPartLanes, "one weight per thread");
+    const int64_t m = mb + threadIdx.x;
+    const float wm = m < M ? (float)w[m] : 0.f;
+    const bool nz = wm != 0.f;
+    const unsigned bal = __ballot_sync(0xffffffffu, nz);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) s_cnt[wid] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < kPartLanes / 32; ++i) {
+      off += i < wid ? s_cnt[i] : 0;
+      tot += s_cnt[i];
+    }
+    if (nz) {
+      const int pos = off + __popc(bal & ((1u << lane) - 1u));
+      s_idx[pos] = threadIdx.x;
+      s_w[pos] = wm;
+    }
+    if (threadIdx.x == 0) s_cnt[kPartLanes / 32] = tot;
+    __syncthreads();
+  }
   S acc[4] = {S(0), S(0), S(0), S(0)};
   if (n > 0) {
     // (constant-index loops with predication keep these in registers)
@@ -403,15 +432,14 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
     if constexpr (std::is_same<S, float>::value) vec = n == 4 && (elems & 3) == 0;
     if (vec) {
       if constexpr (std::is_same<S, float>::value && SUB == 1) {
-        // large E: one streaming walk per thread, pointer-stepped rows
+        // large E: one streaming walk per thread over the compacted rows
         const float4* zp = reinterpret_cast<const float4*>(z + mb * elems + e0);
         const int64_t stride = elems / 4;
-        const int64_t me = mb + kPartLanes < M ? mb + kPartLanes : M;
+        const int nnz = s_cnt[kPartLanes / 32];
 #pragma unroll 4
-        for (int64_t m = mb; m < me; ++m, zp += stride) {
-          const float wm = (float)__ldg(w + m);
-          if (wm == 0.f) continue;  // uniform across the CTA: zero-weight rows are not read
-          const float4 v = __ldcs(zp);
+        for (int q = 0; q < nnz; ++q) {
+          const float wm = s_w[q];
+          const float4 v = __ldcs(zp + (int64_t)s_idx[q] * stride);
           if constexpr (DEV) {
             acc[0] += term(wm, v.x, 0);
             acc[1] += term(wm, v.y, 1);
