@@ -558,23 +558,23 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree(const S* __restrict__ p
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= elems) return;
   S stack[40];
-  int64_t cnt = 0;
   int top = 0;
-  for (int64_t c0 = 0; c0 < nchunks; c0 += 8) {
-    S v8[8];  // eight loads in flight, then merged in order
-    const int nb = nchunks - c0 < 8 ? (int)(nchunks - c0) : 8;
+  // whole blocks of 8 chunks: their perfect 8-leaf subtree in registers, then
+  // the binary counter over blocks (the same tree as leaf by leaf: every block
+  // starts at a multiple of 8, where the leaf counter's low 3 bits are 0)
+  const int64_t nblk = nchunks / 8;
+  for (int64_t b = 0; b < nblk; ++b) {
+    S v8[8];  // eight loads in flight
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < nb) v8[j] = partial[(c0 + j) * elems + e];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j < nb) {
-        S v = v8[j];
-        for (int64_t k = cnt; k & 1; k >>= 1) v = xadd(stack[--top], v);  // merge equal-size subtrees
-        stack[top++] = v;
-        ++cnt;
-      }
-    }
+    for (int j = 0; j < 8; ++j) v8[j] = partial[(8 * b + j) * elems + e];
+    S v = xadd(xadd(xadd(v8[0], v8[1]), xadd(v8[2], v8[3])), xadd(xadd(v8[4], v8[5]), xadd(v8[6], v8[7])));
+    for (int64_t k = b; k & 1; k >>= 1) v = xadd(stack[--top], v);  // merge equal-size subtrees
+    stack[top++] = v;
+  }
+  for (int64_t cnt = 8 * nblk; cnt < nchunks; ++cnt) {  // leaves past the last whole block
+    S v = partial[cnt * elems + e];
+    for (int64_t k = cnt; k & 1; k >>= 1) v = xadd(stack[--top], v);
+    stack[top++] = v;
   }
   S total = stack[--top];
   while (top > 0) total = xadd(stack[--top], total);
