@@ -326,9 +326,12 @@ __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc
         } else {
           obstacle_block(0, n_obs, std::integral_constant<int, 0>{}, std::integral_constant<int, TB / 2>{});
         }
-        uint32_t om = 0;
+        uint32_t om = 0;  // bit 2j / 2j+1: robot pair j's obstacle hits (one funnel shift per bit)
 #pragma unroll
-        for (int j = 0; j < TB / 2; ++j) om |= ((olo[j] >> 31) | ((ohi[j] >> 31) << 1)) << (2 * j);
+        for (int j = TB / 2 - 1; j >= 0; --j) {
+          om = __funnelshift_l(ohi[j], om, 1);
+          om = __funnelshift_l(olo[j], om, 1);
+        }
         const int kv = R - a * TB;  // valid robots in this tile
         *nobs += __popc(kv >= 32 ? om : (om & ((1u << (kv > 0 ? kv : 0)) - 1u)));
         // pairs inside tile a, from the tile already in registers: columns as
@@ -373,14 +376,11 @@ __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc
   }
   const int n_off = ntiles * (ntiles - 1) / 2;
   if (cull && Q > 1 && n_off > 0) __syncwarp(__activemask());  // tile extents written by the item's other lanes
-  for (int k = q; k < n_off; k += Q) {
-    // ---------------- off-diagonal task k → (a, b), a < b
-    int a = 0, rem = k;
-    while (rem >= ntiles - 1 - a) {
-      rem -= ntiles - 1 - a;
-      ++a;
-    }
-    const int b = a + 1 + rem;
+  int k = 0;
+  for (int a = 0; a < ntiles - 1; ++a)
+  for (int b = a + 1; b < ntiles; ++b, ++k) {
+    // ---------------- off-diagonal task k = (a, b), a < b; this lane's when k ≡ q (mod Q)
+    if (Q > 1 && k % Q != q) continue;
     if (cull) {
       const bool apart = bbp[(2 * a + 1) * bbs] + cmg < bbp[(2 * b) * bbs] ||
                          bbp[(2 * b + 1) * bbs] + cmg < bbp[(2 * a) * bbs];
