@@ -487,8 +487,10 @@ __device__ __forceinline__ double item_f64(const FitSmem<double>& sm, int s, int
 // accumulates ‖p − g‖ / ‖start − g‖ (ng = −g, ginv = 1/‖start − g‖).
 template <int PD>
 __device__ __forceinline__ void goal_acc(const float* x, const float* ng, float ginv, float& gsd) {
-  const float dx = x[0] + ng[0], dy = x[1] + ng[1];
-  float d2 = fmaf(dy, dy, dx * dx);
+  // (x, y) − goal and its squares as packed pairs: FADD2 + FMUL2 + FADD
+  const uint64_t dxy = fadd2(pack2(x[0], x[1]), pack2(ng[0], ng[1]));
+  const uint64_t sq = fmul2(dxy, dxy);
+  float d2 = lo_f(sq) + hi_f(sq);
   if constexpr (PD == 3) {
     const float dz = x[2] + ng[2];
     d2 = fmaf(dz, dz, d2);
