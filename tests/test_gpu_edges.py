@@ -1,0 +1,80 @@
+"""Edge shapes for the fused rollout+fitness kernel: a single robot, two
+robots, a long horizon cut into ragged chunks, horizons shorter than a chunk,
+batches that leave a CTA partly empty, and a 100-robot team (Rp 112: items
+shared by two threads, 8 flag words, culling across 7 tiles) — fp64 against the
+oracle to 1e-12, fp32 to the fp32 band, and culling on == off."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2503_12204_b200 as d4
+from paper_2503_12204_b200 import scenarios as S
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(R, T, seed, kind=S.HOLO2D_VEL, side=10.0, n_obs=0, radius=0.2):
+    rng = np.random.default_rng(seed)
+    dx, du, pd = S.DIMS[kind]
+    st = np.zeros((R, dx))
+    st[:, :pd] = rng.uniform(-side / 2, side / 2, (R, pd))
+    go = rng.uniform(-side / 2, side / 2, (R, pd))
+    kw = {}
+    if n_obs:
+        kw = dict(obs_centers=rng.uniform(-side / 2, side / 2, (n_obs, pd)), obs_radii=rng.uniform(0.2, 1.0, n_obs))
+    return S.Problem(kind, starts=st, goals=go, horizon=T, lower=[-1] * du, upper=[1] * du, robot_radius=radius, **kw)
+
+
+SHAPES = {
+    "R1_T3_M7": (1, 3, 7, S.HOLO2D_VEL, 0),
+    "R2_T1_M2": (2, 1, 2, S.HOLO2D_VEL, 1),
+    "R5_T70_M33": (5, 70, 33, S.UNICYCLE, 2),
+    "R17_T9_M5": (17, 9, 5, S.HOLO3D_VEL, 3),
+    "R100_T20_M6": (100, 20, 6, S.HOLO2D_VEL, 5),
+    "R100_T70_M3_diffdrive": (100, 70, 3, S.DIFFDRIVE, 0),
+}
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    g = d4.GpuDenoiser()
+    yield g
+    g.close()
+
+
+@pytest.mark.parametrize("name", list(SHAPES))
+def test_edge_shapes_match_oracle(gpu, oracle, name):
+    from test_gpu_parity import controls_for, explain_flips, oracle_rollout_batch
+    R, T, M, kind, n_obs = SHAPES[name]
+    side = 6.0 if R > 50 else 10.0
+    p = _problem(R, T, sum(map(ord, name)), kind=kind, side=side, n_obs=n_obs)  # stable seed
+    u = controls_for(p, M, 3, scale=1.0)
+    ref = oracle_rollout_batch(oracle, p, u)
+    gpu.set_options(d4.PREC_F64, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    st, ct, rw, cnt = gpu.rollout_fitness(u)
+    for m, (rs, rc, rr, nc, no) in enumerate(ref):
+        np.testing.assert_allclose(st[m], rs, rtol=1e-12, atol=1e-12)
+        assert (cnt[m, 0], cnt[m, 1]) == (nc, no), (m, cnt[m], nc, no)
+        assert abs(rw[m] - rr) <= 1e-12, (m, rw[m], rr)
+    gpu.set_options(d4.PREC_F32, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    res = []
+    for cull in ("1", "0"):
+        os.environ["D4ORM_CULL"] = cull
+        try:
+            gpu.set_problem(p)
+            res.append(gpu.rollout_fitness(u))
+        finally:
+            os.environ.pop("D4ORM_CULL", None)
+    (st1, _, rw1, cnt1), (st0, _, rw0, cnt0) = res
+    np.testing.assert_array_equal(cnt1, cnt0)
+    np.testing.assert_array_equal(rw1, rw0)
+    unit = max(p.w_t, p.obstacle_weight) / (p.robots * p.horizon)
+    for m, (rs, rc, rr, nc, no) in enumerate(ref):
+        np.testing.assert_allclose(st1[m], rs, atol=5e-5, rtol=1e-5)
+        flips = abs(cnt1[m, 0] - nc) + abs(cnt1[m, 1] - no)
+        if flips:
+            assert explain_flips(oracle, p, st1[m], cnt1[m, 0], cnt1[m, 1]), (m, cnt1[m], nc, no)
+        assert abs(rw1[m] - rr) <= 3e-5 + flips * unit, (m, rw1[m], rr, flips)
