@@ -578,10 +578,12 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
         eff32 = fmaf(u[d], u[d], eff32);
       }
       rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
-      float s = x[0];
+      if constexpr (DX != PD) {  // state beyond the position: its own NaN/inf watch
+        float s = x[0];
 #pragma unroll
-      for (int q = 1; q < DX; ++q) s += x[q];
-      chk = fmaf(s, 0.f, chk);
+        for (int q = 1; q < DX; ++q) s += x[q];
+        chk = fmaf(s, 0.f, chk);
+      }
       goal_acc<PD>(x, ng, ginv, gsd);
       px[j * RS] = x[0];
       py[j * RS] = x[1];
@@ -622,6 +624,9 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
     py += kPF * RS;
     pz += kPF * RS;
   }
+  // state = position (velocity-input kinds): a NaN/inf state reaches the goal
+  // distance, so the goal sum (ginv > 0: start ≠ goal is validated) carries it
+  if constexpr (ModelDims<KIND>::DX == PD) return gsd * 0.f;
   return chk;
 }
 
