@@ -78,3 +78,24 @@ def test_edge_shapes_match_oracle(gpu, oracle, name):
         if flips:
             assert explain_flips(oracle, p, st1[m], cnt1[m, 0], cnt1[m, 1]), (m, cnt1[m], nc, no)
         assert abs(rw1[m] - rr) <= 3e-5 + flips * unit, (m, rw1[m], rr, flips)
+
+
+@pytest.mark.parametrize("kind", [S.HOLO2D_VEL, S.UNICYCLE])
+def test_fused_path_reports_nonfinite_state(gpu, kind):
+    """Throughput path (fp32, Philox drawn in the rollout): an infinite base
+    control with unbounded controls makes the state non-finite; the chunk's
+    watch (the goal sum for velocity kinds, the state sum otherwise) triggers
+    the exact replay, which reports the first failing robot and step like
+    dynamics.cpp:81-84 (sample 0 is the lowest failing index)."""
+    dx, du, pd = S.DIMS[kind]
+    R, T = 3, 20
+    st = np.zeros((R, dx))
+    st[:, :pd] = np.array([[0, 0], [2, 0], [0, 2]], dtype=float)[:, :pd]
+    p = S.Problem(kind, starts=st, goals=np.array([[1, 1], [3, 3], [-2, 2]], dtype=float)[:, :pd], horizon=T,
+                  lower=[-np.inf] * du, upper=[np.inf] * du)
+    base = np.zeros((T, R, du))
+    base[7, 2, 0] = np.inf
+    gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX)
+    gpu.set_problem(p)
+    with pytest.raises(d4.D4ormError, match="run_denoising: sample 0 at step 5: rollout: non-finite state for robot 2 at step 8"):
+        gpu.run_denoising(base, d4.DenoiserConfig(steps=5, batch=64, seed=1))
