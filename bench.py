@@ -276,7 +276,13 @@ def main():
     if tf.exists():
         traffic = json.loads(tf.read_text()).get(rc.name)
     E = p.elems
-    k5_bytes = Ml * E * 4 + Ml * 4 + (Ml + 255) // 256 * E * 4 + E * 4
+    # K5a: algorithmic bytes (every sample's z row) and the bytes it actually
+    # moves — z rows of samples with a non-zero fp32 weight only (K4 zeroes
+    # weights below 2^-48 of the largest), + weights + partials
+    parts = (Ml + 255) // 256 * E * 4
+    k5_alg = Ml * E * 4 + Ml * 4 + parts
+    k5_nz = float(kms[5])
+    k5_read = int(k5_nz * E * 4) + Ml * 4 + parts
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -287,8 +293,13 @@ def main():
                      "peak_source": "measured live: d4orm_cuda_fp32_peak (FFMA2 over all SMs); MEASURED_PEAKS.json has no FP32 figure"},
         "kernel_ms": {"K1_philox": kms[0], "K2K3_rollout_fitness": kms[1], "K4_weights": kms[2],
                       "K5_wmean_partial": kms[3], "K5_tree_update": kms[4]},
-        "k5_hbm": {"achieved_gbs": k5_bytes / (kms[3] * 1e-3) / 1e9 if kms[3] > 0 else None,
-                   "peak_gbs": _hbm_peak(), "bytes_per_launch": k5_bytes},
+        "k5_hbm": {"kernel": "k_wmean_partial (K5a)", "bound": "hbm",
+                   "achieved_gbs": k5_read / (kms[3] * 1e-3) / 1e9 if kms[3] > 0 else None,
+                   "peak_gbs": _hbm_peak(), "frac": (k5_read / (kms[3] * 1e-3) / 1e9) / _hbm_peak() if kms[3] > 0 else None,
+                   "bytes_moved_per_launch": k5_read, "samples_with_weight": k5_nz, "samples": Ml,
+                   "algorithmic_bytes_per_launch": k5_alg,
+                   "note": "bytes moved = z rows of samples with non-zero fp32 weight + weights + chunk partials; "
+                           "rows of zero-weight samples are skipped, so the algorithmic all-rows count over-states the rate"},
         "gpu_launches": args.steps * g.launches_per_step(),
         "clocks": clk.summary(),
     }

@@ -210,8 +210,10 @@ int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_
 /* Prepare a device-resident run (base uploaded once), then time `steps`
  * denoising steps after `warmup` untimed ones, with CUDA events on the
  * context's stream.  Fills ms_total and, if non-NULL, per-kernel average
- * milliseconds kernel_ms[5] = {K1 noise, K2+K3 rollout+fitness, K4 weights,
- * K5 partial, K5 tree} (measured in a separate instrumented pass). */
+ * milliseconds kernel_ms[6] = {K1 noise, K2+K3 rollout+fitness, K4 weights,
+ * K5 partial, K5 tree} (measured in a separate instrumented pass), and in
+ * kernel_ms[5] the mean number of this rank's samples with a non-zero weight
+ * in that pass (the z rows K5's partial pass reads; zero weights are skipped). */
 int d4orm_cuda_bench_steps(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* config,
                            int warmup, int steps, double* ms_total, double* kernel_ms);
 /* Number of this library's kernel launches per denoising step (graph nodes). */

@@ -1659,10 +1659,12 @@ int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config
   if (kernel_ms) {
     // Instrumented pass: eager launches with CUDA events between the kernels
     // on the context's stream.
-    double acc[5] = {0, 0, 0, 0, 0};
+    double acc[6] = {0, 0, 0, 0, 0, 0};
     cudaEvent_t e0;
     CU(cudaEventCreate(&e0));
     const int reps = steps < 1 ? 1 : steps;
+    std::vector<S> wl((size_t)rs.Ml);
+    const S* wdev = std::is_same<S, double>::value ? (const S*)ctx->w64.p : (const S*)ctx->w32.p;
     for (int j = 0; j < reps; ++j) {
       const int i = rs.N - ((warmup + steps + j) % rs.N);
       CU(cudaEventRecord(e0, ctx->s_main));
@@ -1675,9 +1677,14 @@ int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config
       CU(cudaEventElapsedTime(&t[3], ctx->ev_k[2], ctx->ev_k[3]));
       CU(cudaEventElapsedTime(&t[4], ctx->ev_k[3], ctx->ev_k[4]));
       for (int k = 0; k < 5; ++k) acc[k] += t[k];
+      // samples whose weight K5a reads a z row for (zero weights are skipped)
+      CU(cudaMemcpy(wl.data(), wdev + rs.m0, sizeof(S) * (size_t)rs.Ml, cudaMemcpyDeviceToHost));
+      int64_t nz = 0;
+      for (const S w : wl) nz += (w != S(0));
+      acc[5] += (double)nz;
     }
     cudaEventDestroy(e0);
-    for (int k = 0; k < 5; ++k) kernel_ms[k] = acc[k] / reps;
+    for (int k = 0; k < 6; ++k) kernel_ms[k] = acc[k] / reps;
   }
   return D4ORM_OK;
 }

@@ -183,7 +183,7 @@ class GpuDenoiser:
     def bench_steps(self, base, cfg: DenoiserConfig, warmup: int, steps: int, kernels: bool = True):
         base = np.ascontiguousarray(base, dtype=np.float64).reshape(self._shape())
         ms = C.c_double()
-        kms = np.zeros(5)
+        kms = np.zeros(6)
         c = cfg.c()
         self._check(self._L.d4orm_cuda_bench_steps(self._h, dptr(base), C.byref(c), warmup, steps, C.byref(ms),
                                                   dptr(kms) if kernels else None))

@@ -9,6 +9,6 @@ p = rc.problem
 g = d4.GpuDenoiser(p)
 g.set_options(graphs=False)
 cfg = d4.DenoiserConfig(steps=rc.steps, batch=rc.samples, seed=0)
-g.bench_steps(np.zeros((p.horizon, p.robots, p.du)), cfg, 0, 1, kernels=False)
+g.bench_steps(np.zeros((p.horizon, p.robots, p.du)), cfg, 2, 1, kernels=False)  # 3 launches: profile with -s 2 -c 1
 g.close()
 print("done")
