@@ -176,7 +176,8 @@ __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
   const float f = __uint_as_float((b >> 9) | 0x3f800000u);     // 1 + k·2^-23
   float s, c;
   __sincosf(fmaf(f, 6.28318530717958647692f, -6.28318530717958647692f), &s, &c);  // 2π·k·2^-23
-  return make_float2(r * c, r * s);
+  const uint64_t z = fmul2(pack2(r, r), pack2(c, s));  // r·cos, r·sin in one FMUL2
+  return make_float2(lo_f(z), hi_f(z));
 }
 
 __device__ __forceinline__ float4 philox_normals(uint2 key, uint64_t m, uint32_t k, uint32_t g) {

@@ -565,19 +565,38 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
     }
   }
 #endif
+  // two-control kinds: the control pair, its effort and (velocity input) the
+  // position update as packed FFMA2 — the same per-lane fma as the scalar form
+  constexpr bool PK = DU == 2 && !SDV;
+  uint64_t eff2 = 0;
 #pragma unroll
   for (int j = 0; j < kPF; ++j) {
     if (FULL || j < nb) {
       float u[DU];
-#pragma unroll
-      for (int d = 0; d < DU; ++d) {
+      if constexpr (PK) {
         // base + (mean_scale·var + std·z), clamped; FMNMX equals cwiseMax/Min
         // here because NaN inputs are rejected on the host before launch
-        const float sdj = SDV ? sq[SDV ? j : 0][d] : p.sd;
-        u[d] = fminf(fmaxf(fmaf(sdj, nz[j * DU + d], bq[j][d]), p.lower[d]), p.upper[d]);
-        eff32 = fmaf(u[d], u[d], eff32);
+        const uint64_t v = ffma2(pack2(p.sd, p.sd), pack2(nz[2 * j], nz[2 * j + 1]), pack2(bq[j][0], bq[j][1]));
+        u[0] = fminf(fmaxf(lo_f(v), p.lower[0]), p.upper[0]);
+        u[1] = fminf(fmaxf(hi_f(v), p.lower[1]), p.upper[1]);
+        const uint64_t uc = pack2(u[0], u[1]);
+        eff2 = ffma2(uc, uc, eff2);
+        if constexpr (KIND == HOLO2D_VEL) {  // rk4: x + dt·u (fp32 velocity-input closed form)
+          const uint64_t xn = ffma2(pack2(p.dt, p.dt), uc, pack2(x[0], x[1]));
+          x[0] = lo_f(xn);
+          x[1] = hi_f(xn);
+        } else {
+          rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
+        }
+      } else {
+#pragma unroll
+        for (int d = 0; d < DU; ++d) {
+          const float sdj = SDV ? sq[SDV ? j : 0][d] : p.sd;
+          u[d] = fminf(fmaxf(fmaf(sdj, nz[j * DU + d], bq[j][d]), p.lower[d]), p.upper[d]);
+          eff32 = fmaf(u[d], u[d], eff32);
+        }
+        rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
       }
-      rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
       if constexpr (DX != PD) {  // state beyond the position: its own NaN/inf watch
         float s = x[0];
 #pragma unroll
@@ -590,6 +609,7 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
       if constexpr (PD == 3) pz[j * RS] = x[2];
     }
   }
+  if constexpr (PK) eff32 += lo_f(eff2) + hi_f(eff2);
 }
 
 template <int KIND, bool SDV>
