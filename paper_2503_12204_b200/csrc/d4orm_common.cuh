@@ -61,6 +61,16 @@ __device__ __forceinline__ void deriv(const S* x, const S* u, S* f) {
   }
 }
 
+// fp32 throughput path: sin/cos with a two-constant Cody-Waite reduction to
+// [−π, π] and the MUFU approximations there (abs. error ≈ 2^-21 for any
+// heading the rollouts reach).  NaN/inf headings stay non-finite.
+__device__ __forceinline__ void fast_sincos(float a, float* s, float* c) {
+  const float q = rintf(a * 0.159154943091895335769f);  // a / 2π
+  float r = fmaf(q, -6.28318548202514648438f, a);       // float(2π) = 2π + 1.7484555e-7
+  r = fmaf(q, 1.74845553e-7f, r);
+  __sincosf(r, s, c);
+}
+
 // detail::rk4_with (dynamics.hpp:123-130), element order as Eigen evaluates it:
 //   k2 = f(x + (0.5dt)k1), k3 = f(x + (0.5dt)k2), k4 = f(x + dt·k3)
 //   x' = x + (dt/6)·(((k1 + 2k2) + 2k3) + k4)
@@ -73,6 +83,27 @@ __device__ __forceinline__ void rk4(S* x, const S* u, S dt, S half_dt, S dt6) {
     // the staged expression the fp64 path evaluates).
 #pragma unroll
     for (int j = 0; j < DX; ++j) x[j] = fmaf(dt, u[j], x[j]);
+    return;
+  }
+  if constexpr (std::is_same<S, float>::value && (KIND == UNICYCLE || KIND == DIFFDRIVE)) {
+    // fp32 throughput path, heading kinds: the derivative depends on (θ, v)
+    // only, and the θ/v components of x + (dt/2)·k1 and x + (dt/2)·k2 are the
+    // same numbers (both derivatives are the held controls), so k3 = k2:
+    // three distinct headings θ, θ + (dt/2)ω, θ + dt·ω, one fast sincos each.
+    constexpr bool UNI = KIND == UNICYCLE;
+    const float w = UNI ? u[1] : u[0];                 // heading rate ω
+    const float v1 = UNI ? u[0] : x[3];                // speed at stages 1, 2 (= 3), 4
+    const float v2 = UNI ? u[0] : x[3] + half_dt * u[1];
+    const float v4 = UNI ? u[0] : x[3] + dt * u[1];
+    float s1, c1, s2, c2, s4, c4;
+    fast_sincos(x[2], &s1, &c1);
+    fast_sincos(x[2] + half_dt * w, &s2, &c2);
+    fast_sincos(x[2] + dt * w, &s4, &c4);
+    const float kx2 = v2 * c2, ky2 = v2 * s2;
+    x[0] = x[0] + dt6 * (((v1 * c1 + 2.f * kx2) + 2.f * kx2) + v4 * c4);
+    x[1] = x[1] + dt6 * (((v1 * s1 + 2.f * ky2) + 2.f * ky2) + v4 * s4);
+    x[2] = x[2] + dt6 * (((w + 2.f * w) + 2.f * w) + w);
+    if constexpr (!UNI) x[3] = x[3] + dt6 * (((u[1] + 2.f * u[1]) + 2.f * u[1]) + u[1]);
     return;
   }
   S k1[DX], k2[DX], k3[DX], k4[DX], tmp[DX];

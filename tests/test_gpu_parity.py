@@ -375,3 +375,22 @@ def test_device_solve_philox_stops_on_success(gpu):
     assert check_success(p, r1.best_states)[0] == r1.success
     best_it = rewards.index(r1.best_reward)
     assert objective(p, r1.best_states) == r1.per_iteration[best_it][1]
+
+
+@pytest.mark.parametrize("kind", ["C3", "diffdrive"])
+def test_heading_kinds_f32_full_horizon(gpu, oracle, kind):
+    """fp32 heading kinds (unicycle, diff-drive) over a full 128-step horizon
+    with headings wound far from [−π, π]: the fast reduced sin/cos and the
+    k2 = k3 stage sharing keep positions within 2e-5 m of the fp64 oracle."""
+    p = (S.baseline_config(3).problem if kind == "C3"
+         else S.antipodal_circle(5, 4.0, S.DIFFDRIVE, horizon=128))
+    gpu.set_options(d4.PREC_F32, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    u = controls_for(p, 16, 5, scale=2.5)   # clamped: |ω| at the limit most of the time
+    st, ct, rw, cnt = gpu.rollout_fitness(u)
+    worst = 0.0
+    for m in range(u.shape[0]):
+        rs, rc = oracle.rollout(p, u[m])
+        worst = max(worst, float(np.abs(st[m][..., :2] - rs[..., :2]).max()))
+        np.testing.assert_allclose(st[m], rs, atol=2e-5, rtol=1e-5)
+    print(f"{kind}: max |Δposition| = {worst:.3g} m over {p.horizon} steps")
