@@ -32,7 +32,7 @@
 
 namespace d4k {
 template <typename S, int KIND>
-cudaError_t launch_k23(int tb, int maxw, int noise, dim3 grid, int threads, size_t smem, cudaStream_t st,
+cudaError_t launch_k23(int tb, int maxw, int noise, bool pl, dim3 grid, int threads, size_t smem, cudaStream_t st,
                        const FitParams<S>& p);
 }
 
@@ -129,6 +129,7 @@ struct d4orm_cuda_ctx {
   d4orm_problem prob{};
   std::vector<double> starts, goals, obs_c, obs_r;
   int TB = 16, Rp = 16, MAXW = 2, spc = 16, TC = 16;
+  bool pl = false;  // fp32 pair-list fitness (planar, 33..64 robots)
   size_t smem32 = 0, smem64 = 0;
   int TC32 = 16, TC64 = 16;
 
@@ -138,7 +139,7 @@ struct d4orm_cuda_ctx {
   void* noise_user = nullptr;
 
   // device buffers (typeless where the scalar type varies)
-  DevBuf<unsigned char> z[2], base, msv, bm, starts_d, goals_d, inv_d, obs_d, ocl_d, partial, roots;
+  DevBuf<unsigned char> z[2], base, msv, bm, starts_d, goals_d, inv_d, obs_d, ocl_d, opl_d, partial, roots;
   DevBuf<unsigned char> states_out, controls_out;
   DevBuf<double> var, rewards, w64, trace, wscratch;
   DevBuf<float> w32;
@@ -175,7 +176,7 @@ struct d4orm_cuda_ctx {
     cub_tmp.release();
     bl_d.release();
     bl_i.release();
-    for (auto* b : {&z[0], &z[1], &base, &msv, &bm, &starts_d, &goals_d, &inv_d, &obs_d, &ocl_d, &partial, &roots,
+    for (auto* b : {&z[0], &z[1], &base, &msv, &bm, &starts_d, &goals_d, &inv_d, &obs_d, &ocl_d, &opl_d, &partial, &roots,
                     &states_out, &controls_out})
       b->release();
     var.release(); rewards.release(); w64.release(); trace.release(); w32.release(); wscratch.release();
@@ -229,7 +230,8 @@ int64_t elems_of(const d4orm_cuda_ctx* c) { return (int64_t)c->prob.robots * c->
 
 template <typename S>
 size_t fit_smem(const d4orm_cuda_ctx* c, int TC) {
-  return d4k::fit_smem_bytes<S>(c->prob.pdim, c->spc, TC, c->Rp, c->prob.n_obstacles, c->spc * c->Rp, c->TB);
+  return d4k::fit_smem_bytes<S>(c->prob.pdim, c->spc, TC, c->Rp, c->prob.n_obstacles, c->spc * c->Rp, c->TB,
+                                std::is_same<S, float>::value && c->pl);
 }
 
 // Time-chunk length: one fitness item per thread (TC = Rp, ≥ 16), a multiple
@@ -240,7 +242,8 @@ int choose_tc(d4orm_cuda_ctx* ctx, int* tc_out, size_t* smem_out) {
   // tile; then halve further (Q ≤ 4) only if the tile still exceeds 100 KB.
   const int Rp = ctx->Rp;
   int TC = Rp >= 16 ? (Rp > 64 ? Rp / 2 : Rp) : 16;
-  if (const char* e = std::getenv("D4ORM_Q")) {  // tuning knob: threads per fitness item (1, 2, 4)
+  const bool pl = std::is_same<S, float>::value && ctx->pl;  // pair-list path: TC = Rp = 64, fixed
+  if (const char* e = pl ? nullptr : std::getenv("D4ORM_Q")) {  // tuning knob: threads per fitness item (1, 2, 4)
     const int q = std::atoi(e);
     if ((q == 2 || q == 4) && Rp % q == 0 && (Rp / q) % d4k::kPF == 0) TC = Rp / q;
   }
@@ -248,6 +251,7 @@ int choose_tc(d4orm_cuda_ctx* ctx, int* tc_out, size_t* smem_out) {
          (TC / 2 >= Rp || (Rp % (TC / 2) == 0 && Rp / (TC / 2) <= 4)))
     TC /= 2;
   if (TC % d4k::kPF != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d not a multiple of %d", TC, d4k::kPF);
+  if (pl && TC != 64) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: pair-list path needs TC = 64, got %d", TC);
   if (TC >= Rp && TC % Rp != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d vs Rp %d", TC, Rp);
   if (TC < Rp && (Rp % TC != 0 || Rp / TC > 4))
     return fail(ctx, D4ORM_E_UNSUPPORTED, "d4orm_cuda: %d robots need a %d-step tile that does not fit", ctx->prob.robots, TC);
@@ -347,6 +351,24 @@ int upload_problem(d4orm_cuda_ctx* ctx) {
     CU(cudaMemcpyAsync(ctx->ocl_d.p, tab.data(), tab.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->s_main));
     CU(cudaStreamSynchronize(ctx->s_main));
     obs[4 * O + 3] = 1e30;  // pad row: |p|² + 1e30 > 0
+    // pair-list path: (cx, cy, −L²↑, 0) and the inflated box the culling tests
+    // (slack > the direct form's rounding error), original obstacle order
+    std::vector<float> opl((size_t)8 * std::max(O, 1), 0.f);
+    for (int o = 0; o < O && PD == 2; ++o) {
+      const double lim = ctx->obs_r[o] + p.robot_radius;
+      const double cx = ctx->obs_c[(size_t)o * PD], cy = ctx->obs_c[(size_t)o * PD + 1];
+      const double slack = 1e-3 + 1e-5 * (std::fabs(cx) + std::fabs(cy) + lim);
+      opl[8 * o] = (float)cx;
+      opl[8 * o + 1] = (float)cy;
+      opl[8 * o + 2] = -std::nextafter((float)(lim * lim), INFINITY);
+      opl[8 * o + 4] = (float)(cx - lim - slack);
+      opl[8 * o + 5] = (float)(cy - lim - slack);
+      opl[8 * o + 6] = (float)(cx + lim + slack);
+      opl[8 * o + 7] = (float)(cy + lim + slack);
+    }
+    CU(ctx->opl_d.ensure(opl.size() * sizeof(float)));
+    CU(cudaMemcpyAsync(ctx->opl_d.p, opl.data(), opl.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->s_main));
+    CU(cudaStreamSynchronize(ctx->s_main));
   }
   CU((upload_as<S>(ctx->obs_d, obs.data(), obs.size(), ctx->s_main)));
   return D4ORM_OK;
@@ -367,6 +389,7 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
   f.inv_dstart = (const S*)ctx->inv_d.p;
   f.obs = (const S*)ctx->obs_d.p;
   f.obs_cull = std::is_same<S, float>::value ? (const S*)ctx->ocl_d.p : nullptr;
+  f.obs_pl = std::is_same<S, float>::value ? (const float*)ctx->opl_d.p : nullptr;
   f.n_obs = p.n_obstacles;
   for (int d = 0; d < 3; ++d) {
     f.lower[d] = (S)p.lower[d];
@@ -406,15 +429,16 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
 
 template <typename S>
 cudaError_t launch_fit(d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f, size_t smem, bool fused) {
+  const bool pl = std::is_same<S, float>::value && ctx->pl;
   const dim3 grid((unsigned)((f.M + ctx->spc - 1) / ctx->spc));
   const int th = ctx->spc * ctx->Rp;
   switch (ctx->prob.kind) {
-    case 0: return d4k::launch_k23<S, 0>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
-    case 1: return d4k::launch_k23<S, 1>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
-    case 2: return d4k::launch_k23<S, 2>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
-    case 3: return d4k::launch_k23<S, 3>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
-    case 4: return d4k::launch_k23<S, 4>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
-    default: return d4k::launch_k23<S, 5>(ctx->TB, ctx->MAXW, fused ? 1 : 0, grid, th, smem, ctx->s_main, f);
+    case 0: return d4k::launch_k23<S, 0>(ctx->TB, ctx->MAXW, fused ? 1 : 0, pl, grid, th, smem, ctx->s_main, f);
+    case 1: return d4k::launch_k23<S, 1>(ctx->TB, ctx->MAXW, fused ? 1 : 0, pl, grid, th, smem, ctx->s_main, f);
+    case 2: return d4k::launch_k23<S, 2>(ctx->TB, ctx->MAXW, fused ? 1 : 0, pl, grid, th, smem, ctx->s_main, f);
+    case 3: return d4k::launch_k23<S, 3>(ctx->TB, ctx->MAXW, fused ? 1 : 0, pl, grid, th, smem, ctx->s_main, f);
+    case 4: return d4k::launch_k23<S, 4>(ctx->TB, ctx->MAXW, fused ? 1 : 0, pl, grid, th, smem, ctx->s_main, f);
+    default: return d4k::launch_k23<S, 5>(ctx->TB, ctx->MAXW, fused ? 1 : 0, pl, grid, th, smem, ctx->s_main, f);
   }
 }
 
@@ -1379,6 +1403,11 @@ int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* p) {
     if (tb == 4 || tb == 8 || tb == 16) ctx->TB = std::max(tb, R <= 4 ? 4 : (R <= 8 ? 8 : 4));
   }
   ctx->Rp = (R + ctx->TB - 1) / ctx->TB * ctx->TB;
+  // planar teams of 33..64 robots: the pair-list fitness (Rp = 64, one warp =
+  // one sample's 32-step window); tuning knob D4ORM_PL=0 keeps the tile path
+  ctx->pl = p->pdim == 2 && R > 32 && R <= 64 && ctx->TB == 16;
+  if (const char* e = std::getenv("D4ORM_PL")) ctx->pl = ctx->pl && std::atoi(e) != 0;
+  if (ctx->pl) ctx->Rp = 64;
   ctx->MAXW = ctx->Rp <= 64 ? 2 : 8;
   // 128-thread CTAs (several resident per SM: one CTA's latency-bound rollout
   // phase overlaps another's compute-bound fitness phase)

@@ -46,6 +46,7 @@ struct FitParams {
   const S* obs_cull;     // fp32: obstacle x-bucket table (kObsBuckets, see upload_problem), obstacles sorted by left end
   S cull_margin;         // fp32: separation (m) beyond which a pair cannot be in conflict, with rounding slack
   int cull;              // fp32: rank robots by x per chunk and cull tile pairs / obstacles (≥ 3 tiles)
+  const float* obs_pl;   // fp32 pair-list path: [O][8] (cx, cy, −L²↑, 0, box lo.x, lo.y, hi.x, hi.y)
   int n_obs;
   S lower[3], upper[3];
   S dt, half_dt, dt6;
@@ -75,6 +76,8 @@ struct FitSmem {
   S* ocl;     // fp32: obstacle x-bucket table (FitParams::obs_cull): {x0, 1/w, -, -} + [kObsBuckets][2] int
   int* key;   // fp32: [spc][Rp] chunk sort keys (x order)
   float* bb;  // fp32: [2·ntiles][nthreads] per-item tile x-extent (lo, hi)
+  float4* pbox;  // fp32 pair-list path: [spc][TC/32][Rp] robot window boxes (lo.x, lo.y, hi.x, hi.y)
+  float* opl;    // fp32 pair-list path: FitParams::obs_pl
   // the final reduction arrays alias `pos` (dead after the last chunk)
   double* red;   // [nthreads]
   double* eff;   // [nthreads]
@@ -86,7 +89,8 @@ struct FitSmem {
 };
 
 template <typename S>
-__host__ __device__ inline size_t fit_smem_bytes(int PD, int spc, int TC, int Rp, int nobs, int nthreads, int TB) {
+__host__ __device__ inline size_t fit_smem_bytes(int PD, int spc, int TC, int Rp, int nobs, int nthreads, int TB,
+                                                 bool pl = false) {
   const int RS = Rp + 2;
   size_t pos = (size_t)PD * spc * TC * RS * sizeof(S);
   const size_t red = 2 * (size_t)nthreads * sizeof(double) + 2 * (size_t)nthreads * sizeof(int);
@@ -94,6 +98,10 @@ __host__ __device__ inline size_t fit_smem_bytes(int PD, int spc, int TC, int Rp
   b += (size_t)4 * (nobs + 1) * sizeof(S);
   if (sizeof(S) == 8) {
     b += (size_t)PD * Rp * sizeof(S) + 2 * (size_t)Rp * sizeof(S);
+  } else if (pl) {  // key, robot window boxes, obstacle table
+    b += (size_t)spc * Rp * sizeof(int);
+    b = (b + 15) & ~size_t(15);
+    b += (size_t)spc * (TC / 32) * Rp * sizeof(float4) + (size_t)8 * nobs * sizeof(float);
   } else {
     b += (size_t)(4 + 2 * kObsBuckets) * sizeof(float) + (size_t)spc * Rp * sizeof(int) +
          (size_t)2 * (Rp / TB) * nthreads * sizeof(float);
@@ -426,6 +434,121 @@ __device__ __forceinline__ void item_f32(const FitSmem<float>& sm, int s, int tc
   }
 }
 
+// ------------------------------------------------------- fp32 pair-list path
+// Rp = 64 robots as 32 column pairs (2l, 2l+1); a warp is one sample's 32
+// consecutive steps (TC = 64: two warp windows per chunk).  Phase A leaves each
+// robot's bounding box over the window (its swept box); the chunk ranking
+// (x strips of 16, y inside a strip) pairs robots that are close.  Per window
+// the warp first decides which pair-pair blocks can hold a conflict — swept
+// pair boxes within the margin, one lane per pair, one ballot per offset d of
+// the circular enumeration (l, l + d mod 32) — then every lane tests only
+// those blocks at its own step: 4 tests per block in the direct form
+// t = Δx² + Δy² − m²↑ (8 packed FP2 ops), sign bit ⇔ the reference's `<=`
+// (reward.cpp:106).  Obstacles likewise: pair boxes vs the obstacles'
+// inflated boxes, then t = |p − c|² − L²↑ (reward.cpp:120).  The culling is
+// exact: swept boxes contain every position of the window and the margin
+// carries a rounding slack (cull_margin), so a skipped block holds no hit.
+__device__ __forceinline__ uint64_t fsub2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+__device__ __forceinline__ bool boxes_meet(float4 a, float4 b) {  // (lo.x, lo.y, hi.x, hi.y)
+  return a.z >= b.x && b.z >= a.x && a.w >= b.y && b.w >= a.y;
+}
+
+// Pair (2l, 2l+1) vs pair (2j, 2j+1) at one step: conflict bits of the four
+// robots OR-ed into `conf` (bit = column).  Hits are rare: the bit assembly
+// is behind a branch on "any test of this lane hit".
+__device__ __forceinline__ void pl_block(const float* X, const float* Y, int l, int j, uint64_t nm2, uint64_t& conf) {
+  const uint64_t xa = *reinterpret_cast<const uint64_t*>(X + 2 * l);
+  const uint64_t ya = *reinterpret_cast<const uint64_t*>(Y + 2 * l);
+  const uint64_t xb = *reinterpret_cast<const uint64_t*>(X + 2 * j);
+  const uint64_t yb = *reinterpret_cast<const uint64_t*>(Y + 2 * j);
+  uint64_t t0 = ffma2_sq(fsub2(xb, pack2(lo_f(xa), lo_f(xa))), nm2);
+  uint64_t t1 = ffma2_sq(fsub2(xb, pack2(hi_f(xa), hi_f(xa))), nm2);
+  t0 = ffma2_sq(fsub2(yb, pack2(lo_f(ya), lo_f(ya))), t0);
+  t1 = ffma2_sq(fsub2(yb, pack2(hi_f(ya), hi_f(ya))), t1);
+  const uint32_t r0 = lo32(t0) | hi32(t0), r1 = lo32(t1) | hi32(t1);
+  if ((int)(r0 | r1) < 0) {
+    const uint32_t c0 = lo32(t0) | lo32(t1), c1 = hi32(t0) | hi32(t1);
+    const uint64_t rb = (r0 >> 31) | ((r1 >> 31) << 1), cb = (c0 >> 31) | ((c1 >> 31) << 1);
+    conf |= (rb << (2 * l)) | (cb << (2 * j));
+  }
+}
+
+// One (sample, t) item of the pair-list path: conflict and obstacle bits per
+// column.  Called by all 32 lanes of a warp (one sample, one window); lanes
+// whose step lies beyond the horizon run along and the caller drops them.
+__device__ __forceinline__ void item_pl(const FitSmem<float>& sm, int s, int tc, int n_obs, float m2u, float cmh,
+                                        bool cull, uint64_t& conf, uint64_t& obsm) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const float* X = sm.row(0, s, tc);
+  const float* Y = sm.row(1, s, tc);
+  float4* pb = sm.pbox + (size_t)(s * (sm.TC / 32) + (tc >> 5)) * sm.Rp;
+  const uint64_t nm2 = pack2(-m2u, -m2u);
+  const float4 b0 = pb[2 * lane], b1 = pb[2 * lane + 1];
+  const float4 A = make_float4(fminf(b0.x, b1.x), fminf(b0.y, b1.y), fmaxf(b0.z, b1.z), fmaxf(b0.w, b1.w));
+  const float4 Ai = make_float4(A.x - cmh, A.y - cmh, A.z + cmh, A.w + cmh);
+  // the pair's own test (2l, 2l+1)
+  uint32_t bits = full;
+  if (cull) {
+    const float4 b0i = make_float4(b0.x - cmh, b0.y - cmh, b0.z + cmh, b0.w + cmh);
+    const float4 b1i = make_float4(b1.x - cmh, b1.y - cmh, b1.z + cmh, b1.w + cmh);
+    bits = __ballot_sync(full, boxes_meet(b0i, b1i));
+  }
+  __syncwarp();
+  pb[lane] = Ai;  // pair boxes replace the robot boxes (this warp's window only)
+  __syncwarp();
+  while (bits) {
+    const int l = __ffs(bits) - 1;
+    bits &= bits - 1u;
+    const float2 x = *reinterpret_cast<const float2*>(X + 2 * l);
+    const float2 y = *reinterpret_cast<const float2*>(Y + 2 * l);
+    const float dx = x.y - x.x, dy = y.y - y.x;
+    const float t = fmaf(dx, dx, fmaf(dy, dy, -m2u));
+    if (t < 0.f) conf |= 3ull << (2 * l);
+  }
+  // pair-pair blocks (l, l + d mod 32), d = 1..16 (d = 16 once per pair)
+#pragma unroll 1
+  for (int d = 1; d <= 16; ++d) {
+    uint32_t live;
+    if (cull) {
+      const float4 B = pb[(lane + d) & 31];
+      live = __ballot_sync(full, (d < 16 || lane < 16) && boxes_meet(Ai, B));
+    } else {
+      live = d < 16 ? full : 0xffffu;
+    }
+    while (live) {
+      const int l = __ffs(live) - 1;
+      live &= live - 1u;
+      pl_block(X, Y, l, (l + d) & 31, nm2, conf);
+    }
+  }
+  // obstacles: pair boxes vs the obstacles' inflated boxes
+#pragma unroll 1
+  for (int o = 0; o < n_obs; ++o) {
+    const float* ob = sm.opl + 8 * o;
+    uint32_t live = full;
+    if (cull) live = __ballot_sync(full, boxes_meet(A, *reinterpret_cast<const float4*>(ob + 4)));
+    if (!live) continue;
+    const float4 oc = *reinterpret_cast<const float4*>(ob);  // cx, cy, −L²↑
+    const uint64_t cx = pack2(oc.x, oc.x), cy = pack2(oc.y, oc.y), nl = pack2(oc.z, oc.z);
+    while (live) {
+      const int l = __ffs(live) - 1;
+      live &= live - 1u;
+      const uint64_t xa = *reinterpret_cast<const uint64_t*>(X + 2 * l);
+      const uint64_t ya = *reinterpret_cast<const uint64_t*>(Y + 2 * l);
+      uint64_t t = ffma2_sq(fsub2(xa, cx), nl);
+      t = ffma2_sq(fsub2(ya, cy), t);
+      if ((int)(lo32(t) | hi32(t)) < 0)
+        obsm |= (uint64_t)((lo32(t) >> 31) | ((hi32(t) >> 31) << 1)) << (2 * l);
+    }
+  }
+}
+
 // One (sample, t) item in fp64: the reference's loops (reward.cpp:88-127) on
 // shared-memory positions, exact `<=` tests; returns Σ goal terms.
 template <int PD>
@@ -513,12 +636,12 @@ __device__ __forceinline__ int chunk_key(float x, int k, int Rp2, bool real) {
 // Pointers advance by a stride per step (no per-step 64-bit index math).  The
 // returned value is 0 unless some state went non-finite (NaN/inf propagate
 // through fma(x, 0, acc)); the caller then replays the chunk exactly.
-template <int KIND, bool FULL, bool SDV>
+template <int KIND, bool FULL, bool SDV, bool PLB>
 __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, const float* bmp, const float* sdp,
                                             float* zp, int RDU,
                                             uint64_t m, int kA, uint32_t g0, uint2 key, float* px, float* py, float* pz,
                                             int RS, float* x, float& eff32, float& chk, const float* ng, float ginv,
-                                            float& gsd) {
+                                            float& gsd, float4& bx) {
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
   float bq[kPF][DU], sq[SDV ? kPF : 1][DU];
 #pragma unroll
@@ -607,12 +730,20 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
       px[j * RS] = x[0];
       py[j * RS] = x[1];
       if constexpr (PD == 3) pz[j * RS] = x[2];
+      if constexpr (PLB) {  // pair-list path: the robot's swept box over the warp window
+        bx.x = fminf(bx.x, x[0]);
+        bx.y = fminf(bx.y, x[1]);
+        bx.z = fmaxf(bx.z, x[0]);
+        bx.w = fmaxf(bx.w, x[1]);
+      }
     }
   }
   if constexpr (PK) eff32 += lo_f(eff2) + hi_f(eff2);
 }
 
-template <int KIND, bool SDV>
+__device__ __forceinline__ float4 empty_box() { return make_float4(INFINITY, INFINITY, -INFINITY, -INFINITY); }
+
+template <int KIND, bool SDV, bool PL>
 __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const FitSmem<float>& sm, int sA, int kA,
                                                int rA, int64_t m, int t0, int nsteps, float* x, float* zrow, uint2 key,
                                                float& eff32, const float* ng, float ginv, float& gsd) {
@@ -627,15 +758,24 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
   float* pz = PD == 3 ? sm.row(2, sA, 0) + rA : px;
   const int RS = sm.RS;
   float chk = 0.f;
+  float4 bx = empty_box();
+  float4* pbw = PL ? sm.pbox + (size_t)sA * (sm.TC / 32) * sm.Rp + rA : nullptr;  // window 0 box slot
   for (int tc = 0; tc < nsteps; tc += kPF) {
     const int nb = nsteps - tc;
     const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
     if (nb >= kPF) {
-      fused_block<KIND, true, SDV>(p, kPF, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk, ng,
-                              ginv, gsd);
+      fused_block<KIND, true, SDV, PL>(p, kPF, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk,
+                                       ng, ginv, gsd, bx);
     } else {
-      fused_block<KIND, false, SDV>(p, nb, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk, ng,
-                               ginv, gsd);
+      fused_block<KIND, false, SDV, PL>(p, nb, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32,
+                                        chk, ng, ginv, gsd, bx);
+    }
+    if constexpr (PL) {
+      if (((tc + kPF) & 31) == 0 || tc + kPF >= nsteps) {  // end of a warp window (or of the steps)
+        *pbw = bx;
+        pbw += sm.Rp;
+        bx = empty_box();
+      }
     }
     bmp += kPF * RDU;
     if constexpr (SDV) sdp += kPF * RDU;
@@ -643,6 +783,9 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
     px += kPF * RS;
     py += kPF * RS;
     pz += kPF * RS;
+  }
+  if constexpr (PL) {  // windows past the horizon: empty boxes
+    for (float4* e = sm.pbox + (size_t)(sA + 1) * (sm.TC / 32) * sm.Rp + rA; pbw < e; pbw += sm.Rp) *pbw = empty_box();
   }
   // state = position (velocity-input kinds): a NaN/inf state reaches the goal
   // distance, so the goal sum (ginv > 0: start ≠ goal is validated) carries it
@@ -677,8 +820,10 @@ __device__ __noinline__ void rollout_check(const FitParams<float>& p, int kA, in
   }
 }
 
-template <typename S, int KIND, int TB, int MAXW, int NOISE>
+template <typename S, int KIND, int TB, int MAXW, int NOISE, bool PL = false>
 __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fitness(const FitParams<S> p) {
+  static_assert(!PL || (std::is_same<S, float>::value && ModelDims<KIND>::PD == 2 && MAXW == 2),
+                "pair-list path: fp32, planar kinds, Rp = 64");
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
   constexpr bool F32 = std::is_same<S, float>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -700,7 +845,14 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
     sm.cnt = reinterpret_cast<int*>(sm.eff + nthreads);
     sm.obs = reinterpret_cast<S*>(smem_raw + (((pos_b > red_b ? pos_b : red_b) + 15) & ~size_t(15)));
   }
-  if constexpr (F32) {
+  if constexpr (F32 && PL) {
+    sm.key = reinterpret_cast<int*>(sm.obs + 4 * (p.n_obs + 1));
+    sm.pbox = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(sm.key + spc * Rp) + 15) & ~uintptr_t(15));
+    sm.opl = reinterpret_cast<float*>(sm.pbox + (size_t)spc * (TC / 32) * Rp);
+    sm.bb = sm.ocl = nullptr;
+    sm.goal = sm.inv = nullptr;
+    for (int j = tid; j < 8 * p.n_obs; j += nthreads) sm.opl[j] = p.obs_pl[j];  // (c, −L²↑, box)
+  } else if constexpr (F32) {
     sm.key = reinterpret_cast<int*>(sm.obs + 4 * (p.n_obs + 1));  // 16-B aligned (Rp % 4 == 0)
     sm.bb = reinterpret_cast<float*>(sm.key + spc * Rp);
     sm.ocl = sm.bb + 2 * (Rp / TB) * nthreads;
@@ -804,7 +956,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
     // ===== fp32: rank the sample's robots by x at the chunk start; a robot's
     // positions go to column rA, so TB-robot tiles are x-strips (culling)
     int rA = kA;
-    if (F32 && p.cull) {
+    if (F32 && (p.cull || PL)) {
       if (liveA) sm.key[tid] = chunk_key((float)x[0], kA, Rp2, robotA);
       __syncthreads();
       if (robotA) {
@@ -817,6 +969,32 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
         }
         rA = r;
       }
+      if constexpr (PL) {
+        // second level: y order inside each 16-robot x strip, so column pairs
+        // (2l, 2l+1) are neighbours in both coordinates (padding stays last)
+        __syncthreads();
+        if (liveA) {
+          int yi = __float_as_int((float)x[1]);
+          yi ^= (yi >> 31) & 0x7fffffff;
+          const uint32_t yu = (uint32_t)yi ^ 0x80000000u;
+          sm.key[tid] = robotA ? (int)(((uint32_t)(rA >> 4) << 28) | ((yu >> 10) << 6) | (uint32_t)kA)
+                               : (int)(0x7fffffc0u | (uint32_t)kA);
+        }
+        __syncthreads();
+        if (robotA) {
+          const int me = sm.key[tid];
+          const int4* kv = reinterpret_cast<const int4*>(sm.key + sA * Rp);
+          int r = 0;
+          for (int j = 0; j < Rp / 4; ++j) {
+            const int4 v = kv[j];
+            r += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
+          }
+          rA = r;
+        }
+        if (liveA && !robotA) {  // padding columns (rank = lane): empty window boxes
+          for (int w = 0; w < TC / 32; ++w) sm.pbox[((size_t)sA * (TC / 32) + w) * Rp + kA] = empty_box();
+        }
+      }
     }
     // ===== phase A: integrate TC steps
     if constexpr (NOISE >= 1) {
@@ -826,7 +1004,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
 #pragma unroll
         for (int q = 0; q < DX; ++q) x0[q] = x[q];
         float gsd = 0.f;
-        const float chk = rollout_fused<KIND, NOISE == 2>(p, sm, sA, kA, rA, p.m_global0 + mA, t0, nsteps, x, zst, key, eff32,
+        const float chk = rollout_fused<KIND, NOISE == 2, PL>(p, sm, sA, kA, rA, p.m_global0 + mA, t0, nsteps, x, zst, key, eff32,
                                               ng, ginv, gsd);
         goalA += (Acc)nsteps - (Acc)gsd;
         if (!(chk == 0.f)) rollout_check<KIND>(p, kA, p.m_global0 + mA, t0, nsteps, x0, zst);
@@ -834,6 +1012,8 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
     } else if (robotA) {
       float gsd = 0.f;
       const int t_end = t0 + TC < T ? t0 + TC : T;
+      float4 bxA = empty_box();  // pair-list path: swept box of the warp window
+      float4* pbwA = PL ? sm.pbox + (size_t)sA * (TC / 32) * Rp + rA : nullptr;
 #pragma unroll
       for (int j = 0; j < kPF; ++j) fetch(t0 + j, t_end, j);
       for (int tc = 0; tc < TC; tc += kPF) {
@@ -873,6 +1053,17 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
             sm.row(0, sA, tc + j)[rA] = x[0];
             sm.row(1, sA, tc + j)[rA] = x[1];
             if constexpr (PD == 3) sm.row(2, sA, tc + j)[rA] = x[2];
+            if constexpr (PL) {
+              bxA.x = fminf(bxA.x, (float)x[0]);
+              bxA.y = fminf(bxA.y, (float)x[1]);
+              bxA.z = fmaxf(bxA.z, (float)x[0]);
+              bxA.w = fmaxf(bxA.w, (float)x[1]);
+              if (((tc + j + 1) & 31) == 0 || t + 1 == t_end) {
+                *pbwA = bxA;
+                pbwA += Rp;
+                bxA = empty_box();
+              }
+            }
             if (NOISE == 0 && p.states_out) {
               S* so = p.states_out + (mA * (int64_t)(T + 1) + t + 1) * R * DX + (int64_t)kA * DX;
 #pragma unroll
@@ -887,6 +1078,9 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
         }
       }
       if constexpr (F32) goalA += (Acc)(t_end - t0) - (Acc)gsd;
+      if constexpr (PL) {  // windows past the horizon: empty boxes
+        for (float4* e = sm.pbox + (size_t)(sA + 1) * (TC / 32) * Rp + rA; pbwA < e; pbwA += Rp) *pbwA = empty_box();
+      }
     }
     effort += (Acc)eff32;  // per-chunk fp32 partial → the cross-chunk accumulator
     eff32 = 0.f;
@@ -894,10 +1088,26 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
 
     // ===== phase B: fitness of the TC steps just integrated
 #ifdef D4K_EXPERIMENT_SKIP_B
-    if (liveB && p.n_obs < 0) {
+    const bool runB = p.n_obs < 0;
 #else
-    if (liveB) {
+    constexpr bool runB = true;
 #endif
+    if (PL && runB && mB < p.M) {
+      // pair-list path: the warp is one sample's 32-step window; lanes past the
+      // horizon run the warp-collective loops and are dropped here
+      if constexpr (PL) {
+        const int tc = item0 - sB * TC;
+        if (t0 + (tc & ~31) < T) {
+          uint64_t conf = 0, obsm = 0;
+          item_pl(sm, sB, tc, p.n_obs, p.margin_sq, 0.5f * p.cull_margin, p.cull != 0, conf, obsm);
+          if (t0 + tc < T) {
+            const uint64_t real = R >= 64 ? ~0ull : ((1ull << R) - 1ull);
+            nconf += __popcll(conf & real);
+            nobs += __popcll(obsm & real);
+          }
+        }
+      }
+    } else if (liveB && runB) {
       for (int j = 0; j < ipt; ++j) {
         const int tc = item0 + j - sB * TC;
         if (t0 + tc >= T) break;

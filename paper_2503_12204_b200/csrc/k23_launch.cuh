@@ -9,9 +9,9 @@
 
 namespace d4k {
 
-template <typename S, int KIND, int TB, int MAXW, int NOISE>
+template <typename S, int KIND, int TB, int MAXW, int NOISE, bool PL = false>
 cudaError_t launch_k23_tb(dim3 grid, int threads, size_t smem, cudaStream_t st, const FitParams<S>& p) {
-  auto fn = k_rollout_fitness<S, KIND, TB, MAXW, NOISE>;
+  auto fn = k_rollout_fitness<S, KIND, TB, MAXW, NOISE, PL>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   fn<<<grid, threads, smem, st>>>(p);
@@ -19,8 +19,14 @@ cudaError_t launch_k23_tb(dim3 grid, int threads, size_t smem, cudaStream_t st, 
 }
 
 template <typename S, int KIND, int NOISE>
-cudaError_t launch_k23_n(int tb, int maxw, dim3 grid, int threads, size_t smem, cudaStream_t st,
+cudaError_t launch_k23_n(int tb, int maxw, bool pl, dim3 grid, int threads, size_t smem, cudaStream_t st,
                          const FitParams<S>& p) {
+  if (pl) {  // pair-list fitness: fp32, planar kinds, Rp = 64
+    if constexpr (std::is_same<S, float>::value && ModelDims<KIND>::PD == 2) {
+      if (tb == 16 && maxw == 2) return launch_k23_tb<S, KIND, 16, 2, NOISE, true>(grid, threads, smem, st, p);
+    }
+    return cudaErrorInvalidValue;
+  }
   if (maxw <= 2) {
     switch (tb) {
       case 4: return launch_k23_tb<S, KIND, 4, 2, NOISE>(grid, threads, smem, st, p);
@@ -34,21 +40,21 @@ cudaError_t launch_k23_n(int tb, int maxw, dim3 grid, int threads, size_t smem, 
 }
 
 template <typename S, int KIND>
-cudaError_t launch_k23(int tb, int maxw, int noise, dim3 grid, int threads, size_t smem, cudaStream_t st,
+cudaError_t launch_k23(int tb, int maxw, int noise, bool pl, dim3 grid, int threads, size_t smem, cudaStream_t st,
                        const FitParams<S>& p) {
   if constexpr (std::is_same<S, float>::value) {
-    if (noise && p.sdv) return launch_k23_n<S, KIND, 2>(tb, maxw, grid, threads, smem, st, p);  // CEM
-    if (noise) return launch_k23_n<S, KIND, 1>(tb, maxw, grid, threads, smem, st, p);
+    if (noise && p.sdv) return launch_k23_n<S, KIND, 2>(tb, maxw, pl, grid, threads, smem, st, p);  // CEM
+    if (noise) return launch_k23_n<S, KIND, 1>(tb, maxw, pl, grid, threads, smem, st, p);
   } else {
-    if (noise) return cudaErrorInvalidValue;
+    if (noise || pl) return cudaErrorInvalidValue;
   }
-  return launch_k23_n<S, KIND, 0>(tb, maxw, grid, threads, smem, st, p);
+  return launch_k23_n<S, KIND, 0>(tb, maxw, pl, grid, threads, smem, st, p);
 }
 
-#define D4K_INSTANTIATE_K23(KIND)                                                                  \
-  template cudaError_t launch_k23<float, KIND>(int, int, int, dim3, int, size_t, cudaStream_t,     \
-                                               const FitParams<float>&);                            \
-  template cudaError_t launch_k23<double, KIND>(int, int, int, dim3, int, size_t, cudaStream_t,    \
+#define D4K_INSTANTIATE_K23(KIND)                                                                      \
+  template cudaError_t launch_k23<float, KIND>(int, int, int, bool, dim3, int, size_t, cudaStream_t,   \
+                                               const FitParams<float>&);                                \
+  template cudaError_t launch_k23<double, KIND>(int, int, int, bool, dim3, int, size_t, cudaStream_t,  \
                                                 const FitParams<double>&);
 
 }  // namespace d4k
