@@ -511,40 +511,61 @@ __device__ __forceinline__ void item_pl(const FitSmem<float>& sm, int s, int tc,
     const float t = fmaf(dx, dx, fmaf(dy, dy, -m2u));
     if (t < 0.f) conf |= 3ull << (2 * l);
   }
-  // pair-pair blocks (l, l + d mod 32), d = 1..16 (d = 16 once per pair)
-#pragma unroll 1
+  // pair-pair blocks (l, l + d mod 32), d = 1..16 (d = 16 once per pair):
+  // all 16 ballots first (independent loads and votes), then the blocks, two
+  // per iteration so their load → test chains overlap
+  uint32_t lv[16];
+#pragma unroll
   for (int d = 1; d <= 16; ++d) {
-    uint32_t live;
     if (cull) {
       const float4 B = pb[(lane + d) & 31];
-      live = __ballot_sync(full, (d < 16 || lane < 16) && boxes_meet(Ai, B));
+      lv[d - 1] = __ballot_sync(full, (d < 16 || lane < 16) && boxes_meet(Ai, B));
     } else {
-      live = d < 16 ? full : 0xffffu;
-    }
-    while (live) {
-      const int l = __ffs(live) - 1;
-      live &= live - 1u;
-      pl_block(X, Y, l, (l + d) & 31, nm2, conf);
+      lv[d - 1] = d < 16 ? full : 0xffffu;
     }
   }
-  // obstacles: pair boxes vs the obstacles' inflated boxes
-#pragma unroll 1
-  for (int o = 0; o < n_obs; ++o) {
-    const float* ob = sm.opl + 8 * o;
-    uint32_t live = full;
-    if (cull) live = __ballot_sync(full, boxes_meet(A, *reinterpret_cast<const float4*>(ob + 4)));
-    if (!live) continue;
-    const float4 oc = *reinterpret_cast<const float4*>(ob);  // cx, cy, −L²↑
-    const uint64_t cx = pack2(oc.x, oc.x), cy = pack2(oc.y, oc.y), nl = pack2(oc.z, oc.z);
+#pragma unroll
+  for (int d = 1; d <= 16; ++d) {
+    uint32_t live = lv[d - 1];
     while (live) {
-      const int l = __ffs(live) - 1;
+      const int l1 = __ffs(live) - 1;
       live &= live - 1u;
-      const uint64_t xa = *reinterpret_cast<const uint64_t*>(X + 2 * l);
-      const uint64_t ya = *reinterpret_cast<const uint64_t*>(Y + 2 * l);
-      uint64_t t = ffma2_sq(fsub2(xa, cx), nl);
-      t = ffma2_sq(fsub2(ya, cy), t);
-      if ((int)(lo32(t) | hi32(t)) < 0)
-        obsm |= (uint64_t)((lo32(t) >> 31) | ((hi32(t) >> 31) << 1)) << (2 * l);
+      if (live) {
+        const int l2 = __ffs(live) - 1;
+        live &= live - 1u;
+        pl_block(X, Y, l1, (l1 + d) & 31, nm2, conf);
+        pl_block(X, Y, l2, (l2 + d) & 31, nm2, conf);
+      } else {
+        pl_block(X, Y, l1, (l1 + d) & 31, nm2, conf);
+      }
+    }
+  }
+  // obstacles: pair boxes vs the obstacles' inflated boxes, eight ballots at a time
+  for (int o0 = 0; o0 < n_obs; o0 += 8) {
+    uint32_t ov[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int o = o0 + q;
+      ov[q] = 0;
+      if (o < n_obs)
+        ov[q] = cull ? __ballot_sync(full, boxes_meet(A, *reinterpret_cast<const float4*>(sm.opl + 8 * o + 4))) : full;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint32_t live = ov[q];
+      if (!live) continue;
+      const float4 oc = *reinterpret_cast<const float4*>(sm.opl + 8 * (o0 + q));  // cx, cy, −L²↑
+      const uint64_t cx = pack2(oc.x, oc.x), cy = pack2(oc.y, oc.y), nl = pack2(oc.z, oc.z);
+      while (live) {
+        const int l = __ffs(live) - 1;
+        live &= live - 1u;
+        const uint64_t xa = *reinterpret_cast<const uint64_t*>(X + 2 * l);
+        const uint64_t ya = *reinterpret_cast<const uint64_t*>(Y + 2 * l);
+        uint64_t t = ffma2_sq(fsub2(xa, cx), nl);
+        t = ffma2_sq(fsub2(ya, cy), t);
+        if ((int)(lo32(t) | hi32(t)) < 0)
+          obsm |= (uint64_t)((lo32(t) >> 31) | ((hi32(t) >> 31) << 1)) << (2 * l);
+      }
     }
   }
 }
@@ -972,20 +993,22 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fi
       if constexpr (PL) {
         // second level: y order inside each 16-robot x strip, so column pairs
         // (2l, 2l+1) are neighbours in both coordinates (padding stays last)
+        // (keys stored at the x-rank slot: a strip's 16 keys are contiguous)
         __syncthreads();
+        int me = 0;
         if (liveA) {
           int yi = __float_as_int((float)x[1]);
           yi ^= (yi >> 31) & 0x7fffffff;
           const uint32_t yu = (uint32_t)yi ^ 0x80000000u;
-          sm.key[tid] = robotA ? (int)(((uint32_t)(rA >> 4) << 28) | ((yu >> 10) << 6) | (uint32_t)kA)
-                               : (int)(0x7fffffc0u | (uint32_t)kA);
+          me = robotA ? (int)(((yu >> 10) << 6) | (uint32_t)kA) : (int)(0x7fffffc0u | (uint32_t)kA);
+          sm.key[sA * Rp + rA] = me;
         }
         __syncthreads();
         if (robotA) {
-          const int me = sm.key[tid];
-          const int4* kv = reinterpret_cast<const int4*>(sm.key + sA * Rp);
-          int r = 0;
-          for (int j = 0; j < Rp / 4; ++j) {
+          const int4* kv = reinterpret_cast<const int4*>(sm.key + sA * Rp + (rA & ~15));
+          int r = rA & ~15;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
             const int4 v = kv[j];
             r += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
           }

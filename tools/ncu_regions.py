@@ -38,25 +38,48 @@ for r in rows[2:]:
     tot[1] += w
 
 
+ROOT = __import__("pathlib").Path(__file__).resolve().parent.parent / "paper_2503_12204_b200" / "csrc"
+# region = the last anchor (a source substring) at or above the line
+ANCHORS = {
+    "d4orm_common.cuh": [("enum Kind", "other (common)"), ("fast_sincos", "rollout: RK4"),
+                         ("detail::rk4_with", "rollout: RK4"), ("packed f32x2", "packed FP2 ops (tests, goal, controls)"),
+                         ("Philox noise", "noise: Philox4x32-10"), ("(2k+1)", "noise: Box-Muller")],
+    "k23.cuh": [("namespace d4k", "other (setup, barriers)"), ("fp32 tiles", "fitness (tiles): helpers"),
+                ("Obstacle index range", "fitness (tiles): obstacle range lookup"),
+                ("One (sample, t) item in fp32", "fitness (tiles): diagonal tiles + obstacles"),
+                ("pairs inside tile a", "fitness (tiles): diagonal inner pairs"),
+                ("const int n_off", "fitness (tiles): off-diagonal tile pairs"),
+                ("---- fp32 pair-list path", "fitness (pair list): block tests"),
+                ("One (sample, t) item of the pair-list", "fitness (pair list): boxes + self pairs"),
+                ("pair-pair blocks (l, l + d", "fitness (pair list): pair-pair liveness + loop"),
+                ("obstacles: pair boxes vs", "fitness (pair list): obstacles"),
+                ("One (sample, t) item in fp64", "fitness fp64"),
+                ("fp32 fused rollout (phase A)", "rollout: controls, clamp, goal, stores, boxes"),
+                ("Chunk sort key", "chunk ranking"), ("One robot's `nsteps` steps", "rollout: controls, clamp, goal, stores, boxes"),
+                ("Exact replay of a chunk", "rollout: replay"), ("__launch_bounds__", "other (setup, barriers)"),
+                ("rank the sample's robots", "chunk ranking"), ("phase A: integrate", "rollout: controls, clamp, goal, stores, boxes"),
+                ("phase B: fitness", "phase-B glue + final reduction")],
+}
+_tables = {}
+
+
 def region(f, l):
-    """Code regions of k23.cuh / d4orm_common.cuh (line ranges of the v11 sources)."""
-    if f == "d4orm_common.cuh":
-        if 140 <= l <= 164: return "noise: Philox4x32-10"
-        if 165 <= l <= 193: return "noise: Box-Muller"
-        if 100 <= l <= 135: return "packed FP2 ops (pair/obstacle tests, goal)"
-        if 60 <= l <= 99: return "rollout: RK4"
-        return "other (common)"
-    if f == "k23.cuh":
-        if 105 <= l <= 200: return "fitness: tile helpers"
-        if 203 <= l <= 208: return "fitness: obstacle range lookup"
-        if 241 <= l <= 336: return "fitness: diagonal tiles, extents + obstacles"
-        if 337 <= l <= 374: return "fitness: diagonal tiles, inner pairs"
-        if 377 <= l <= 426: return "fitness: off-diagonal tile pairs"
-        if 485 <= l <= 631: return "rollout: controls, clamp, goal, z/position stores"
-        if 783 <= l <= 800: return "chunk ranking"
-        if 881 <= l <= 942: return "phase-B glue + final reduction"
-        return "other (setup, barriers)"
-    return "intrinsics (" + f + ")"
+    if f not in ANCHORS:
+        return "intrinsics (" + f + ")"
+    if f not in _tables:
+        lines = (ROOT / f).read_text().splitlines()
+        marks = []
+        for sub, name in ANCHORS[f]:
+            for i, ln in enumerate(lines, 1):
+                if sub in ln:
+                    marks.append((i, name))
+                    break
+        _tables[f] = sorted(marks)
+    name = "other"
+    for i, nm in _tables[f]:
+        if i <= l:
+            name = nm
+    return name
 
 
 print(f"total warp instructions {tot[0]:.4g}, stall samples {tot[1]}")
