@@ -30,6 +30,9 @@ constexpr int kObsBuckets = 64;  // x-buckets of the obstacle culling table
 #define D4K_KPF 8
 #endif
 constexpr int kPF = D4K_KPF;  // rollout block depth (time steps): Philox draws in flight per thread
+#ifndef D4K_MINB16
+#define D4K_MINB16 3  // resident CTAs per SM the 16-robot-tile kernels are register-capped for
+#endif
 
 template <typename S>
 struct FitParams {
@@ -842,14 +845,16 @@ __device__ __noinline__ void rollout_check(const FitParams<float>& p, int kA, in
 }
 
 template <typename S, int KIND, int TB, int MAXW, int NOISE, bool PL = false>
-__global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? 3 : 5) k_rollout_fitness(const __grid_constant__ FitParams<S> p) {
+__global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? D4K_MINB16 : 5) k_rollout_fitness(const __grid_constant__ FitParams<S> p) {
   static_assert(!PL || (std::is_same<S, float>::value && ModelDims<KIND>::PD == 2 && MAXW == 2),
                 "pair-list path: fp32, planar kinds, Rp = 64");
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
   constexpr bool F32 = std::is_same<S, float>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int tid = threadIdx.x, nthreads = blockDim.x;
-  const int R = p.R, Rp = p.Rp, TC = p.TC, spc = p.spc, T = p.T;
+  // the pair-list instantiation has a fixed shape (Rp = TC = 64, 2 samples per
+  // 128-thread CTA): compile-time constants for all identity / index math
+  const int tid = threadIdx.x, nthreads = PL ? 128 : blockDim.x;
+  const int R = p.R, Rp = PL ? 64 : p.Rp, TC = PL ? 64 : p.TC, spc = PL ? 2 : p.spc, T = p.T;
 
   FitSmem<S> sm;
   sm.RS = Rp + 2;
