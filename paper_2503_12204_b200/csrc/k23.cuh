@@ -515,8 +515,8 @@ __device__ __forceinline__ void item_pl(const FitSmem<float>& sm, int s, int tc,
     if (t < 0.f) conf |= 3ull << (2 * l);
   }
   // pair-pair blocks (l, l + d mod 32), d = 1..16 (d = 16 once per pair):
-  // all 16 ballots first (independent loads and votes), then the blocks, two
-  // per iteration so their load → test chains overlap
+  // all 16 ballots first (independent loads and votes), then the blocks
+  // (pairing two blocks per iteration, or four, measured slower: code size)
   uint32_t lv[16];
 #pragma unroll
   for (int d = 1; d <= 16; ++d) {
@@ -533,14 +533,7 @@ __device__ __forceinline__ void item_pl(const FitSmem<float>& sm, int s, int tc,
     while (live) {
       const int l1 = __ffs(live) - 1;
       live &= live - 1u;
-      if (live) {
-        const int l2 = __ffs(live) - 1;
-        live &= live - 1u;
-        pl_block(X, Y, l1, (l1 + d) & 31, nm2, conf);
-        pl_block(X, Y, l2, (l2 + d) & 31, nm2, conf);
-      } else {
-        pl_block(X, Y, l1, (l1 + d) & 31, nm2, conf);
-      }
+      pl_block(X, Y, l1, (l1 + d) & 31, nm2, conf);
     }
   }
   // obstacles: pair boxes vs the obstacles' inflated boxes, eight ballots at a time
