@@ -866,7 +866,10 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? D4K_MINB16 : 5) k_r
   }
   if constexpr (F32 && PL) {
     sm.key = reinterpret_cast<int*>(sm.obs + 4 * (p.n_obs + 1));
-    sm.pbox = reinterpret_cast<float4*>((reinterpret_cast<uintptr_t>(sm.key + spc * Rp) + 15) & ~uintptr_t(15));
+    // plain pointer arithmetic on the shared base (an integer round trip would
+    // lose the address space: generic LD/ST instead of LDS/STS); key is 16-B
+    // aligned and spc·Rp = 128 ints, so pbox is too
+    sm.pbox = reinterpret_cast<float4*>(sm.key + spc * Rp);
     sm.opl = reinterpret_cast<float*>(sm.pbox + (size_t)spc * (TC / 32) * Rp);
     sm.bb = sm.ocl = nullptr;
     sm.goal = sm.inv = nullptr;
