@@ -10,6 +10,10 @@ extern "C" {
  * FFMA2 chains over all SMs, best of `reps`.  The roofline denominator for the
  * CUDA-core kernels (K2+K3), measured on the box that runs the bench. */
 int d4orm_cuda_fp32_peak(int device, int reps, double* tflops, double* sm_clock_mhz);
+/* Which fp32 fitness form K2+K3 runs for the context's problem: 1 = pair list
+ * (planar teams of 33..64 robots), 0 = robot tiles, -1 = no problem set. */
+struct d4orm_cuda_ctx;
+int d4orm_cuda_fitness_path(const struct d4orm_cuda_ctx* ctx);
 #ifdef __cplusplus
 }
 #endif

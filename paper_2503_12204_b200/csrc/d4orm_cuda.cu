@@ -1651,6 +1651,11 @@ int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_
   return D4ORM_OK;
 }
 
+int d4orm_cuda_fitness_path(const d4orm_cuda_ctx* ctx) {
+  if (!ctx || !ctx->has_problem) return -1;
+  return ctx->pl ? 1 : 0;
+}
+
 int d4orm_cuda_launches_per_step(const d4orm_cuda_ctx* ctx) {
   // K2+K3, K4, K5 partial, K5 tree (+ K1 on the fp64 path, + the root tree when sharded)
   return 4 + (ctx->precision == D4ORM_PREC_F64 ? 1 : 0) + (ctx->comm ? 1 : 0);

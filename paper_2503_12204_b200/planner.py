@@ -192,6 +192,10 @@ class GpuDenoiser:
     def launches_per_step(self) -> int:
         return self._L.d4orm_cuda_launches_per_step(self._h)
 
+    def fitness_path(self) -> int:
+        """fp32 fitness form for the current problem: 1 pair list, 0 tiles."""
+        return self._L.d4orm_cuda_fitness_path(self._h)
+
     # ---------------------------------------------------------- anytime loop
     def solve(self, cfg: DenoiserConfig, max_iterations: int = 10, stop_on_success: bool = True,
               deadline_seconds: float | None = None, on_iteration=None):

@@ -91,3 +91,44 @@ def test_culling_changes_nothing(gpu, oracle, case):
     for m, (rs, rc, rr, nc, no) in enumerate(ref):
         if (cnt1[m, 0], cnt1[m, 1]) != (nc, no):
             assert explain_flips(oracle, p, st1[m], cnt1[m, 0], cnt1[m, 1]), (case, m, cnt1[m], nc, no)
+
+
+def test_fitness_path_selection(gpu):
+    """Planar teams of 33..64 run the pair-list fitness, the rest the tiles."""
+    gpu.set_problem(S.baseline_config(5).problem.with_horizon(16))
+    assert gpu.fitness_path() == 1
+    gpu.set_problem(CASES["R40_huge_obstacle"])
+    assert gpu.fitness_path() == 1
+    gpu.set_problem(CASES["holo3d_64"])
+    assert gpu.fitness_path() == 0
+    gpu.set_problem(S.baseline_config(2).problem)
+    assert gpu.fitness_path() == 0
+
+
+@pytest.mark.parametrize("case", ["dense", "same_x_line", "R40_huge_obstacle"])
+def test_pair_list_matches_tiles(gpu, oracle, case):
+    """The pair-list fitness (direct-form tests) and the tile fitness
+    (expanded-form tests) see the same states; their counts differ only by
+    decisions inside the fp32 band, and both match the fp64 oracle up to
+    explained flips."""
+    from test_gpu_parity import controls_for, explain_flips
+    p = CASES[case]
+    u = controls_for(p, 16, 9, scale=1.0)
+    os.environ["D4ORM_PL"] = "0"
+    try:
+        gpu.set_problem(p)
+        assert gpu.fitness_path() == 0
+        st0, _, rw0, cnt0 = gpu.rollout_fitness(u)
+    finally:
+        os.environ.pop("D4ORM_PL", None)
+    gpu.set_problem(p)
+    assert gpu.fitness_path() == 1
+    st1, _, rw1, cnt1 = gpu.rollout_fitness(u)
+    np.testing.assert_array_equal(st1, st0)
+    unit = max(p.w_t, p.obstacle_weight) / (p.robots * p.horizon)
+    for m in range(u.shape[0]):
+        if (cnt1[m] != cnt0[m]).any():
+            assert explain_flips(oracle, p, st1[m], cnt1[m, 0], cnt1[m, 1]), (case, m, cnt1[m], cnt0[m])
+            assert explain_flips(oracle, p, st0[m], cnt0[m, 0], cnt0[m, 1]), (case, m, cnt1[m], cnt0[m])
+        flips = abs(int(cnt1[m, 0]) - int(cnt0[m, 0])) + abs(int(cnt1[m, 1]) - int(cnt0[m, 1]))
+        assert abs(rw1[m] - rw0[m]) <= 1e-5 + flips * unit, (case, m, rw1[m], rw0[m])
