@@ -610,6 +610,18 @@ int enqueue_fitness(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
 int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc) {
   d4k::WeightParams wp{ctx->rewards.p, rs.M, rs.lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p + 4 * sc.trace_off,
                        sc.trace_step, ctx->errw.p};
+  // M ≤ 8192 (C1, C2): one CTA, ≤ 8 rewards per thread, shared-memory folds
+  // (beyond that one SM's fp64 exp throughput loses to the cooperative grid)
+  if (rs.M <= 8LL * d4k::kWThreads) {
+    const int per = rs.M <= 1024 ? 1 : rs.M <= 2048 ? 2 : rs.M <= 4096 ? 4 : 8;
+    const void* fn = per == 1   ? (const void*)d4k::k_score_weights_cta<1>
+                     : per == 2 ? (const void*)d4k::k_score_weights_cta<2>
+                     : per == 4 ? (const void*)d4k::k_score_weights_cta<4>
+                                : (const void*)d4k::k_score_weights_cta<8>;
+    void* args1[] = {(void*)&wp};
+    CU(cudaLaunchKernel(fn, dim3(1), dim3(d4k::kWThreads), args1, 0, ctx->s_main));
+    return D4ORM_OK;
+  }
   // 2 rewards per thread (16 beyond 148·2048 samples) held in registers;
   // one CTA → plain launch, several → cooperative launch (grid.sync)
   const bool big = rs.M > 148LL * d4k::kWThreads * 2;
@@ -1619,8 +1631,16 @@ int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t
   CU(ctx->trace.ensure(4));
   CU(ctx->errw.ensure(1));
   CU(cudaMemcpyAsync(ctx->rewards.p, rewards, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->s_main));
-  d4k::WeightParams wp{ctx->rewards.p, m, lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p, 0, ctx->errw.p};
-  d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
+  CU(ctx->wscratch.ensure((size_t)6 * 160));
+  if (m <= 148LL * d4k::kWThreads * 16) {  // the denoising step's own K4 dispatch
+    RunShape rs;
+    rs.M = m;
+    rs.lambda = lambda;
+    if (int r = enqueue_weights(ctx, rs, StepConsts{})) return r;
+  } else {  // beyond one cooperative wave: the single-CTA loop over any M
+    d4k::WeightParams wp{ctx->rewards.p, m, lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p, 0, ctx->errw.p};
+    d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
+  }
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(ctx->s_main));
   CU(cudaMemcpy(weights, ctx->w64.p, sizeof(double) * m, cudaMemcpyDeviceToHost));

@@ -254,6 +254,135 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
   }
 }
 
+// Small batches (M ≤ 8192, C1 and C2): the same computation in ONE CTA of
+// 1024 threads, PER ≤ 8 rewards per thread in registers, folds through shared
+// memory — no cooperative launch, no grid barriers, no global scratch round
+// trips (C1 step 29.1 → 26.9 µs).  Fixed fold order (warp tree, then warp 0 over
+// the 32 warp partials): deterministic, identical on every rank.
+template <int N, int MAXMASK>
+__device__ __forceinline__ void cta_fold_n(double* v, double* sh) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    const bool mx = (MAXMASK >> i) & 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, v[i], o);
+      v[i] = mx ? fmax(v[i], u) : v[i] + u;
+    }
+    if (lane == 0) sh[i * 32 + wid] = v[i];
+  }
+  __syncthreads();
+  if (wid == 0) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const bool mx = (MAXMASK >> i) & 1;
+      double r = sh[i * 32 + lane];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double u = __shfl_xor_sync(0xffffffffu, r, o);
+        r = mx ? fmax(r, u) : r + u;
+      }
+      if (lane == 0) sh[96 + i] = r;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = sh[96 + i];
+  __syncthreads();
+}
+
+template <int PER>
+__global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const WeightParams p) {
+  __shared__ double sh[3 * 32 + 4];
+  const int tid = threadIdx.x;
+  double r[PER];
+  double s = 0.0, best = -INFINITY;
+  bool finite = true;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int64_t j = tid + (int64_t)q * kWThreads;
+    r[q] = j < p.M ? p.reward[j] : 0.0;
+  }
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (tid + (int64_t)q * kWThreads < p.M) {
+      finite = finite && isfinite(r[q]);
+      s += r[q];
+      best = fmax(best, r[q]);
+    }
+  }
+  double f3[3] = {finite ? 0.0 : 1.0, s, best};
+  cta_fold_n<3, 4>(f3, sh);
+  if (f3[0] != 0.0) {
+    if (tid == 0) atomicMin(p.err, 0xFFFFFFFFFFFFFFFEull);
+    return;
+  }
+  const double mean = f3[1] / (double)p.M;
+  best = f3[2];
+  double v = 0.0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (tid + (int64_t)q * kWThreads < p.M) {
+      const double d = r[q] - mean;
+      v += d * d;
+    }
+  }
+  double f1[1] = {v};
+  cta_fold_n<1, 0>(f1, sh);
+  const double std_dev = sqrt(f1[0] / (double)p.M);
+  if (std_dev < 1e-8) {  // degenerate batch → uniform (denoiser.cpp:74-77)
+    const double u = 1.0 / (double)p.M;
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+      const int64_t j = tid + (int64_t)q * kWThreads;
+      if (j < p.M) {
+        p.w64[j] = u;
+        p.w32[j] = (float)u;
+      }
+    }
+    if (tid == 0) {
+      p.trace[0] = p.step;
+      p.trace[1] = best;
+      p.trace[2] = mean;
+      p.trace[3] = -(double)p.M * u * log(u);
+    }
+    return;
+  }
+  const double inv = 1.0 / (std_dev * p.lambda);
+  const double max_scaled = (best - mean) * inv;
+  double sum = 0.0, es = 0.0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    if (tid + (int64_t)q * kWThreads < p.M) {
+      const double a = (r[q] - mean) * inv - max_scaled;  // shifted exponent
+      const double e = exp(a);
+      sum += e;
+      es += e * a;
+      r[q] = e;
+    }
+  }
+  double f2[2] = {sum, es};
+  cta_fold_n<2, 0>(f2, sh);
+  sum = f2[0];
+  const double rsum = 1.0 / sum;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    const int64_t j = tid + (int64_t)q * kWThreads;
+    if (j < p.M) {
+      const double w = r[q] * rsum;
+      p.w64[j] = w;
+      p.w32[j] = r[q] >= kW32Floor ? (float)w : 0.f;
+    }
+  }
+  if (tid == 0) {
+    p.trace[0] = p.step;
+    p.trace[1] = best;
+    p.trace[2] = mean;
+    p.trace[3] = log(sum) - f2[1] / sum;
+  }
+}
+
 // Single-CTA variant (kept for d4orm_cuda_score_weights on arbitrary M).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_score_weights(const WeightParams p) {

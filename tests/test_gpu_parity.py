@@ -136,7 +136,7 @@ def test_collisions_are_counted(gpu, oracle):
         assert abs(rw[0] - r) < 1e-6
 
 
-@pytest.mark.parametrize("m", [2, 3, 1000, 8192, 70001])
+@pytest.mark.parametrize("m", [2, 3, 1000, 8192, 16384, 70001, 400000])
 def test_score_weights(gpu, oracle, m):
     rng = np.random.default_rng(m)
     r = rng.normal(size=m) * 0.01 + 0.3
