@@ -33,6 +33,9 @@ constexpr int kPF = D4K_KPF;  // rollout block depth (time steps): Philox draws 
 #ifndef D4K_MINB16
 #define D4K_MINB16 3  // resident CTAs per SM the 16-robot-tile kernels are register-capped for
 #endif
+#ifndef D4K_MINB8
+#define D4K_MINB8 5   // ... and the small-tile (R <= 16) kernels
+#endif
 
 template <typename S>
 struct FitParams {
@@ -838,7 +841,7 @@ __device__ __noinline__ void rollout_check(const FitParams<float>& p, int kA, in
 }
 
 template <typename S, int KIND, int TB, int MAXW, int NOISE, bool PL = false>
-__global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? D4K_MINB16 : 5) k_rollout_fitness(const __grid_constant__ FitParams<S> p) {
+__global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? D4K_MINB16 : D4K_MINB8) k_rollout_fitness(const __grid_constant__ FitParams<S> p) {
   static_assert(!PL || (std::is_same<S, float>::value && ModelDims<KIND>::PD == 2 && MAXW == 2),
                 "pair-list path: fp32, planar kinds, Rp = 64");
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
