@@ -1,0 +1,114 @@
+"""C5 at its full BASELINE size (R = 64, T = 256, N = 262144 samples, 16
+obstacles) through size-independent properties — the oracle cannot run a full
+step in test time (≈ 2 min on 8 cores, 68.7 GB), so:
+
+  * K4 at full size equals the oracle's score_weights on the step's own rewards
+    (rel 1e-9), and the trace record is consistent with them;
+  * single samples picked across the whole batch (first, last, both shard
+    boundaries of an 8-way split) re-run on the host from their Philox noise
+    agree with the fp64 oracle (rewards 2e-5 + explained fp32-band flips);
+  * the step is deterministic, and the sharded protocol on a 1-rank NCCL
+    communicator gives bitwise the same variable, rewards and weights;
+  * a full 100-step run_denoising stays finite with entropies in [0, log N].
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import paper_2503_12204_b200 as d4
+from paper_2503_12204_b200 import scenarios as S
+
+pytestmark = pytest.mark.gpu
+
+RC = S.baseline_config(5)
+P = RC.problem
+M = RC.samples
+STEP = 100          # the first denoising step (largest sampling spread)
+SEED = 21
+
+
+def _variable():
+    rng = np.random.default_rng(5)
+    return 0.2 * rng.normal(size=(P.horizon, P.robots, P.du))
+
+
+@pytest.fixture(scope="module")
+def full_step():
+    g = d4.GpuDenoiser(P)
+    cfg = d4.DenoiserConfig(steps=RC.steps, batch=M, seed=SEED)
+    base = np.zeros((P.horizon, P.robots, P.du))
+    var = _variable()
+    v1, r1, w1, rec1 = g.denoise_step(base, var, STEP, cfg)
+    v2, r2, w2, rec2 = g.denoise_step(base, var, STEP, cfg)
+    yield g, cfg, base, var, (v1, r1, w1, rec1), (v2, r2, w2, rec2)
+    g.close()
+
+
+def test_full_size_step_is_deterministic(full_step):
+    _, _, _, _, a, b = full_step
+    for x, y in zip(a[:3], b[:3]):
+        np.testing.assert_array_equal(x, y)
+    assert a[3] == b[3]
+
+
+def test_full_size_weights_match_oracle(full_step, oracle):
+    _, cfg, _, _, (v, r, w, rec), _ = full_step
+    assert r.shape == (M,) and np.isfinite(r).all() and np.isfinite(v).all()
+    wo = oracle.score_weights(r, cfg.lam)
+    np.testing.assert_allclose(w, wo, rtol=1e-9, atol=1e-300)
+    assert abs(w.sum() - 1.0) < 1e-9 and (w >= 0).all()
+    step, best, mean, ent = rec
+    assert step == STEP and best == r.max() and abs(mean - r.mean()) < 1e-12
+    assert abs(ent - oracle.weight_entropy(wo)) < 1e-9 * max(1.0, abs(ent))
+    assert 0.0 <= ent <= np.log(M)
+
+
+@pytest.mark.parametrize("m", [0, 1, 32767, 32768, 131071, 131072, 262143])
+def test_full_size_samples_match_oracle(full_step, oracle, m):
+    """Sample m of the full-size step, rebuilt from its own Philox noise."""
+    from test_gpu_parity import explain_flips
+    g, cfg, base, var, (_, r, _, _), _ = full_step
+    ab = d4.make_schedule(cfg.steps, cfg.alpha_bar_final)
+    ms, sd = 1.0 / np.sqrt(ab[STEP]), np.sqrt(1.0 / ab[STEP] - 1.0)
+    z = g.philox_noise(cfg.seed, STEP, m, 1)[0].astype(np.float64).reshape(P.horizon, P.robots, P.du)
+    u = base + ms * var + sd * z
+    st_o, _ = oracle.rollout(P, u)
+    r_o, nc, no = oracle.total_reward(P, st_o)
+    g.set_options(d4.PREC_F32, d4.NOISE_HOST)
+    st_g, _, r_g, cnt = g.rollout_fitness(u[None])
+    g.set_options(d4.PREC_F32, d4.NOISE_PHILOX)
+    np.testing.assert_allclose(st_g[0], st_o, atol=2e-5, rtol=1e-5)
+    unit = max(P.w_t, P.obstacle_weight) / (P.robots * P.horizon)
+    flips = abs(int(cnt[0, 0]) - nc) + abs(int(cnt[0, 1]) - no)
+    if flips:
+        assert explain_flips(oracle, P, st_g[0], cnt[0, 0], cnt[0, 1]), (m, cnt[0], nc, no)
+    # the full-size step's reward for sample m and the oracle's, same noise
+    assert abs(r[m] - r_o) <= 2e-5 + (flips + 2) * unit, (m, r[m], r_o)
+
+
+def test_full_size_sharded_protocol_is_bitwise(full_step):
+    """The step through a 1-rank NCCL communicator (reward all-gather and the
+    chunk-tree root all-gather inside the step) at full size."""
+    from paper_2503_12204_b200._lib import lib
+    g, cfg, base, var, (v, r, w, rec), _ = full_step
+    buf = C.create_string_buffer(128)
+    assert lib().d4orm_cuda_nccl_id(buf) == 0
+    b = d4.GpuDenoiser(P, rank=0, world=1, nccl_id=bytes(buf.raw))
+    try:
+        vb, rb, wb, recb = b.denoise_step(base, var, STEP, cfg)
+    finally:
+        b.close()
+    np.testing.assert_array_equal(rb, r)
+    np.testing.assert_array_equal(wb, w)
+    np.testing.assert_array_equal(vb, v)
+    assert recb == rec
+
+
+def test_full_size_run_denoising(full_step):
+    g, cfg, base, _, _, _ = full_step
+    v, tr = g.run_denoising(base, cfg)
+    assert np.isfinite(v).all() and len(tr) == cfg.steps
+    assert [t[0] for t in tr] == list(range(cfg.steps, 0, -1))
+    for step, best, mean, ent in tr:
+        assert best >= mean and 0.0 <= ent <= np.log(M) + 1e-9
