@@ -1,6 +1,8 @@
-"""C5 at its full BASELINE size (R = 64, T = 256, N = 262144 samples, 16
-obstacles) through size-independent properties — the oracle cannot run a full
-step in test time (≈ 2 min on 8 cores, 68.7 GB), so:
+"""Every BASELINE config at its full size.  C1–C4: one denoising step against
+the oracle on the oracle's own noise (fp64 to 1e-9, fp32 within the band).
+C5 (R = 64, T = 256, N = 262144 samples, 16 obstacles) through size-independent
+properties — the oracle cannot run a full C5 step in test time (≈ 2 min on 8
+cores, 68.7 GB), so:
 
   * K4 at full size equals the oracle's score_weights on the step's own rewards
     (rel 1e-9), and the trace record is consistent with them;
@@ -112,3 +114,38 @@ def test_full_size_run_denoising(full_step):
     assert [t[0] for t in tr] == list(range(cfg.steps, 0, -1))
     for step, best, mean, ent in tr:
         assert best >= mean and 0.0 <= ent <= np.log(M) + 1e-9
+
+
+@pytest.mark.parametrize("cfg_index", [1, 2, 3, 4])
+@pytest.mark.parametrize("prec", [d4.PREC_F64, d4.PREC_F32])
+def test_full_size_teacher_forced_step_c1_c4(oracle, cfg_index, prec):
+    """C1–C4 are small enough for the oracle: one denoising step at the full
+    BASELINE shape (N, T, R, obstacles) with the oracle's own noise, GPU vs
+    oracle — fp64 to 1e-9, fp32 within the stated band."""
+    from oracle.oracle import make_config
+    rc = S.baseline_config(cfg_index)
+    p, M, N, i = rc.problem, rc.samples, rc.steps, 63
+    cfg = d4.DenoiserConfig(steps=N, batch=M, seed=17)
+    ocfg = make_config(N, M, seed=17)
+    ab, _ = oracle.make_schedule(N, 0.05)
+    rng = np.random.default_rng(cfg_index)
+    base = 0.3 * rng.normal(size=(p.horizon, p.robots, p.du))
+    var = 0.2 * rng.normal(size=base.shape)
+    noise = oracle.step_noise(17, i, 0, M, p.elems)
+    g = d4.GpuDenoiser(p, precision=prec, noise=d4.NOISE_HOST)
+    try:
+        v_g, r_g, w_g, rec_g = g.denoise_step(base, var, i, cfg, noise)
+    finally:
+        g.close()
+    v_o, r_o, w_o, rec_o = oracle.denoise_step(p, base, var, ab, ocfg, i, noise)
+    assert rec_g[0] == i
+    if prec == d4.PREC_F64:
+        np.testing.assert_allclose(r_g, r_o, atol=1e-12)
+        np.testing.assert_allclose(w_g, w_o, rtol=1e-8, atol=1e-300)
+        np.testing.assert_allclose(v_g, v_o, rtol=1e-9, atol=1e-12)
+    else:
+        unit = max(p.w_t, p.obstacle_weight) / (p.robots * p.horizon)
+        dr = np.abs(r_g - r_o)
+        assert (dr <= 2e-5 + 4 * unit).all(), dr.max()
+        assert (dr <= 2e-5).mean() > 0.95
+        np.testing.assert_allclose(v_g, v_o, atol=2e-3 * np.abs(v_o).max())
