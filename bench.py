@@ -290,7 +290,10 @@ def main():
         "roofline": {"kernel": "k_rollout_fitness (K2+K3)", "bound": "fp32", "achieved": achieved, "peak": peak_tf.value,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf.value if peak_tf.value else None,
                      "traffic": traffic, "flops_per_eval": F, "evals_per_launch": Ml, "launch_ms": k23_ms,
-                     "peak_source": "measured live: d4orm_cuda_fp32_peak (FFMA2 over all SMs); MEASURED_PEAKS.json has no FP32 figure"},
+                     "peak_source": "measured live: d4orm_cuda_fp32_peak (FFMA2 over all SMs); MEASURED_PEAKS.json has no FP32 figure",
+                     "note": "achieved = SURVEY 8d algorithmic FLOPs (every unordered pair and robot-obstacle test counted) / "
+                             "launch time; the kernel culls tests exactly, so the executed FMA-pipe utilisation is lower "
+                             "(ncu, profiles/r01_ncu_k23_c5_v15.md)"},
         "kernel_ms": {"K1_philox": kms[0], "K2K3_rollout_fitness": kms[1], "K4_weights": kms[2],
                       "K5_wmean_partial": kms[3], "K5_tree_update": kms[4]},
         "k5_hbm": {"kernel": "k_wmean_partial (K5a)", "bound": "hbm",
