@@ -191,6 +191,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--graphs", type=int, default=1)
+    ap.add_argument("--force-comm", action="store_true",
+                    help="N = 1 through the sharded protocol (1-rank NCCL communicator): exercises the N > 1 path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -208,6 +210,10 @@ def main():
     from paper_2503_12204_b200._lib import lib
     dist = dist_setup(world) if world > 1 else None
     nccl_id = None
+    if world == 1 and args.force_comm:
+        buf = C.create_string_buffer(128)
+        assert lib().d4orm_cuda_nccl_id(buf) == 0, "ncclGetUniqueId failed"
+        nccl_id = bytes(buf.raw)
     if world > 1:
         buf = C.create_string_buffer(128)
         obj = [None]

@@ -311,6 +311,33 @@ def test_nccl_protocol_on_one_rank():
     b.close()
 
 
+def test_nccl_protocol_solve_and_baselines_on_one_rank():
+    """solve / MPPI / CEM (the bench's solve leg and the sharded baselines) on a
+    1-rank NCCL communicator: bitwise the single-GPU results."""
+    import ctypes as C
+    from paper_2503_12204_b200._lib import lib
+    p = CASES["C2"]()
+    buf = C.create_string_buffer(128)
+    assert lib().d4orm_cuda_nccl_id(buf) == 0
+    a = d4.GpuDenoiser(p)
+    b = d4.GpuDenoiser(p, rank=0, world=1, nccl_id=bytes(buf.raw))
+    try:
+        cfg = d4.DenoiserConfig(steps=6, batch=1024, seed=5)
+        ra = a.solve(cfg, max_iterations=3, stop_on_success=False)
+        rb = b.solve(cfg, max_iterations=3, stop_on_success=False)
+        assert [x[:3] for x in ra.per_iteration] == [x[:3] for x in rb.per_iteration]
+        np.testing.assert_array_equal(ra.best_states, rb.best_states)
+        assert ra.traces == rb.traces
+        for fn in ("mppi_solve", "cem_solve"):
+            xa = getattr(a, fn)(batch=1024, iterations=4, seed=3, stop_on_success=False)
+            xb = getattr(b, fn)(batch=1024, iterations=4, seed=3, stop_on_success=False)
+            assert [x[:3] for x in xa.per_iteration] == [x[:3] for x in xb.per_iteration], fn
+            np.testing.assert_array_equal(xa.best_controls, xb.best_controls)
+    finally:
+        a.close()
+        b.close()
+
+
 def test_philox_noise_matches_cpu_model(gpu):
     """K1 / the fused draw against the numpy model (tests/philox_model.py,
     itself pinned to the Philox4x32-10 known-answer vectors): the integer stream
