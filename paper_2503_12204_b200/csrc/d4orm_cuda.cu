@@ -598,6 +598,9 @@ int enqueue_fitness(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
   f.step = sc.key_i;
   f.z_store = (S*)ctx->z[0].p;
   f.sdv = (const S*)sc.sdv;
+  // z small enough to stay in L2 for K5a (C1–C4): keep it there; else stream it
+  f.z_keep = (double)rs.Ml * rs.E * sizeof(S) <= 256.0 * (1 << 20) ? 1 : 0;
+  if (const char* e = std::getenv("D4ORM_ZKEEP")) f.z_keep = std::atoi(e);
   CU(launch_fit<S>(ctx, f, smem, fused));
   if (timing) CU(cudaEventRecord(ctx->ev_k[1], ctx->s_main));
   if (ctx->comm) {

@@ -53,6 +53,8 @@ struct FitParams {
   S cull_margin;         // fp32: separation (m) beyond which a pair cannot be in conflict, with rounding slack
   int cull;              // fp32: rank robots by x per chunk and cull tile pairs / obstacles (≥ 3 tiles)
   const float* obs_pl;   // fp32 pair-list path: [O][8] (cx, cy, −L²↑, 0, box lo.x, lo.y, hi.x, hi.y)
+  int z_keep;            // fused noise: z stores with an L2 evict_last hint (z fits in L2: K5a reads it
+                         // there) instead of evict_first (z ≫ L2: stream it out)
   int n_obs;
   S lower[3], upper[3];
   S dt, half_dt, dt6;
@@ -696,14 +698,20 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
     nz[4 * g + 3] = v.w;
   }
 #ifndef D4K_EXPERIMENT_NO_ZSTORE
+  uint64_t zpol;  // L2 policy of the z stores (FitParams::z_keep)
+  if (p.z_keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(zpol));
+  else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(zpol));
 #pragma unroll
   for (int j = 0; j < kPF; ++j) {
     if (FULL || j < nb) {
       if constexpr (DU == 2) {
-        __stcs(reinterpret_cast<float2*>(zp + j * RDU), make_float2(nz[2 * j], nz[2 * j + 1]));
+        asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(zp + j * RDU), "f"(nz[2 * j]),
+                     "f"(nz[2 * j + 1]), "l"(zpol) : "memory");
       } else {
 #pragma unroll
-        for (int d = 0; d < DU; ++d) __stcs(zp + j * RDU + d, nz[j * DU + d]);
+        for (int d = 0; d < DU; ++d)
+          asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(zp + j * RDU + d), "f"(nz[j * DU + d]),
+                       "l"(zpol) : "memory");
       }
     }
   }
