@@ -1,8 +1,9 @@
 """Edge shapes for the fused rollout+fitness kernel: a single robot, two
 robots, a long horizon cut into ragged chunks, horizons shorter than a chunk,
-batches that leave a CTA partly empty, and a 100-robot team (Rp 112: items
-shared by two threads, 8 flag words, culling across 7 tiles) — fp64 against the
-oracle to 1e-12, fp32 to the fp32 band, and culling on == off."""
+batches that leave a CTA partly empty, a 100-robot team (Rp 112: items
+shared by two threads, 8 flag words, culling across 7 tiles), and pair-list
+teams (33..64 robots: padding, ragged windows, a dead sample slot) — fp64
+against the oracle to 1e-12, fp32 to the fp32 band, and culling on == off."""
 import os
 
 import numpy as np
@@ -33,6 +34,11 @@ SHAPES = {
     "R17_T9_M5": (17, 9, 5, S.HOLO3D_VEL, 3),
     "R100_T20_M6": (100, 20, 6, S.HOLO2D_VEL, 5),
     "R100_T70_M3_diffdrive": (100, 70, 3, S.DIFFDRIVE, 0),
+    # pair-list fitness (planar, 33..64 robots): odd team padded to 64, ragged
+    # chunks (T = 70: a partial window and an empty one), a dead sample slot
+    "R33_T70_M5_pairlist": (33, 70, 5, S.HOLO2D_VEL, 4),
+    "R64_T33_M3_pairlist": (64, 33, 3, S.HOLO2D_VEL, 6),
+    "R49_T40_M7_pairlist_unicycle": (49, 40, 7, S.UNICYCLE, 3),
 }
 
 
