@@ -154,7 +154,11 @@ def config_json(rc, world: int) -> dict:
     return {"workload": rc.name, "model": p.name, "robots": p.robots, "horizon": p.horizon, "samples_per_step": rc.samples,
             "denoising_steps": rc.steps, "iterations": rc.iterations, "obstacles": int(len(p.obs_radii)),
             "global_batch": rc.samples, "seq_len": p.horizon, "parallelism": f"samples-sharded x{world}",
-            "l2": "inputs larger than L2 (per-step noise buffer > 126 MB)"}
+            "l2": "no flush needed: every step draws fresh noise (Philox keyed by step), so no step re-reads inputs "
+                  "a previous step left in L2 except the %d KB base/variable; per-step chunk partials %.0f MB "
+                  "(+ z rows %.0f MB when stored) vs 126 MB L2" % (p.elems * 4 // 1024,
+                                                                 (rc.samples // world + 255) // 256 * p.elems * 4 / 1e6,
+                                                                 rc.samples // world * p.elems * 4 / 1e6)}
 
 
 def run_reference_arm(args, rc, rank: int, world: int):
@@ -289,6 +293,21 @@ def main():
     k5_alg = Ml * E * 4 + Ml * 4 + parts
     k5_nz = float(kms[5])
     k5_read = int(k5_nz * E * 4) + Ml * 4 + parts
+    if g.k5_regen() == 1:
+        # K5a regenerates the Philox normals of the samples that keep a weight
+        # (no z rows in HBM): instruction-issue bound, reported as normals/s
+        k5_info = {"kernel": "k_wmean_regen (K5a)", "bound": "issue (Philox4x32-10 + Box-Muller per normal)",
+                   "normals_per_launch": int(k5_nz * E), "samples_with_weight": k5_nz, "samples": Ml,
+                   "gnormals_per_s": k5_nz * E / (kms[3] * 1e-3) / 1e9 if kms[3] > 0 else None,
+                   "note": "z is not stored by K2+K3 nor read here; see DESIGN.md 3 (K5a) for the stored-vs-regenerated A/B"}
+    else:
+        k5_info = {"kernel": "k_wmean_partial (K5a)", "bound": "hbm",
+                   "achieved_gbs": k5_read / (kms[3] * 1e-3) / 1e9 if kms[3] > 0 else None,
+                   "peak_gbs": _hbm_peak(), "frac": (k5_read / (kms[3] * 1e-3) / 1e9) / _hbm_peak() if kms[3] > 0 else None,
+                   "bytes_moved_per_launch": k5_read, "samples_with_weight": k5_nz, "samples": Ml,
+                   "algorithmic_bytes_per_launch": k5_alg,
+                   "note": "bytes moved = z rows of samples with non-zero fp32 weight + weights + chunk partials; "
+                           "rows of zero-weight samples are skipped, so the algorithmic all-rows count over-states the rate"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -302,13 +321,7 @@ def main():
                              "(ncu, profiles/r01_ncu_k23_c5_v15.md)"},
         "kernel_ms": {"K1_philox": kms[0], "K2K3_rollout_fitness": kms[1], "K4_weights": kms[2],
                       "K5_wmean_partial": kms[3], "K5_tree_update": kms[4]},
-        "k5_hbm": {"kernel": "k_wmean_partial (K5a)", "bound": "hbm",
-                   "achieved_gbs": k5_read / (kms[3] * 1e-3) / 1e9 if kms[3] > 0 else None,
-                   "peak_gbs": _hbm_peak(), "frac": (k5_read / (kms[3] * 1e-3) / 1e9) / _hbm_peak() if kms[3] > 0 else None,
-                   "bytes_moved_per_launch": k5_read, "samples_with_weight": k5_nz, "samples": Ml,
-                   "algorithmic_bytes_per_launch": k5_alg,
-                   "note": "bytes moved = z rows of samples with non-zero fp32 weight + weights + chunk partials; "
-                           "rows of zero-weight samples are skipped, so the algorithmic all-rows count over-states the rate"},
+        "k5": k5_info,
         "gpu_launches": args.steps * g.launches_per_step(),
         "clocks": clk.summary(),
     }

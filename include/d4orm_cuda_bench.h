@@ -14,6 +14,10 @@ int d4orm_cuda_fp32_peak(int device, int reps, double* tflops, double* sm_clock_
  * (planar teams of 33..64 robots), 0 = robot tiles, -1 = no problem set. */
 struct d4orm_cuda_ctx;
 int d4orm_cuda_fitness_path(const struct d4orm_cuda_ctx* ctx);
+/* How the context's last run formed the weighted mean (K5a): 1 = regenerated
+ * the Philox noise (no z rows stored, k_wmean_regen), 0 = read the z rows
+ * K2+K3 stored, -1 = no run yet. */
+int d4orm_cuda_k5_regen(const struct d4orm_cuda_ctx* ctx);
 #ifdef __cplusplus
 }
 #endif

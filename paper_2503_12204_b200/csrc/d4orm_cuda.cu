@@ -126,6 +126,9 @@ struct d4orm_cuda_ctx {
 
   // problem (host copies)
   bool has_problem = false;
+  bool regen_ok = false;  // this run's Philox steps regenerate the noise in K5a (no z rows; ensure_buffers)
+  bool k5_regen = false;  // this step's K5a regenerates the noise (set by enqueue_fitness)
+  bool ran = false;       // ensure_buffers ran (a run was set up)
   d4orm_problem prob{};
   std::vector<double> starts, goals, obs_c, obs_r;
   int TB = 16, Rp = 16, MAXW = 2, spc = 16, TC = 16;
@@ -486,9 +489,17 @@ int check_config(d4orm_cuda_ctx* ctx, const d4orm_denoiser_config* c, RunShape* 
 
 size_t ssize(const d4orm_cuda_ctx* c) { return c->precision == D4ORM_PREC_F64 ? sizeof(double) : sizeof(float); }
 
-int ensure_buffers(d4orm_cuda_ctx* ctx, const RunShape& rs, bool two_z) {
+bool regen_wanted(const d4orm_cuda_ctx* ctx, const RunShape& rs);
+
+// philox_sc: the run draws Philox noise with a scalar std (denoiser, MPPI):
+// when K5a regenerates it there are no z rows, only one row for the
+// FromScratch initial variable (34 GB less at C5 on one GPU).
+int ensure_buffers(d4orm_cuda_ctx* ctx, const RunShape& rs, bool two_z, bool philox_sc = false) {
   const size_t S = ssize(ctx);
-  CU(ctx->z[0].ensure((size_t)rs.Ml * rs.E * S));
+  const bool rows = !(philox_sc && ctx->precision == D4ORM_PREC_F32 && rs.E % 4 == 0 && regen_wanted(ctx, rs));
+  ctx->regen_ok = !rows;  // decided once per run: enqueue_fitness stores z rows iff they exist
+  ctx->ran = true;
+  CU(ctx->z[0].ensure((size_t)(rows ? rs.Ml : 1) * rs.E * S));
   if (two_z) CU(ctx->z[1].ensure((size_t)rs.Ml * rs.E * S));
   CU(ctx->base.ensure((size_t)rs.E * S));
   CU(ctx->msv.ensure((size_t)rs.E * S));
@@ -581,6 +592,19 @@ StepConsts denoise_consts(const d4orm_cuda_ctx* ctx, const RunShape& rs, int i) 
   return c;
 }
 
+// K5a regenerates the Philox normals (k_wmean_regen) instead of reading the z
+// rows K2+K3 stores: decided per problem (knob D4ORM_K5REGEN=0/1).
+// Measured on the B200 (profiles/r01_k5regen.md, ms per step stored → regen):
+// C5 23.09 → 22.98 (K2+K3 −1.04 ms of z stores, K5a +0.90 ms: Philox + Box-
+// Muller for the ~60 % of samples that keep a weight is issue-bound at ≈3 ms,
+// reading their z is HBM-bound at 2.3 ms) and 34 GB less HBM; C4 (du = 3: three
+// scalar z stores per robot-step) 0.1667 → 0.1601; C1–C3 lose 2–10 µs (their
+// z stays in L2 for K5a), so they keep the stored rows.
+bool regen_wanted(const d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  if (const char* e = std::getenv("D4ORM_K5REGEN")) return std::atoi(e) != 0;
+  return rs.E >= kPartLargeE || ctx->prob.du == 3;
+}
+
 // K2+K3 (+ K1 on the fp64 Philox path) and the reward all-gather.
 template <typename S>
 int enqueue_fitness(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc, bool philox, bool timing) {
@@ -600,7 +624,12 @@ int enqueue_fitness(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
   f.sdv = (const S*)sc.sdv;
   // z small enough to stay in L2 for K5a (C1–C4): keep it there; else stream it
   f.z_keep = (double)rs.Ml * rs.E * sizeof(S) <= 256.0 * (1 << 20) ? 1 : 0;
-  if (const char* e = std::getenv("D4ORM_ZKEEP")) f.z_keep = std::atoi(e);
+  if (const char* e = std::getenv("D4ORM_ZKEEP")) f.z_keep = std::atoi(e) ? 1 : 0;
+  // K5a regenerates the normals instead of reading z back: no z stores at all
+  // (E % 4 == 0: the stored path's fused float4 walk, which regen equals
+  // bitwise; decided with the buffers, ensure_buffers)
+  ctx->k5_regen = fused && sc.sdv == nullptr && ctx->regen_ok;
+  if (ctx->k5_regen) f.z_keep = 2;
   CU(launch_fit<S>(ctx, f, smem, fused));
   if (timing) CU(cudaEventRecord(ctx->ev_k[1], ctx->s_main));
   if (ctx->comm) {
@@ -669,8 +698,25 @@ int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc
         d4k::k_wmean_partial<S, float, SUB, 0><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w32.p + rs.m0);
     }
   };
-  if (rs.E >= kPartLargeE) partial(std::integral_constant<int, 1>{});
-  else partial(std::integral_constant<int, 16>{});
+  auto regen = [&](auto sub_tag) {
+    constexpr int SUB = decltype(sub_tag)::value;
+    const int G = (ctx->prob.horizon * ctx->prob.du + 3) / 4;  // Philox groups per robot
+    const unsigned gx = (unsigned)(((int64_t)ctx->prob.robots * G + 256 / SUB - 1) / (256 / SUB));
+    d4k::RegenArgs ra{(const float*)ctx->msv.p, (float)sc.sd, rs.Ml, rs.m0, rs.E, ctx->prob.robots,
+                      ctx->prob.horizon, ctx->prob.du, ctx->keys.p, sc.key_i, (float*)ctx->partial.p};
+    d4k::k_wmean_regen<SUB><<<dim3(gx, (unsigned)rs.chunks_local), 256, 0, ctx->s_main>>>(ra, ctx->w32.p + rs.m0);
+  };
+  // (the flag is set by this step's enqueue_fitness: fp32, Philox, scalar std)
+  const bool use_regen = !f64 && dev_mode == 0 && ctx->k5_regen;
+  ctx->k5_regen = false;
+  if (use_regen) {
+    if (rs.E >= kPartLargeE) regen(std::integral_constant<int, 1>{});
+    else regen(std::integral_constant<int, 16>{});
+  } else if (rs.E >= kPartLargeE) {
+    partial(std::integral_constant<int, 1>{});
+  } else {
+    partial(std::integral_constant<int, 16>{});
+  }
   CU(cudaGetLastError());
   if (timing) CU(cudaEventRecord(ctx->ev_k[3], ctx->s_main));
   const unsigned tgrid = (unsigned)((rs.E + d4k::kThreads - 1) / d4k::kThreads);
@@ -851,7 +897,7 @@ int run_denoising_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoise
   RunShape rs;
   if (int r = check_config(ctx, c, &rs)) return r;
   const bool philox = ctx->noise_source == D4ORM_NOISE_PHILOX;
-  if (int r = ensure_buffers(ctx, rs, false)) return r;
+  if (int r = ensure_buffers(ctx, rs, false, philox)) return r;
   if (int r = prologue<S>(ctx, rs, base, c, philox)) return r;
   if (philox && ctx->use_graphs) {
     if (int r = ensure_graphs<S>(ctx, rs)) return r;
@@ -1009,7 +1055,7 @@ int solve_t(d4orm_cuda_ctx* ctx, const d4orm_solve_config* sc, double* best_stat
   const bool philox = ctx->noise_source == D4ORM_NOISE_PHILOX;
   if (!philox && !ctx->noise_fn)
     return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: host noise selected but no noise fn set");
-  if (int r = ensure_buffers(ctx, rs, false)) return r;
+  if (int r = ensure_buffers(ctx, rs, false, philox)) return r;
   const d4orm_problem& p = ctx->prob;
   const SolveLayout L = solve_layout(p, sc->max_iterations);
   CU(ctx->sv.ensure(L.total));
@@ -1213,7 +1259,7 @@ int baseline_solve_t(d4orm_cuda_ctx* ctx, BaselineSpec b, double* best_states, d
   const bool philox = ctx->noise_source == D4ORM_NOISE_PHILOX;
   if (!philox && !ctx->noise_fn)
     return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: host noise selected but no noise fn set");
-  if (int r = ensure_buffers(ctx, rs, false)) return r;
+  if (int r = ensure_buffers(ctx, rs, false, philox && !b.cem)) return r;
   const SolveLayout L = solve_layout(p, b.iterations);
   CU(ctx->sv.ensure(L.total));
   CU(ctx->sst.ensure(sizeof(d4k::SolveState)));
@@ -1506,7 +1552,7 @@ int denoise_step_t(d4orm_cuda_ctx* ctx, const double* base, const double* var_in
   if (int r = check_config(ctx, c, &rs)) return r;
   if (i < 1 || i > rs.N)
     return fail(ctx, D4ORM_E_INVALID, "denoise_step: step index %d outside 1..%d", i, rs.N);
-  if (int r = ensure_buffers(ctx, rs, false)) return r;
+  if (int r = ensure_buffers(ctx, rs, false, noise == nullptr && ctx->noise_source == D4ORM_NOISE_PHILOX)) return r;
   const int64_t E = rs.E;
   std::vector<double> b(E, 0.0);
   if (rs.mode == D4ORM_DEFORMATION) std::memcpy(b.data(), base, sizeof(double) * E);
@@ -1679,6 +1725,11 @@ int d4orm_cuda_fitness_path(const d4orm_cuda_ctx* ctx) {
   return ctx->pl ? 1 : 0;
 }
 
+int d4orm_cuda_k5_regen(const d4orm_cuda_ctx* ctx) {
+  if (!ctx || !ctx->ran) return -1;
+  return ctx->regen_ok ? 1 : 0;
+}
+
 int d4orm_cuda_launches_per_step(const d4orm_cuda_ctx* ctx) {
   // K2+K3, K4, K5 partial, K5 tree (+ K1 on the fp64 path, + the root tree when sharded)
   return 4 + (ctx->precision == D4ORM_PREC_F64 ? 1 : 0) + (ctx->comm ? 1 : 0);
@@ -1690,7 +1741,7 @@ int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config
   RunShape rs;
   if (int r = check_config(ctx, c, &rs)) return r;
   if (ctx->noise_source != D4ORM_NOISE_PHILOX) return fail(ctx, D4ORM_E_INVALID, "bench requires Philox noise");
-  if (int r = ensure_buffers(ctx, rs, false)) return r;
+  if (int r = ensure_buffers(ctx, rs, false, true)) return r;
   if (int r = prologue<S>(ctx, rs, base, c, true)) return r;
   if (ctx->use_graphs) {
     if (int r = ensure_graphs<S>(ctx, rs)) return r;

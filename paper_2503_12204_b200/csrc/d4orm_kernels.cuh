@@ -654,6 +654,117 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
   }
 }
 
+// K5a, regenerating variant (fp32, Philox noise).  A sample's noise is a pure
+// function of (key, m, k, n) (the counter mapping above), so instead of reading
+// back the z rows K2+K3 would have stored, the weighted mean draws the normals
+// again for the samples that keep a weight: K2+K3 skips its z stores
+// (FitParams::z_keep == 2) and no z buffer is round-tripped through HBM.
+// Thread = one Philox group (robot k, normals n = 4g..4g+3 of its stream, i.e.
+// the elements ((n/du)·R + k)·du + n%du) × one sub-range of the 256-sample
+// chunk.  The chunk's non-zero weights are compacted in ascending m first; every
+// per-element sum is the same ascending-m fmaf chain, and the sub-range split /
+// pairwise tree are k_wmean_partial's (SUB = 1 for large E, 16 for small E), so
+// the partials equal the stored-z path's bit for bit (a zero weight adds an
+// exact 0 there).
+struct RegenArgs {
+  const float* msv;  // [E] mean-scaled variable (sample = msv + sd·z)
+  float sd;
+  int64_t M, m_global0, elems;
+  int R, T, du;
+  const uint2* keys;
+  int step;
+  float* partial;  // [chunks][E]
+};
+
+template <int SUB>
+__global__ void __launch_bounds__(256) k_wmean_regen(const RegenArgs a, const float* __restrict__ w) {
+  constexpr int GROUPS = 256 / SUB, LANES = 256 / SUB;
+  __shared__ float red[SUB][GROUPS][4];
+  __shared__ int s_idx[256];
+  __shared__ float s_w[256];
+  __shared__ int s_pos[257];
+  __shared__ int s_cnt[8];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int64_t c = blockIdx.y, mc = c * 256;
+  // compaction: s_pos[i] = non-zero weights before sample i of the chunk
+  {
+    const int64_t m = mc + tid;
+    const float wm = m < a.M ? w[m] : 0.f;
+    const bool nz = wm != 0.f;
+    const unsigned bal = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) s_cnt[wid] = __popc(bal);
+    __syncthreads();
+    int off = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      off += i < wid ? s_cnt[i] : 0;
+      tot += s_cnt[i];
+    }
+    const int pos = off + __popc(bal & ((1u << lane) - 1u));
+    s_pos[tid] = pos;
+    if (nz) {
+      s_idx[pos] = tid;
+      s_w[pos] = wm;
+    }
+    if (tid == 0) s_pos[256] = tot;
+    __syncthreads();
+  }
+  const int g = tid % GROUPS, sr = tid / GROUPS;
+  const int G = (a.T * a.du + 3) >> 2;  // Philox groups per robot
+  const int gi = blockIdx.x * GROUPS + g;
+  const int k = gi / G, gg = gi - k * G;
+  const int nmax = a.T * a.du;
+  int64_t e[4];
+  float mv[4] = {0.f, 0.f, 0.f, 0.f};
+  bool ok[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int n = 4 * gg + j;
+    ok[j] = k < a.R && n < nmax;
+    const int t = n / a.du, d = n - t * a.du;
+    e[j] = ((int64_t)t * a.R + k) * a.du + d;
+    if (ok[j]) mv[j] = a.msv[e[j]];
+  }
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (k < a.R) {
+    const uint2 key = a.keys[a.step];
+    const float sd = a.sd;
+    const int q0 = s_pos[sr * LANES], q1 = s_pos[(sr + 1) * LANES];
+    const uint64_t mg = (uint64_t)(a.m_global0 + mc);
+#pragma unroll 2
+    for (int q = q0; q < q1; ++q) {
+      const float wm = s_w[q];
+      const float4 v = philox_normals(key, mg + (uint64_t)s_idx[q], (uint32_t)k, (uint32_t)gg);
+      acc[0] = fmaf(wm, fmaf(sd, v.x, mv[0]), acc[0]);
+      acc[1] = fmaf(wm, fmaf(sd, v.y, mv[1]), acc[1]);
+      acc[2] = fmaf(wm, fmaf(sd, v.z, mv[2]), acc[2]);
+      acc[3] = fmaf(wm, fmaf(sd, v.w, mv[3]), acc[3]);
+    }
+  }
+  if constexpr (SUB > 1) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[sr][g][j] = acc[j];
+    __syncthreads();
+#pragma unroll
+    for (int s = 1; s < SUB; s <<= 1) {  // k_wmean_partial's pairwise order
+      if ((sr & (2 * s - 1)) == 0) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) red[sr][g][j] = red[sr][g][j] + red[sr + s][g][j];
+      }
+      __syncthreads();
+    }
+    if (sr == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = red[0][g][j];
+    }
+  }
+  if (sr == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (ok[j]) a.partial[c * a.elems + e[j]] = acc[j];
+  }
+}
+
 // What the tree does with the total of each element.
 enum { FIN_UPDATE = 0, FIN_CEM_MEAN = 1, FIN_CEM_VAR = 2 };
 template <typename S>

@@ -53,8 +53,9 @@ struct FitParams {
   S cull_margin;         // fp32: separation (m) beyond which a pair cannot be in conflict, with rounding slack
   int cull;              // fp32: rank robots by x per chunk and cull tile pairs / obstacles (≥ 3 tiles)
   const float* obs_pl;   // fp32 pair-list path: [O][8] (cx, cy, −L²↑, 0, box lo.x, lo.y, hi.x, hi.y)
-  int z_keep;            // fused noise: z stores with an L2 evict_last hint (z fits in L2: K5a reads it
-                         // there) instead of evict_first (z ≫ L2: stream it out)
+  int z_keep;            // fused noise: z stores with an L2 evict_last hint (1: z fits in L2, K5a reads
+                         // it there) or evict_first (0: z ≫ L2, stream it out); 2: no z stores at all
+                         // (K5a regenerates the normals, k_wmean_regen)
   int n_obs;
   S lower[3], upper[3];
   S dt, half_dt, dt6;
@@ -699,10 +700,11 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
   }
 #ifndef D4K_EXPERIMENT_NO_ZSTORE
   uint64_t zpol;  // L2 policy of the z stores (FitParams::z_keep)
-  if (p.z_keep) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(zpol));
+  if (p.z_keep == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(zpol));
   else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(zpol));
 #pragma unroll
   for (int j = 0; j < kPF; ++j) {
+    if (p.z_keep == 2) break;  // K5a regenerates the noise
     if (FULL || j < nb) {
       if constexpr (DU == 2) {
         asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(zp + j * RDU), "f"(nz[2 * j]),
@@ -834,8 +836,18 @@ __device__ __noinline__ void rollout_check(const FitParams<float>& p, int kA, in
     const int t = t0 + tc;
     const int64_t e = ((int64_t)t * p.R + kA) * DU;
     float u[DU];
-    for (int d = 0; d < DU; ++d)
-      u[d] = fminf(fmaxf(fmaf(p.sdv ? p.sdv[e + d] : p.sd, zrow[e + d], p.bm[e + d]), p.lower[d]), p.upper[d]);
+    for (int d = 0; d < DU; ++d) {
+      float zv;
+      if (p.z_keep == 2) {  // z not stored: the same Philox draw as the fused block
+        const int n = t * DU + d;
+        const float4 v = philox_normals(p.keys[p.step], (uint64_t)m, (uint32_t)kA, (uint32_t)(n >> 2));
+        const int l = n & 3;
+        zv = l == 0 ? v.x : l == 1 ? v.y : l == 2 ? v.z : v.w;
+      } else {
+        zv = zrow[e + d];
+      }
+      u[d] = fminf(fmaxf(fmaf(p.sdv ? p.sdv[e + d] : p.sd, zv, p.bm[e + d]), p.lower[d]), p.upper[d]);
+    }
     rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
     bool fin = true;
     for (int q = 0; q < DX; ++q) fin = fin && isfinite(x[q]);

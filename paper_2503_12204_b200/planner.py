@@ -192,6 +192,11 @@ class GpuDenoiser:
     def launches_per_step(self) -> int:
         return self._L.d4orm_cuda_launches_per_step(self._h)
 
+    def k5_regen(self) -> int:
+        """1: the last run's K5a regenerated the Philox noise (no z rows), 0: it
+        read the stored z rows, -1: no run yet."""
+        return self._L.d4orm_cuda_k5_regen(self._h)
+
     def fitness_path(self) -> int:
         """fp32 fitness form for the current problem: 1 pair list, 0 tiles."""
         return self._L.d4orm_cuda_fitness_path(self._h)
