@@ -318,7 +318,7 @@ def main():
                      "peak_source": "measured live: d4orm_cuda_fp32_peak (FFMA2 over all SMs); MEASURED_PEAKS.json has no FP32 figure",
                      "note": "achieved = SURVEY 8d algorithmic FLOPs (every unordered pair and robot-obstacle test counted) / "
                              "launch time; the kernel culls tests exactly, so the executed FMA-pipe utilisation is lower "
-                             "(ncu, profiles/r01_ncu_k23_c5_v15.md)"},
+                             "(ncu, profiles/r01_ncu_k23k5_c5_v17.md)"},
         "kernel_ms": {"K1_philox": kms[0], "K2K3_rollout_fitness": kms[1], "K4_weights": kms[2],
                       "K5_wmean_partial": kms[3], "K5_tree_update": kms[4]},
         "k5": k5_info,

@@ -211,8 +211,34 @@ __device__ __forceinline__ float2 box_muller(uint32_t a, uint32_t b) {
   return make_float2(lo_f(z), hi_f(z));
 }
 
+// Round keys of Philox::gen, precomputed once (a loop drawing many groups under
+// one key keeps them in registers instead of re-deriving the schedule per draw).
+struct PhiloxKeys {
+  uint2 rk[D4K_PHILOX_ROUNDS];
+  __device__ __forceinline__ explicit PhiloxKeys(uint2 k) {
+#pragma unroll
+    for (int r = 0; r < D4K_PHILOX_ROUNDS; ++r) {
+      rk[r] = k;
+      k.x += 0x9E3779B9u;
+      k.y += 0xBB67AE85u;
+    }
+  }
+  __device__ __forceinline__ uint4 gen(uint4 c) const {
+#pragma unroll
+    for (int r = 0; r < D4K_PHILOX_ROUNDS; ++r) c = Philox::round(c, rk[r]);
+    return c;
+  }
+};
+
 __device__ __forceinline__ float4 philox_normals(uint2 key, uint64_t m, uint32_t k, uint32_t g) {
   const uint4 r = Philox::gen(make_uint4(g, (uint32_t)m, (uint32_t)(m >> 32), k), key);
+  const float2 a = box_muller(r.x, r.y), b = box_muller(r.z, r.w);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+// philox_normals with a precomputed key schedule (same numbers)
+__device__ __forceinline__ float4 philox_normals(const PhiloxKeys& ks, uint64_t m, uint32_t k, uint32_t g) {
+  const uint4 r = ks.gen(make_uint4(g, (uint32_t)m, (uint32_t)(m >> 32), k));
   const float2 a = box_muller(r.x, r.y), b = box_muller(r.z, r.w);
   return make_float4(a.x, a.y, b.x, b.y);
 }

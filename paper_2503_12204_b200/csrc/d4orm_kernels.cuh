@@ -4,6 +4,7 @@
 //   K2+K3 k_rollout_fitness  fused rollout + team fitness → reward[m]   (k23.cuh)
 //   K4    k_score_weights    z-scored softmax weights (fp64), entropy, best/mean
 //   K5    k_wmean_partial    streaming weighted mean over [chunk of m] × E
+//         k_wmean_regen      the same partials, the noise regenerated (no z rows)
 //         k_wmean_tree       deterministic pairwise tree over chunk partials +
 //                            the update var ← √ᾱ_{i−1} · Σ_m w_m sample_m
 //
@@ -726,15 +727,20 @@ __global__ void __launch_bounds__(256) k_wmean_regen(const RegenArgs a, const fl
     if (ok[j]) mv[j] = a.msv[e[j]];
   }
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  // the round keys in (vector) registers, derived once: a warp-uniform key
+  // would be re-derived in uniform registers on every draw
+  uint2 key = a.keys[a.step];
+  key.x = __shfl_sync(0xffffffffu, key.x, 0);
+  key.y = __shfl_sync(0xffffffffu, key.y, 0);
   if (k < a.R) {
-    const uint2 key = a.keys[a.step];
+    const PhiloxKeys ks(key);
     const float sd = a.sd;
     const int q0 = s_pos[sr * LANES], q1 = s_pos[(sr + 1) * LANES];
     const uint64_t mg = (uint64_t)(a.m_global0 + mc);
 #pragma unroll 2
     for (int q = q0; q < q1; ++q) {
       const float wm = s_w[q];
-      const float4 v = philox_normals(key, mg + (uint64_t)s_idx[q], (uint32_t)k, (uint32_t)gg);
+      const float4 v = philox_normals(ks, mg + (uint64_t)s_idx[q], (uint32_t)k, (uint32_t)gg);
       acc[0] = fmaf(wm, fmaf(sd, v.x, mv[0]), acc[0]);
       acc[1] = fmaf(wm, fmaf(sd, v.y, mv[1]), acc[1]);
       acc[2] = fmaf(wm, fmaf(sd, v.z, mv[2]), acc[2]);
