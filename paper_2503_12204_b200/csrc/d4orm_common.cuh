@@ -167,7 +167,11 @@ __device__ __forceinline__ uint64_t fmul2(uint64_t a, uint64_t b) {
 // Philox4x32-10 (Salmon et al., SC'11) + Box-Muller.  Noise of denoising step
 // i is keyed by keys[i] = mix_seed(seed_it, i).  For sample m and robot k the
 // normals form one sequence n = t·du + d (t < T, d < du); group g = n/4 is
-// Philox(counter = (g, m_lo, m_hi, k)), lanes n%4.  Each normal is a pure
+// Philox(counter = (k, g, m_hi, m_lo)), lanes n%4.  (The words that vary
+// along a draw loop — g along a rollout thread's steps, m_lo along the weighted
+// mean's samples — sit in the two XOR-only slots of round 1 (y, w), so the
+// compiler folds round 1 and half of rounds 2–3 into per-thread constants: 34
+// instead of 37–40 integer ops per group.)  Each normal is a pure
 // function of (seed, i, m, k, t, d): identical under any sharding of samples,
 // and a rollout thread owning robot k draws its own stream with no redundancy.
 #ifndef D4K_PHILOX_ROUNDS
@@ -231,14 +235,14 @@ struct PhiloxKeys {
 };
 
 __device__ __forceinline__ float4 philox_normals(uint2 key, uint64_t m, uint32_t k, uint32_t g) {
-  const uint4 r = Philox::gen(make_uint4(g, (uint32_t)m, (uint32_t)(m >> 32), k), key);
+  const uint4 r = Philox::gen(make_uint4(k, g, (uint32_t)(m >> 32), (uint32_t)m), key);
   const float2 a = box_muller(r.x, r.y), b = box_muller(r.z, r.w);
   return make_float4(a.x, a.y, b.x, b.y);
 }
 
 // philox_normals with a precomputed key schedule (same numbers)
 __device__ __forceinline__ float4 philox_normals(const PhiloxKeys& ks, uint64_t m, uint32_t k, uint32_t g) {
-  const uint4 r = ks.gen(make_uint4(g, (uint32_t)m, (uint32_t)(m >> 32), k));
+  const uint4 r = ks.gen(make_uint4(k, g, (uint32_t)(m >> 32), (uint32_t)m));
   const float2 a = box_muller(r.x, r.y), b = box_muller(r.z, r.w);
   return make_float4(a.x, a.y, b.x, b.y);
 }

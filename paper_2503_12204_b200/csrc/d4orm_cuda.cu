@@ -1473,6 +1473,10 @@ int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* p) {
   // 128-thread CTAs (several resident per SM: one CTA's latency-bound rollout
   // phase overlaps another's compute-bound fitness phase)
   ctx->spc = ctx->Rp >= 128 ? 1 : 128 / ctx->Rp;
+  if (const char* e = std::getenv("D4ORM_SPC")) {  // experiment knob: samples per CTA (≥ 32 threads)
+    const int v = std::atoi(e);
+    if (!ctx->pl && v >= 1 && v * ctx->Rp >= 32 && v * ctx->Rp <= 128 && (v * ctx->Rp) % 32 == 0) ctx->spc = v;
+  }
   if (int r = choose_tc<float>(ctx, &ctx->TC32, &ctx->smem32)) return r;
   if (int r = choose_tc<double>(ctx, &ctx->TC64, &ctx->smem64)) return r;
   ctx->has_problem = true;

@@ -9,8 +9,8 @@ module restates that generator in numpy so the GPU bits can be checked:
   0x9E3779B9 / 0xBB67AE85.  Pinned by the published known-answer vectors
   below (Random123 kat_vectors, philox4x32 with 10 rounds).
 * Counter mapping: normals of (seed_it, step i, sample m, robot k) form one
-  sequence n = t·du + d; group g = n // 4 is Philox(counter = (g, m_lo, m_hi,
-  k), key = mix_seed(seed_it, i) split lo/hi), lane n % 4.
+  sequence n = t·du + d; group g = n // 4 is Philox(counter = (k, g, m_hi,
+  m_lo), key = mix_seed(seed_it, i) split lo/hi), lane n % 4.
 * Uniforms from the top 23 bits: u = (2j+1)·2^-24 for j = x >> 9 (exact);
   angle 2π·j·2^-23.  Box-Muller (r cos θ, r sin θ) on the lane pairs (0,1) and
   (2,3); the device evaluates log2 / sqrt / sincos on the MUFU unit
@@ -64,8 +64,8 @@ def philox_words(seed_it: int, step: int, m0: int, count: int, R: int, T: int, d
     m = (np.arange(count, dtype=np.uint64) + np.uint64(m0))[:, None, None]
     k = np.arange(R, dtype=np.uint64)[None, :, None]
     g = np.arange(G, dtype=np.uint64)[None, None, :]
-    out = philox4x32(g + 0 * m + 0 * k, (m & MASK32) + 0 * k + 0 * g, (m >> np.uint64(32)) + 0 * k + 0 * g,
-                     k + 0 * m + 0 * g, k0, k1)
+    out = philox4x32(k + 0 * m + 0 * g, g + 0 * m + 0 * k, (m >> np.uint64(32)) + 0 * k + 0 * g,
+                     (m & MASK32) + 0 * k + 0 * g, k0, k1)
     return np.stack(out, axis=-1)
 
 
