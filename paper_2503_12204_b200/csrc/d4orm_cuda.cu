@@ -828,8 +828,8 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
     h = (h ^ v) * 1099511628211ull;
   }
   char b[600];
-  snprintf(b, sizeof b, "%llx/%lld/%d/%.17g/%.17g/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p",
-           (unsigned long long)h, (long long)rs.M, rs.N, rs.abf, rs.lambda, ctx->precision, rs.mode, (void*)ctx->z[0].p, (void*)ctx->z[1].p, (void*)ctx->partial.p,
+  snprintf(b, sizeof b, "%d/%llx/%lld/%d/%.17g/%.17g/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p",
+           ctx->regen_ok ? 1 : 0, (unsigned long long)h, (long long)rs.M, rs.N, rs.abf, rs.lambda, ctx->precision, rs.mode, (void*)ctx->z[0].p, (void*)ctx->z[1].p, (void*)ctx->partial.p,
            (void*)ctx->base.p, (void*)ctx->msv.p, (void*)ctx->var.p, (void*)ctx->rewards.p, (void*)ctx->w64.p,
            (void*)ctx->w32.p, (void*)ctx->trace.p, (void*)ctx->keys.p, (void*)ctx->errw.p, (void*)ctx->roots.p);
   return b;

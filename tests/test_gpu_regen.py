@@ -93,3 +93,27 @@ def test_regen_solve_and_mppi():
     np.testing.assert_array_equal(a.best_controls, b.best_controls)
     assert a.best_reward == b.best_reward
     assert [r[:3] for r in a.per_iteration] == [r[:3] for r in b.per_iteration]
+
+
+def test_regen_switch_in_one_context():
+    """One context, the K5a mode switched between runs: the captured graphs are
+    keyed on the mode (and the z buffer grows when the stored path needs rows),
+    so every run gives the same bits."""
+    p = S.baseline_config(4).problem
+    g = d4.GpuDenoiser()
+    try:
+        g.set_problem(p)
+        cfg = d4.DenoiserConfig(steps=4, batch=4096, seed=5)
+        base = np.zeros((p.horizon, p.robots, p.du))
+        outs, modes = [], []
+        for flag in ("1", "0", "1", "0"):
+            os.environ["D4ORM_K5REGEN"] = flag
+            outs.append(g.run_denoising(base, cfg))
+            modes.append(g.k5_regen())
+        assert modes == [1, 0, 1, 0]
+        for v, tr in outs[1:]:
+            np.testing.assert_array_equal(v, outs[0][0])
+            assert tr == outs[0][1]
+    finally:
+        os.environ.pop("D4ORM_K5REGEN", None)
+        g.close()
