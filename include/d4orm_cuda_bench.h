@@ -3,6 +3,7 @@
  */
 #ifndef D4ORM_CUDA_BENCH_H
 #define D4ORM_CUDA_BENCH_H
+#include <stdint.h>
 #ifdef __cplusplus
 extern "C" {
 #endif
@@ -18,6 +19,10 @@ int d4orm_cuda_fitness_path(const struct d4orm_cuda_ctx* ctx);
  * the Philox noise (no z rows stored, k_wmean_regen), 0 = read the z rows
  * K2+K3 stored, -1 = no run yet. */
 int d4orm_cuda_k5_regen(const struct d4orm_cuda_ctx* ctx);
+/* The fp32 weights K4 left for K5 (after d4orm_cuda_score_weights or a step):
+ * w64 cast to float, zero below the adaptive floor (weights whose total is at
+ * most 2^-30 of the sum).  m = how many to copy. */
+int d4orm_cuda_last_w32(struct d4orm_cuda_ctx* ctx, float* out, int64_t m);
 #ifdef __cplusplus
 }
 #endif

@@ -511,7 +511,7 @@ int ensure_buffers(d4orm_cuda_ctx* ctx, const RunShape& rs, bool two_z, bool phi
   CU(ctx->partial.ensure((size_t)rs.chunks_local * rs.E * S));
   CU(ctx->roots.ensure((size_t)ctx->world * rs.E * S));
   CU(ctx->trace.ensure((size_t)4 * (rs.N + 1)));
-  CU(ctx->wscratch.ensure((size_t)6 * 160));
+  CU(ctx->wscratch.ensure((size_t)d4k::kWScratch));
   CU(ctx->errw.ensure(1));
   CU(ctx->keys.ensure((size_t)rs.N + 1));
   return D4ORM_OK;
@@ -600,9 +600,13 @@ StepConsts denoise_consts(const d4orm_cuda_ctx* ctx, const RunShape& rs, int i) 
 // reading their z is HBM-bound at 2.3 ms) and 34 GB less HBM; C4 (du = 3: three
 // scalar z stores per robot-step) 0.1667 → 0.1601; C1–C3 lose 2–10 µs (their
 // z stays in L2 for K5a), so they keep the stored rows.
+bool k5_skips_class(const d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  return rs.E >= kPartLargeE || ctx->prob.du == 3;
+}
+
 bool regen_wanted(const d4orm_cuda_ctx* ctx, const RunShape& rs) {
   if (const char* e = std::getenv("D4ORM_K5REGEN")) return std::atoi(e) != 0;
-  return rs.E >= kPartLargeE || ctx->prob.du == 3;
+  return k5_skips_class(ctx, rs);
 }
 
 // K2+K3 (+ K1 on the fp64 Philox path) and the reward all-gather.
@@ -640,8 +644,12 @@ int enqueue_fitness(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
 
 // K4: z-scored softmax weights over all M rewards.
 int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc) {
+  // adaptive w32 floor for the problem shapes whose K5a skips zero-weight
+  // samples (one sequential walk per thread, or regenerated noise); the fixed
+  // floor elsewhere.  By shape only, so every noise source / K5a mode of a
+  // problem sees the same weights.
   d4k::WeightParams wp{ctx->rewards.p, rs.M, rs.lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p + 4 * sc.trace_off,
-                       sc.trace_step, ctx->errw.p};
+                       sc.trace_step, ctx->errw.p, (rs.E == 0 || k5_skips_class(ctx, rs)) ? 1 : 0};
   // M ≤ 8192 (C1, C2): one CTA, ≤ 8 rewards per thread, shared-memory folds
   // (beyond that one SM's fp64 exp throughput loses to the cooperative grid)
   if (rs.M <= 8LL * d4k::kWThreads) {
@@ -1684,14 +1692,14 @@ int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t
   CU(ctx->trace.ensure(4));
   CU(ctx->errw.ensure(1));
   CU(cudaMemcpyAsync(ctx->rewards.p, rewards, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->s_main));
-  CU(ctx->wscratch.ensure((size_t)6 * 160));
+  CU(ctx->wscratch.ensure((size_t)d4k::kWScratch));
   if (m <= 148LL * d4k::kWThreads * 16) {  // the denoising step's own K4 dispatch
     RunShape rs;
     rs.M = m;
     rs.lambda = lambda;
     if (int r = enqueue_weights(ctx, rs, StepConsts{})) return r;
   } else {  // beyond one cooperative wave: the single-CTA loop over any M
-    d4k::WeightParams wp{ctx->rewards.p, m, lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p, 0, ctx->errw.p};
+    d4k::WeightParams wp{ctx->rewards.p, m, lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p, 0, ctx->errw.p, 1};
     d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
   }
   CU(cudaGetLastError());
@@ -1727,6 +1735,14 @@ int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_
 int d4orm_cuda_fitness_path(const d4orm_cuda_ctx* ctx) {
   if (!ctx || !ctx->has_problem) return -1;
   return ctx->pl ? 1 : 0;
+}
+
+int d4orm_cuda_last_w32(d4orm_cuda_ctx* ctx, float* out, int64_t m) {
+  if (!ctx || !out || m < 0 || (size_t)m > ctx->w32.n) return D4ORM_E_INVALID;
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize(ctx->s_main));
+  CU(cudaMemcpy(out, ctx->w32.p, sizeof(float) * (size_t)m, cudaMemcpyDeviceToHost));
+  return D4ORM_OK;
 }
 
 int d4orm_cuda_k5_regen(const d4orm_cuda_ctx* ctx) {

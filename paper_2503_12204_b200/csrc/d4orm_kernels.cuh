@@ -50,7 +50,68 @@ __global__ void __launch_bounds__(kThreads) k_philox_noise(S* __restrict__ z, in
 }
 
 // ------------------------------------------------------------ K4 weights
-constexpr double kW32Floor = 3.5527136788005009e-15;  // 2^-48: relative weight below which w32 = 0
+// fp32 weights drive the fp32 weighted mean (K5), which skips samples whose
+// w32 is 0.  A sample's w32 is zeroed when its weight lies below an adaptive
+// floor: the largest power of two 2^-b such that the weights below it provably
+// add up to at most 2^-30 of the total (1e-9 — far below the fp32 sum's own
+// rounding).  The proof is a count histogram over octaves: e = exp(s − s_max)
+// ∈ [2^-(b+1), 2^-b) falls in bin b (bin 128: e < 2^-128), and bins ≥ b hold at
+// most Σ c_b'·2^-b' of Σe.  Integer counts → deterministic, identical on every
+// rank.  (At C5 this keeps ≈ 41 % of the samples, against 59 % for a fixed
+// 2^-48 floor — which gave the same 2^-30 bound only at M = 2^18.)
+// Where K5a reads every row anyway (small E, z in L2) the histogram is not
+// built and the fixed floor 2^-48 of the largest weight applies (bound
+// M·2^-48 of the total).
+constexpr double kW32Floor = 3.5527136788005009e-15;  // 2^-48
+constexpr int kWBins = 129;
+constexpr double kW32Mass = 9.313225746154785e-10;  // 2^-30
+constexpr int kWScratch = 6 * 160 + 80;               // grid folds + the bin counts (as doubles)
+
+__device__ __forceinline__ int wbin(double e) {  // e ∈ (0, 1]: octave below the max
+  if (!(e >= 0x1p-128)) return 128;
+  const int ex = (int)((__double_as_longlong(e) >> 52) & 0x7ff) - 1023;  // ilogb, e normal
+  return ex >= -1 ? 0 : -ex - 1;
+}
+
+// Floor from the bin counts, by one warp (all 32 lanes; the same fixed-order
+// arithmetic on every CTA and rank): U(b) = Σ_{b' ≥ b} c_b'·2^-b' as a suffix
+// scan (5 bins per lane, then across lanes), floor = 2^-b* for the smallest
+// b* ≥ 1 with U(b*) ≤ 2^-30·Σe (0 if none).
+__device__ __forceinline__ double w32_floor_warp(const unsigned* c, double sum_e) {
+  constexpr int PER = 5;  // 32·5 ≥ kWBins
+  const int lane = threadIdx.x & 31;
+  const double bound = kW32Mass * sum_e;
+  double m[PER], loc = 0.0;
+#pragma unroll
+  for (int j = PER - 1; j >= 0; --j) {
+    const int b = lane * PER + j;
+    if (b < kWBins) loc += (double)c[b] * __longlong_as_double((long long)(1023 - b) << 52);  // c·2^-b
+    m[j] = loc;
+  }
+  double x = loc;  // Σ over lanes ≥ lane
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_down_sync(0xffffffffu, x, o);
+    if (lane + o < 32) x += y;
+  }
+  double above = __shfl_down_sync(0xffffffffu, x, 1);
+  if (lane == 31) above = 0.0;
+  int best = 1 << 30;
+#pragma unroll
+  for (int j = PER - 1; j >= 0; --j) {
+    const int b = lane * PER + j;
+    if (b >= 1 && b < kWBins && m[j] + above <= bound) best = b;
+  }
+  best = __reduce_min_sync(0xffffffffu, best);
+  return best < kWBins ? __longlong_as_double((long long)(1023 - best) << 52) : 0.0;
+}
+
+// One count into bin b, aggregated over the warp's lanes that share the bin.
+__device__ __forceinline__ void hist_add(unsigned* h, int b) {
+  const unsigned peers = __match_any_sync(__activemask(), b);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[b], (unsigned)__popc(peers));
+}
+
 struct WeightParams {
   const double* reward;  // [M] all samples (global)
   int64_t M;
@@ -60,6 +121,7 @@ struct WeightParams {
   double* trace;         // [4]: step, best, mean, entropy
   int step;
   unsigned long long* err;  // set on non-finite reward
+  int adaptive;             // 1: the adaptive w32 floor (K5 skips zero weights); 0: the fixed 2^-48 one
 };
 
 template <int NT>
@@ -154,6 +216,13 @@ template <int NT, int kWPer>
 __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p, double* scratch) {
   static_assert(NT == kWThreads, "k_score_weights_grid block size");
   __shared__ double sh[3 * 32];
+  __shared__ unsigned s_hist[kWBins];
+  __shared__ double s_floor;
+  unsigned* g_hist = reinterpret_cast<unsigned*>(scratch + 6 * 160);
+  if (threadIdx.x < kWBins) {
+    s_hist[threadIdx.x] = 0u;
+    if (blockIdx.x == 0) g_hist[threadIdx.x] = 0u;  // added to only after two grid barriers
+  }
   const int64_t stride = (int64_t)gridDim.x * kWThreads;
   const int64_t g0 = (int64_t)blockIdx.x * kWThreads + threadIdx.x;
   double r[kWPer];
@@ -226,11 +295,25 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
       e[q] = exp(r[q]);
       sum += e[q];
       es += e[q] * r[q];
+      if (p.adaptive) hist_add(s_hist, wbin(e[q]));
     }
   }
+  __syncthreads();
+  if (p.adaptive && threadIdx.x < kWBins && s_hist[threadIdx.x]) atomicAdd(&g_hist[threadIdx.x], s_hist[threadIdx.x]);
   double f2[2] = {sum, es};
-  grid_fold_n<2, 0>(f2, sh, scratch, 4);
+  grid_fold_n<2, 0>(f2, sh, scratch, 4);  // (its grid barrier also completes g_hist)
   sum = f2[0];
+  double floor32 = kW32Floor;
+  if (p.adaptive) {
+    if (threadIdx.x < kWBins) s_hist[threadIdx.x] = __ldcg(&g_hist[threadIdx.x]);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const double f = w32_floor_warp(s_hist, sum);
+      if (threadIdx.x == 0) s_floor = f;
+    }
+    __syncthreads();
+    floor32 = s_floor;
+  }
   const double rsum = 1.0 / sum, lsum = log(sum);
   // entropy −Σ w·log w with log w = s − log Σe: log Σe − Σe·s / Σe (terms with
   // e = 0 contribute 0, as the w > 0 guard of denoiser.cpp:24-30)
@@ -241,10 +324,7 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
     if (j < p.M) {
       const double w = e[q] * rsum;
       p.w64[j] = w;
-      // fp32 weights drive the fp32 weighted mean (K5): a sample whose weight
-      // is below 2^-48 of the largest cannot move an fp32 sum (even M = 2^18
-      // of them add < 1e-9 of the total) and its z row is not read at all
-      p.w32[j] = e[q] >= kW32Floor ? (float)w : 0.f;
+      p.w32[j] = e[q] >= floor32 ? (float)w : 0.f;  // adaptive floor (kW32Mass)
     }
   }
   if (head) {
@@ -296,7 +376,10 @@ __device__ __forceinline__ void cta_fold_n(double* v, double* sh) {
 template <int PER>
 __global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const WeightParams p) {
   __shared__ double sh[3 * 32 + 4];
+  __shared__ unsigned s_hist[kWBins];
+  __shared__ double s_floor;
   const int tid = threadIdx.x;
+  if (tid < kWBins) s_hist[tid] = 0u;
   double r[PER];
   double s = 0.0, best = -INFINITY;
   bool finite = true;
@@ -361,11 +444,21 @@ __global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const Weight
       sum += e;
       es += e * a;
       r[q] = e;
+      if (p.adaptive) hist_add(s_hist, wbin(e));
     }
   }
   double f2[2] = {sum, es};
-  cta_fold_n<2, 0>(f2, sh);
+  cta_fold_n<2, 0>(f2, sh);  // (its barriers also complete s_hist)
   sum = f2[0];
+  double floor32 = kW32Floor;
+  if (p.adaptive) {
+    if (tid < 32) {
+      const double f = w32_floor_warp(s_hist, sum);
+      if (tid == 0) s_floor = f;
+    }
+    __syncthreads();
+    floor32 = s_floor;
+  }
   const double rsum = 1.0 / sum;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
@@ -373,7 +466,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const Weight
     if (j < p.M) {
       const double w = r[q] * rsum;
       p.w64[j] = w;
-      p.w32[j] = r[q] >= kW32Floor ? (float)w : 0.f;
+      p.w32[j] = r[q] >= floor32 ? (float)w : 0.f;  // adaptive floor (kW32Mass)
     }
   }
   if (tid == 0) {

@@ -192,6 +192,12 @@ class GpuDenoiser:
     def launches_per_step(self) -> int:
         return self._L.d4orm_cuda_launches_per_step(self._h)
 
+    def last_w32(self, m: int) -> np.ndarray:
+        """The fp32 weights K4 left for K5 (zero below the adaptive floor)."""
+        out = np.empty(m, dtype=np.float32)
+        self._check(self._L.d4orm_cuda_last_w32(self._h, out.ctypes.data_as(C.POINTER(C.c_float)), m))
+        return out
+
     def k5_regen(self) -> int:
         """1: the last run's K5a regenerated the Philox noise (no z rows), 0: it
         read the stored z rows, -1: no run yet."""

@@ -13,10 +13,16 @@ cfg = d4.DenoiserConfig(steps=rc.steps, batch=rc.samples, seed=0)
 ab = d4.make_schedule(cfg.steps, cfg.alpha_bar_final)
 base = np.zeros((p.horizon, p.robots, p.du))
 var = np.zeros_like(base)
-fr = []
+fr, fa = [], {30: [], 40: []}
 for i in range(cfg.steps, 0, -1):
     var, r, w, rec = g.denoise_step(base, var, i, cfg, None)
     fr.append(float(np.mean(w >= w.max() * 2.0 ** -48)))
-print("significant fraction per step (i = N..1):")
+    # adaptive alternative: drop the smallest weights whose total is <= 2^-b of the sum
+    cs = np.cumsum(np.sort(w))
+    for b in fa:
+        fa[b].append(1.0 - np.searchsorted(cs, cs[-1] * 2.0 ** -b, side="right") / len(w))
+print("significant fraction per step (i = N..1), floor 2^-48 of the max:")
 print(" ".join("%.3f" % f for f in fr))
 print("mean %.3f  min %.3f  max %.3f" % (np.mean(fr), np.min(fr), np.max(fr)))
+for b, v in fa.items():
+    print("adaptive (dropped mass <= 2^-%d of the sum): mean %.3f  min %.3f  max %.3f" % (b, np.mean(v), np.min(v), np.max(v)))
