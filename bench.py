@@ -319,8 +319,10 @@ def main():
                      "note": "achieved = SURVEY 8d algorithmic FLOPs (every unordered pair and robot-obstacle test counted) / "
                              "launch time; the kernel culls tests exactly, so the executed FMA-pipe utilisation is lower "
                              "(ncu, profiles/r01_ncu_k23k5_c5_v17.md)"},
-        "kernel_ms": {"K1_philox": kms[0], "K2K3_rollout_fitness": kms[1], "K4_weights": kms[2],
-                      "K5_wmean_partial": kms[3], "K5_tree_update": kms[4]},
+        "kernel_ms": {"K1_philox": None, "K2K3_rollout_fitness": kms[1], "K4_weights": kms[2],
+                      "K5_wmean_partial": kms[3], "K5_tree_update": kms[4],
+                      "note": "K1 (Philox + Box-Muller) is fused into K2+K3 on the fp32 path: the noise is drawn in "
+                              "registers there (and regenerated by K5a where k5.kernel says k_wmean_regen)"},
         "k5": k5_info,
         "gpu_launches": args.steps * g.launches_per_step(),
         "clocks": clk.summary(),
