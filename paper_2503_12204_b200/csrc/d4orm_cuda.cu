@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "k_seg.cuh"
 #include "../../include/d4orm_cuda.h"
 #include "d4orm_kernels.cuh"
 #include "k_outcome.cuh"
@@ -430,8 +431,23 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
   return f;
 }
 
+// The time-segmented K2+K3 (k_seg.cu) for launches the regular kernel leaves
+// latency-bound: fewer than two of its CTAs per SM (C1), velocity-input kinds,
+// fp32, scalar std, no state/control output.  Knob D4ORM_SEG=0/1.
+template <typename S>
+bool use_seg(const d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f) {
+  if (!std::is_same<S, float>::value || f.sdv || f.states_out || f.controls_out) return false;
+  const d4orm_problem& p = ctx->prob;
+  if (!d4k::seg_supported(p.kind, p.robots, p.horizon, p.du)) return false;
+  if (const char* e = std::getenv("D4ORM_SEG")) return std::atoi(e) != 0;
+  return (f.M + ctx->spc - 1) / ctx->spc < 2 * 148;
+}
+
 template <typename S>
 cudaError_t launch_fit(d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f, size_t smem, bool fused) {
+  if constexpr (std::is_same<S, float>::value) {
+    if (use_seg(ctx, f)) return d4k::launch_seg(ctx->prob.kind, fused, f.M, ctx->s_main, f);
+  }
   const bool pl = std::is_same<S, float>::value && ctx->pl;
   const dim3 grid((unsigned)((f.M + ctx->spc - 1) / ctx->spc));
   const int th = ctx->spc * ctx->Rp;
