@@ -47,9 +47,8 @@ __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_consta
   const int64_t m = (int64_t)blockIdx.x * spc + s;
   const bool live = s < spc && m < p.M;
   float* P = pos + (size_t)s * (T + 1) * R * PD;
-  double* red = reinterpret_cast<double*>(pos + (size_t)spc * (T + 1) * R * PD);  // [blockDim] goal
-  float* eff_sh = reinterpret_cast<float*>(red + blockDim.x);                      // [blockDim]
-  int* cnt = reinterpret_cast<int*>(eff_sh + blockDim.x);                         // [2·blockDim]
+  double* red = reinterpret_cast<double*>(pos + (size_t)spc * (T + 1) * R * PD);  // [8] warp goal / effort sums
+  int* cnt = reinterpret_cast<int*>(red + 8);                                     // [8] warp counts
 
   // ---- 1. noise, controls, local prefix (states → shared as q_t for now)
   float q[PD], eff = 0.f;
@@ -59,6 +58,12 @@ __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_consta
   if (live) {
     const float* bm = p.bm + ((size_t)t0 * R + k) * DU;
     const int RDU = R * DU;
+    float bq[kSegMaxL * DU];  // base + msv, loaded first: the draws hide the latency
+#pragma unroll
+    for (int i = 0; i < kSegMaxL; ++i)
+      if (i < L)
+#pragma unroll
+        for (int d = 0; d < DU; ++d) bq[i * DU + d] = __ldg(bm + i * RDU + d);
     float z[kSegMaxL * DU];
     if constexpr (NOISE == 1) {
       const uint2 key = p.keys[p.step];
@@ -94,7 +99,7 @@ __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_consta
       if (i < L) {
 #pragma unroll
         for (int d = 0; d < DU; ++d) {
-          const float u = fminf(fmaxf(fmaf(p.sd, z[i * DU + d], __ldg(bm + i * RDU + d)), p.lower[d]), p.upper[d]);
+          const float u = fminf(fmaxf(fmaf(p.sd, z[i * DU + d], bq[i * DU + d]), p.lower[d]), p.upper[d]);
           eff = fmaf(u, u, eff);
           q[d] = fmaf(p.dt, u, q[d]);
           P[((size_t)(t0 + i + 1) * R + k) * PD + d] = q[d];
@@ -123,6 +128,9 @@ __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_consta
       for (int d = 0; d < PD; ++d) P[(size_t)k * PD + d] = off[d];
     }
     const float ginv = p.inv_dstart[k];
+    float gl[PD];
+#pragma unroll
+    for (int d = 0; d < PD; ++d) gl[d] = p.goals[(size_t)k * PD + d];
     for (int i = 0; i < L; ++i) {
       float* x = P + ((size_t)(t0 + i + 1) * R + k) * PD;
       float d2 = 0.f;
@@ -132,7 +140,7 @@ __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_consta
         const float v = off[d] + x[d];
         x[d] = v;
         fin = fin && isfinite(v);
-        const float e = v - p.goals[(size_t)k * PD + d];
+        const float e = v - gl[d];
         d2 = fmaf(e, e, d2);
       }
       if (!fin && bad_t == 0x3ff) bad_t = t0 + i + 1;
@@ -183,35 +191,50 @@ __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_consta
       no += ob ? 1 : 0;
     }
   }
-  // ---- 4. per-sample fixed-order reduction
-  red[tid] = live ? (double)L - (double)gsd : 0.0;
-  eff_sh[tid] = live ? eff : 0.f;
-  cnt[2 * tid] = nc;
-  cnt[2 * tid + 1] = no;
-  __syncthreads();
-  if (live && r == 0) {
-    const int first = s * per_sample;
-    double g = 0.0, ef = 0.0;
-    long long ncs = 0, nos = 0;
-    for (int i = 0; i < per_sample; ++i) {
-      g += red[first + i];
-      ef += (double)eff_sh[first + i];
-      ncs += cnt[2 * (first + i)];
-      nos += cnt[2 * (first + i) + 1];
+  // ---- 4. per-sample fixed-order reduction: a shuffle tree per warp (a warp
+  // never spans two samples: per_sample is 8·R ∈ {8, …, 128}), then the
+  // sample's warps in index order
+  double g = live ? (double)L - (double)gsd : 0.0, ef = live ? (double)eff : 0.0;
+  int ncs = nc, nos = no;
+  const int width = per_sample < 32 ? per_sample : 32;
+  for (int o = width / 2; o > 0; o >>= 1) {
+    g += __shfl_down_sync(0xffffffffu, g, o, width);
+    ef += __shfl_down_sync(0xffffffffu, ef, o, width);
+    ncs += __shfl_down_sync(0xffffffffu, ncs, o, width);
+    nos += __shfl_down_sync(0xffffffffu, nos, o, width);
+  }
+  const int lane = tid & 31, w = tid >> 5;
+  if (per_sample > 32) {
+    if (lane == 0) {
+      red[w] = g;
+      red[4 + w] = ef;
+      cnt[2 * w] = ncs;
+      cnt[2 * w + 1] = nos;
     }
+    __syncthreads();
+    if (r == 0) {
+      for (int q = 1; q < per_sample / 32; ++q) {
+        g += red[w + q];
+        ef += red[4 + w + q];
+        ncs += cnt[2 * (w + q)];
+        nos += cnt[2 * (w + q) + 1];
+      }
+    }
+  }
+  if (live && r == 0) {
     double value = g - p.w_t * (double)ncs - p.w_o * (double)nos;
     if (p.w_e != 0.0) value -= p.w_e * ef;
     p.reward[m] = value / ((double)R * (double)T);
     if (p.counts) {
-      p.counts[2 * m] = (int)ncs;
-      p.counts[2 * m + 1] = (int)nos;
+      p.counts[2 * m] = ncs;
+      p.counts[2 * m + 1] = nos;
     }
   }
 }
 
 size_t seg_smem_bytes(int R, int T, int pdim) {
   const int spc = 128 / (R * kSegs);
-  return (size_t)spc * (T + 1) * R * pdim * sizeof(float) + 128 * (sizeof(double) + sizeof(float) + 2 * sizeof(int));
+  return (size_t)spc * (T + 1) * R * pdim * sizeof(float) + 8 * sizeof(double) + 8 * sizeof(int);
 }
 
 bool seg_supported(int kind, int R, int T, int du) {
