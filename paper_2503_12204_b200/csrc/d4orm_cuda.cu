@@ -433,7 +433,9 @@ d4k::FitParams<S> fit_params(d4orm_cuda_ctx* ctx, const S* z, const S* base, con
 
 // The time-segmented K2+K3 (k_seg.cu) for launches the regular kernel leaves
 // latency-bound: fewer than two of its CTAs per SM (C1), velocity-input kinds,
-// fp32, scalar std, no state/control output.  Knob D4ORM_SEG=0/1.
+// fp32, scalar std, no state/control output.  Knob D4ORM_SEG=0/1.  (It trades
+// work efficiency for a short chain: forced onto the throughput-bound C2 / C4
+// it is 7× / 6× slower than the register-tiled regular kernel.)
 template <typename S>
 bool use_seg(const d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f) {
   if (!std::is_same<S, float>::value || f.sdv || f.states_out || f.controls_out) return false;
