@@ -673,13 +673,14 @@ int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
   // M ≤ 8192 (C1, C2): one CTA, ≤ 8 rewards per thread, shared-memory folds
   // (beyond that one SM's fp64 exp throughput loses to the cooperative grid)
   if (rs.M <= 8LL * d4k::kWThreads) {
-    const int per = rs.M <= 1024 ? 1 : rs.M <= 2048 ? 2 : rs.M <= 4096 ? 4 : 8;
-    const void* fn = per == 1   ? (const void*)d4k::k_score_weights_cta<1>
-                     : per == 2 ? (const void*)d4k::k_score_weights_cta<2>
-                     : per == 4 ? (const void*)d4k::k_score_weights_cta<4>
-                                : (const void*)d4k::k_score_weights_cta<8>;
+    // ≤ 2048 rewards: 256 threads (8-warp folds), else 1024
+    const int nt = rs.M <= 2048 ? 256 : d4k::kWThreads;
+    const void* fn = rs.M <= 1024   ? (const void*)d4k::k_score_weights_cta<256, 4>
+                     : rs.M <= 2048 ? (const void*)d4k::k_score_weights_cta<256, 8>
+                     : rs.M <= 4096 ? (const void*)d4k::k_score_weights_cta<d4k::kWThreads, 4>
+                                    : (const void*)d4k::k_score_weights_cta<d4k::kWThreads, 8>;
     void* args1[] = {(void*)&wp};
-    CU(cudaLaunchKernel(fn, dim3(1), dim3(d4k::kWThreads), args1, 0, ctx->s_main));
+    CU(cudaLaunchKernel(fn, dim3(1), dim3(nt), args1, 0, ctx->s_main));
     return D4ORM_OK;
   }
   // 2 rewards per thread (16 beyond 148·2048 samples) held in registers;

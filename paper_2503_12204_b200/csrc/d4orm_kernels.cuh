@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
 // memory — no cooperative launch, no grid barriers, no global scratch round
 // trips (C1 step 29.1 → 26.9 µs).  Fixed fold order (warp tree, then warp 0 over
 // the 32 warp partials): deterministic, identical on every rank.
-template <int N, int MAXMASK>
+template <int N, int MAXMASK, int NT = kWThreads>
 __device__ __forceinline__ void cta_fold_n(double* v, double* sh) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
 #pragma unroll
@@ -358,7 +358,7 @@ __device__ __forceinline__ void cta_fold_n(double* v, double* sh) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const bool mx = (MAXMASK >> i) & 1;
-      double r = sh[i * 32 + lane];
+      double r = lane < NT / 32 ? sh[i * 32 + lane] : (mx ? -INFINITY : 0.0);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const double u = __shfl_xor_sync(0xffffffffu, r, o);
@@ -373,8 +373,8 @@ __device__ __forceinline__ void cta_fold_n(double* v, double* sh) {
   __syncthreads();
 }
 
-template <int PER>
-__global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const WeightParams p) {
+template <int NT, int PER>
+__global__ void __launch_bounds__(NT, 1) k_score_weights_cta(const WeightParams p) {
   __shared__ double sh[3 * 32 + 4];
   __shared__ unsigned s_hist[kWBins];
   __shared__ double s_floor;
@@ -385,19 +385,19 @@ __global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const Weight
   bool finite = true;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    const int64_t j = tid + (int64_t)q * kWThreads;
+    const int64_t j = tid + (int64_t)q * NT;
     r[q] = j < p.M ? p.reward[j] : 0.0;
   }
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    if (tid + (int64_t)q * kWThreads < p.M) {
+    if (tid + (int64_t)q * NT < p.M) {
       finite = finite && isfinite(r[q]);
       s += r[q];
       best = fmax(best, r[q]);
     }
   }
   double f3[3] = {finite ? 0.0 : 1.0, s, best};
-  cta_fold_n<3, 4>(f3, sh);
+  cta_fold_n<3, 4, NT>(f3, sh);
   if (f3[0] != 0.0) {
     if (tid == 0) atomicMin(p.err, 0xFFFFFFFFFFFFFFFEull);
     return;
@@ -407,19 +407,19 @@ __global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const Weight
   double v = 0.0;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    if (tid + (int64_t)q * kWThreads < p.M) {
+    if (tid + (int64_t)q * NT < p.M) {
       const double d = r[q] - mean;
       v += d * d;
     }
   }
   double f1[1] = {v};
-  cta_fold_n<1, 0>(f1, sh);
+  cta_fold_n<1, 0, NT>(f1, sh);
   const double std_dev = sqrt(f1[0] / (double)p.M);
   if (std_dev < 1e-8) {  // degenerate batch → uniform (denoiser.cpp:74-77)
     const double u = 1.0 / (double)p.M;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
-      const int64_t j = tid + (int64_t)q * kWThreads;
+      const int64_t j = tid + (int64_t)q * NT;
       if (j < p.M) {
         p.w64[j] = u;
         p.w32[j] = (float)u;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const Weight
   double sum = 0.0, es = 0.0;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    if (tid + (int64_t)q * kWThreads < p.M) {
+    if (tid + (int64_t)q * NT < p.M) {
       const double a = (r[q] - mean) * inv - max_scaled;  // shifted exponent
       const double e = exp(a);
       sum += e;
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const Weight
     }
   }
   double f2[2] = {sum, es};
-  cta_fold_n<2, 0>(f2, sh);  // (its barriers also complete s_hist)
+  cta_fold_n<2, 0, NT>(f2, sh);  // (its barriers also complete s_hist)
   sum = f2[0];
   double floor32 = kW32Floor;
   if (p.adaptive) {
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kWThreads, 1) k_score_weights_cta(const Weight
   const double rsum = 1.0 / sum;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
-    const int64_t j = tid + (int64_t)q * kWThreads;
+    const int64_t j = tid + (int64_t)q * NT;
     if (j < p.M) {
       const double w = r[q] * rsum;
       p.w64[j] = w;
