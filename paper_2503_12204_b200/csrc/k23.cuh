@@ -30,6 +30,11 @@ constexpr int kObsBuckets = 64;  // x-buckets of the obstacle culling table
 #define D4K_KPF 8
 #endif
 constexpr int kPF = D4K_KPF;  // rollout block depth (time steps): Philox draws in flight per thread
+// The fused-noise rollout's block depth per kind: 16 steps for the two-control
+// kinds (C5 K2+K3 19.28 → 18.97 ms, C2 0.110 → 0.108 ms), 8 for du = 3 (16
+// measured +18 µs on C4: 48 normals in flight spill)
+template <int KIND>
+constexpr int kPFf = ModelDims<KIND>::DU == 3 ? kPF : 2 * kPF;
 #ifndef D4K_MINB16
 #define D4K_MINB16 3  // resident CTAs per SM the 16-robot-tile kernels are register-capped for
 #endif
@@ -666,9 +671,10 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
                                             int RS, float* x, float& eff32, float& chk, const float* ng, float ginv,
                                             float& gsd, float4& bx) {
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
-  float bq[kPF][DU], sq[SDV ? kPF : 1][DU];
+  constexpr int KPF = kPFf<KIND>;
+  float bq[KPF][DU], sq[SDV ? KPF : 1][DU];
 #pragma unroll
-  for (int j = 0; j < kPF; ++j) {
+  for (int j = 0; j < KPF; ++j) {
     if (FULL || j < nb) {
       if constexpr (DU == 2) {
         const float2 v = __ldg(reinterpret_cast<const float2*>(bmp + j * RDU));
@@ -684,9 +690,9 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
       }
     }
   }
-  float nz[kPF * DU];
+  float nz[KPF * DU];
 #pragma unroll
-  for (int g = 0; g < kPF * DU / 4; ++g) {
+  for (int g = 0; g < KPF * DU / 4; ++g) {
 #ifdef D4K_EXPERIMENT_CHEAP_RNG
     const float h = __uint_as_float(((key.x ^ (uint32_t)m * 0x9E3779B9u ^ kA * 0x85EBCA6Bu ^ (g0 + g) * 0xC2B2AE35u) >> 9) | 0x3f800000u) - 1.5f;
     const float4 v = make_float4(h, -h, 0.5f * h, -0.5f * h);
@@ -703,7 +709,7 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
   if (p.z_keep == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(zpol));
   else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(zpol));
 #pragma unroll
-  for (int j = 0; j < kPF; ++j) {
+  for (int j = 0; j < KPF; ++j) {
     if (p.z_keep == 2) break;  // K5a regenerates the noise
     if (FULL || j < nb) {
       if constexpr (DU == 2) {
@@ -723,7 +729,7 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
   constexpr bool PK = DU == 2 && !SDV;
   uint64_t eff2 = 0;
 #pragma unroll
-  for (int j = 0; j < kPF; ++j) {
+  for (int j = 0; j < KPF; ++j) {
     if (FULL || j < nb) {
       float u[DU];
       if constexpr (PK) {
@@ -778,6 +784,7 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
                                                int rA, int64_t m, int t0, int nsteps, float* x, float* zrow, uint2 key,
                                                float& eff32, const float* ng, float ginv, float& gsd) {
   constexpr int DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
+  constexpr int KPF = kPFf<KIND>;
   const int RDU = p.R * DU;
   const int64_t e0 = ((int64_t)t0 * p.R + kA) * DU;
   const float* bmp = p.bm + e0;
@@ -790,29 +797,29 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
   float chk = 0.f;
   float4 bx = empty_box();
   float4* pbw = PL ? sm.pbox + (size_t)sA * (sm.TC / 32) * sm.Rp + rA : nullptr;  // window 0 box slot
-  for (int tc = 0; tc < nsteps; tc += kPF) {
+  for (int tc = 0; tc < nsteps; tc += KPF) {
     const int nb = nsteps - tc;
     const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
-    if (nb >= kPF) {
-      fused_block<KIND, true, SDV, PL>(p, kPF, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk,
+    if (nb >= KPF) {
+      fused_block<KIND, true, SDV, PL>(p, KPF, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32, chk,
                                        ng, ginv, gsd, bx);
     } else {
       fused_block<KIND, false, SDV, PL>(p, nb, bmp, sdp, zp, RDU, (uint64_t)m, kA, g0, key, px, py, pz, RS, x, eff32,
                                         chk, ng, ginv, gsd, bx);
     }
     if constexpr (PL) {
-      if (((tc + kPF) & 31) == 0 || tc + kPF >= nsteps) {  // end of a warp window (or of the steps)
+      if (((tc + KPF) & 31) == 0 || tc + KPF >= nsteps) {  // end of a warp window (or of the steps)
         *pbw = bx;
         pbw += sm.Rp;
         bx = empty_box();
       }
     }
-    bmp += kPF * RDU;
-    if constexpr (SDV) sdp += kPF * RDU;
-    zp += kPF * RDU;
-    px += kPF * RS;
-    py += kPF * RS;
-    pz += kPF * RS;
+    bmp += KPF * RDU;
+    if constexpr (SDV) sdp += KPF * RDU;
+    zp += KPF * RDU;
+    px += KPF * RS;
+    py += KPF * RS;
+    pz += KPF * RS;
   }
   if constexpr (PL) {  // windows past the horizon: empty boxes
     for (float4* e = sm.pbox + (size_t)(sA + 1) * (sm.TC / 32) * sm.Rp + rA; pbw < e; pbw += sm.Rp) *pbw = empty_box();
