@@ -1,6 +1,8 @@
 #pragma once
 // GPU execution options for the drop-in (kept out of the reference structs so
-// their signatures stay unchanged).  Per host thread.
+// their signatures stay unchanged).  Per host thread; the defaults come from
+// D4ORM_DEVICE / D4ORM_PRECISION=f32|f64 / D4ORM_NOISE=philox|host /
+// D4ORM_GRAPHS=0|1 (for callers compiled unchanged against the reference headers).
 #include "../d4orm_cuda.h"
 
 namespace d4orm {

@@ -202,6 +202,15 @@ int d4orm_cuda_rollout_fitness(d4orm_cuda_ctx* ctx, const double* u, int64_t cou
 /* score_weights (denoiser.cpp:50-90) + entropy (:24-30). trace4 = {best, mean, entropy}. */
 int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t m, double lambda,
                              double* weights, double* trace3);
+/* mc_average (denoiser.cpp:92-108): out = sum_m weights[m] * samples[m] over
+ * m sample rows of `elems` values (m x elems fp64, any layout the caller
+ * shares between rows), after the reference's |sum(w) - 1| <= 1e-9 check
+ * (D4ORM_E_INVALID "mc_average: weights must sum to 1").  K5a + K5b in the
+ * context's precision: each 256-row chunk summed in ascending m, the chunk
+ * partials combined by a fixed pairwise tree (fp64: within rounding of the
+ * reference's sequential sum).  Needs no problem. */
+int d4orm_cuda_weighted_mean(d4orm_cuda_ctx* ctx, const double* samples, const double* weights, int64_t m,
+                             int64_t elems, double* out);
 /* K1: the Philox normals of (seed, step) for samples [m0, m0+count). */
 int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_t m0, int64_t count,
                             float* out);

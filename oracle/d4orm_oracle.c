@@ -665,6 +665,51 @@ done:
   return rc;
 }
 
+/* mc_average (denoiser.cpp:92-108): |Σw − 1| ≤ 1e-9, then out = Σ_m w_m·sample_m
+ * accumulated in ascending m, one element at a time. */
+int or_mc_average(const double* samples, const double* w, int64_t M, int64_t elems, double* out) {
+  double sum = 0.0;
+  for (int64_t m = 0; m < M; ++m) sum += w[m];
+  if (fabs(sum - 1.0) > 1e-9) {
+    set_err("mc_average: weights must sum to 1");
+    return 4;
+  }
+  for (int64_t e = 0; e < elems; ++e) out[e] = 0.0;
+  for (int64_t m = 0; m < M; ++m) {
+    const double* smp = samples + m * elems;
+    const double wm = w[m];
+    for (int64_t e = 0; e < elems; ++e) out[e] = out[e] + wm * smp[e];
+  }
+  return 0;
+}
+
+/* The tail of one denoising step for given weights: sample_batch
+ * (denoiser.cpp:39-46, sample_m = mean_scale·variable + std·z_m) formed one
+ * sample at a time, mc_average (:92-108) in ascending m, then denoise_step
+ * (:110-117) variable' = update_scale·average.  Same arithmetic as
+ * or_denoise_step's tail without holding the M sample matrices. */
+int or_weighted_update(const double* variable, const double* noise, const double* w, int64_t M, int64_t elems,
+                       double mean_scale, double std_dev, double update_scale, double* out) {
+  double sum = 0.0;
+  for (int64_t m = 0; m < M; ++m) sum += w[m];
+  if (fabs(sum - 1.0) > 1e-9) {
+    set_err("mc_average: weights must sum to 1");
+    return 4;
+  }
+  double* acc = (double*)calloc((size_t)elems, sizeof(double));
+  for (int64_t m = 0; m < M; ++m) {
+    const double* z = noise + m * elems;
+    const double wm = w[m];
+    for (int64_t e = 0; e < elems; ++e) {
+      const double smp = mean_scale * variable[e] + std_dev * z[e];
+      acc[e] = acc[e] + wm * smp;
+    }
+  }
+  for (int64_t e = 0; e < elems; ++e) out[e] = update_scale * acc[e];
+  free(acc);
+  return 0;
+}
+
 /* run_denoising (denoiser.cpp:119-184) */
 int or_run_denoising(const or_problem* p, const double* base, const or_denoiser_config* cfg,
                      double* variable, or_trace_rec* trace) {

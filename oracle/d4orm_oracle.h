@@ -126,6 +126,14 @@ int or_denoise_step(const or_problem* p, const double* base, const double* alpha
                     const or_denoiser_config* cfg, int i, double* variable, const double* noise,
                     double* rewards_out, double* weights_out, or_trace_rec* rec);
 
+/* mc_average (denoiser.cpp:92-108): samples M x elems, ascending-m sum.
+ * Returns 0, or 4 when |Σw − 1| > 1e-9. */
+int or_mc_average(const double* samples, const double* w, int64_t M, int64_t elems, double* out);
+/* sample_batch (denoiser.cpp:39-46) + mc_average + denoise_step (:110-117)
+ * for given weights: out = update_scale · Σ_m w_m (mean_scale·variable + std·z_m). */
+int or_weighted_update(const double* variable, const double* noise, const double* w, int64_t M, int64_t elems,
+                       double mean_scale, double std_dev, double update_scale, double* out);
+
 /* run_denoising (denoiser.cpp:119-184).  trace has cfg->steps records. */
 int or_run_denoising(const or_problem* p, const double* base, const or_denoiser_config* cfg,
                      double* variable_out, or_trace_rec* trace);

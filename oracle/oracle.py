@@ -148,6 +148,8 @@ class Oracle(_Base):
         L.or_denoise_step.argtypes = [C.POINTER(OrProblem), dp, dp, C.POINTER(OrConfig), C.c_int, dp, dp, dp, dp,
                                       C.POINTER(OrTrace)]
         L.or_run_denoising.argtypes = [C.POINTER(OrProblem), dp, C.POINTER(OrConfig), dp, C.POINTER(OrTrace)]
+        L.or_mc_average.argtypes = [dp, dp, i64, i64, dp]
+        L.or_weighted_update.argtypes = [dp, dp, dp, i64, i64, C.c_double, C.c_double, C.c_double, dp]
         L.or_solve.argtypes = [C.POINTER(OrProblem), C.POINTER(OrConfig), C.POINTER(OrOptConfig), dp, dp, dp,
                                C.POINTER(C.c_int), C.POINTER(OrIterStats), C.POINTER(OrTrace)]
         L.or_select_elites.argtypes = [dp, i64, C.c_int, C.POINTER(C.c_int)]
@@ -253,6 +255,28 @@ class Oracle(_Base):
         if rc:
             raise RuntimeError(self.err())
         return var, rw, w, (rec.step, rec.best_reward, rec.mean_reward, rec.weight_entropy)
+
+    def mc_average(self, samples, weights):
+        """mc_average (denoiser.cpp:92-108) of M sample rows."""
+        smp = np.ascontiguousarray(samples, dtype=np.float64)
+        M = smp.shape[0]
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        out = np.empty(smp.shape[1:])
+        if self.L.or_mc_average(_dp(smp), _dp(w), M, smp[0].size, _dp(out)):
+            raise ValueError(self.err())
+        return out
+
+    def weighted_update(self, variable, noise, weights, mean_scale, std_dev, update_scale):
+        """sample_batch + mc_average + denoise_step for given weights:
+        update_scale · Σ_m w_m (mean_scale·variable + std_dev·z_m)."""
+        var = np.ascontiguousarray(variable, dtype=np.float64)
+        nz = np.ascontiguousarray(noise, dtype=np.float64).reshape(len(weights), var.size)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        out = np.empty_like(var)
+        if self.L.or_weighted_update(_dp(var), _dp(nz), _dp(w), len(w), var.size, mean_scale, std_dev,
+                                     update_scale, _dp(out)):
+            raise ValueError(self.err())
+        return out
 
     def run_denoising(self, p, base, cfg: OrConfig):
         s, keep = make_problem(p)

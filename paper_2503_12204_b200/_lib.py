@@ -26,6 +26,7 @@ EXPORTS = (
     "d4orm_cuda_run_denoising", "d4orm_cuda_denoise_step", "d4orm_cuda_rollout_fitness",
     "d4orm_cuda_score_weights", "d4orm_cuda_philox_noise", "d4orm_cuda_bench_steps",
     "d4orm_cuda_launches_per_step", "d4orm_cuda_solve", "d4orm_cuda_mppi_solve", "d4orm_cuda_cem_solve",
+    "d4orm_cuda_weighted_mean",
 )
 
 
@@ -106,6 +107,7 @@ def lib() -> C.CDLL:
     L.d4orm_cuda_rollout_fitness.argtypes = [vp, dp, i64, dp, dp, dp, C.POINTER(C.c_int64)]
     L.d4orm_cuda_score_weights.argtypes = [vp, dp, i64, C.c_double, dp, dp]
     L.d4orm_cuda_philox_noise.argtypes = [vp, C.c_uint64, i32, i64, i64, C.POINTER(C.c_float)]
+    L.d4orm_cuda_weighted_mean.argtypes = [vp, dp, dp, i64, i64, dp]
     L.d4orm_cuda_bench_steps.argtypes = [vp, dp, C.POINTER(DenoiserConfig_C), i32, i32, dp, dp]
     L.d4orm_cuda_launches_per_step.argtypes = [vp]
     L.d4orm_cuda_fitness_path.argtypes = [vp]

@@ -1736,6 +1736,69 @@ int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t
   return D4ORM_OK;
 }
 
+// mc_average (denoiser.cpp:92-108) on the device: K5a (chunk partials, each
+// the ascending-m sum of its 256 samples) + K5b (the pairwise tree) with a
+// pass-through finalisation.  Sample rows are uploaded as z with msv = 0 and
+// sd = 1, so every sample enters unchanged (0 + 1·z = z in both precisions).
+extern "C++" template <typename S>
+int weighted_mean_t(d4orm_cuda_ctx* ctx, const double* samples, const double* weights, int64_t m, int64_t E,
+                    double* out) {
+  if (m < 1) return fail(ctx, D4ORM_E_INVALID, "mc_average: empty sample set");
+  if (E < 1) return fail(ctx, D4ORM_E_INVALID, "mc_average: empty samples");
+  double sum = 0.0;
+  for (int64_t j = 0; j < m; ++j) sum += weights[j];
+  if (std::abs(sum - 1.0) > 1e-9) return fail(ctx, D4ORM_E_INVALID, "mc_average: weights must sum to 1");
+  const int64_t chunks = (m + kChunk - 1) / kChunk;
+  CU(ctx->z[0].ensure((size_t)m * E * sizeof(S)));
+  CU(ctx->msv.ensure((size_t)E * sizeof(S)));
+  CU(ctx->base.ensure((size_t)E * sizeof(S)));
+  CU(ctx->partial.ensure((size_t)chunks * E * sizeof(S)));
+  CU(ctx->var.ensure((size_t)E));
+  CU(ctx->w64.ensure((size_t)m));
+  CU(ctx->w32.ensure((size_t)m));
+  CU((upload_as<S>(ctx->z[0], samples, (size_t)m * E, ctx->s_main)));
+  CU(cudaMemsetAsync(ctx->msv.p, 0, E * sizeof(S), ctx->s_main));
+  CU(cudaMemsetAsync(ctx->base.p, 0, E * sizeof(S), ctx->s_main));
+  const bool f64 = std::is_same<S, double>::value;
+  if (f64) {
+    CU(cudaMemcpyAsync(ctx->w64.p, weights, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->s_main));
+  } else {
+    std::vector<float> w32((size_t)m);
+    for (int64_t j = 0; j < m; ++j) w32[j] = (float)weights[j];
+    CU(cudaMemcpyAsync(ctx->w32.p, w32.data(), sizeof(float) * m, cudaMemcpyHostToDevice, ctx->s_main));
+    CU(cudaStreamSynchronize(ctx->s_main));
+  }
+  RunShape rs;
+  rs.M = rs.Ml = m;
+  rs.E = E;
+  rs.chunks_local = chunks;
+  StepConsts sc;  // sd = 1
+  d4k::TreeFinal<S> fin{};
+  fin.mode = d4k::FIN_UPDATE;  // var ← 1·total (msv/bm scratch)
+  fin.scale = 1.0;
+  fin.next_ms = 0.0;
+  fin.var = ctx->var.p;
+  fin.msv = (S*)ctx->msv.p;
+  fin.base = (const S*)ctx->base.p;
+  fin.bm = nullptr;
+  ncclComm_t comm = ctx->comm;  // single-process operator: no root exchange
+  ctx->comm = nullptr;
+  ctx->k5_regen = false;
+  const int r = enqueue_reduce<S>(ctx, rs, sc, 0, fin, false);
+  ctx->comm = comm;
+  if (r) return r;
+  CU(cudaStreamSynchronize(ctx->s_main));
+  CU(cudaMemcpy(out, ctx->var.p, sizeof(double) * E, cudaMemcpyDeviceToHost));
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_weighted_mean(d4orm_cuda_ctx* ctx, const double* samples, const double* weights, int64_t m,
+                             int64_t elems, double* out) {
+  CU(cudaSetDevice(ctx->device));
+  return ctx->precision == D4ORM_PREC_F64 ? weighted_mean_t<double>(ctx, samples, weights, m, elems, out)
+                                          : weighted_mean_t<float>(ctx, samples, weights, m, elems, out);
+}
+
 int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_t m0, int64_t count, float* out) {
   CU(cudaSetDevice(ctx->device));
   if (!ctx->has_problem) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: set_problem not called");

@@ -6,16 +6,18 @@
 //   rollout / batch_rollout → d4orm_cuda_rollout_fitness (GPU, fp64 parity
 //                     instantiation: the reference's arithmetic)
 //   score_weights   → d4orm_cuda_score_weights (GPU K4)
+//   mc_average      → d4orm_cuda_weighted_mean (GPU K5a + K5b, fp64)
 //   iterate / solve → the anytime loop (optimizer.cpp:19-102) driving the above
 //
 // Single-trajectory utilities (total_reward/objective/check_success on a given
-// trajectory, derivative/rk4_step on one state, sample_batch/mc_average on host
-// matrices, the scenario generators) run on the host exactly as the reference
+// trajectory, derivative/rk4_step on one state, sample_batch on host matrices,
+// the scenario generators) run on the host exactly as the reference
 // defines them; none of them is on the per-step path.  Errors come back as the
 // reference's exception types with its messages.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <memory>
@@ -41,7 +43,21 @@ namespace d4orm {
 // ================================================================ GPU context
 namespace {
 
-thread_local GpuOptions g_opts;
+// Defaults from the environment, so a caller compiled unchanged against the
+// reference headers (which has no set_gpu_options call — e.g. the reference's
+// own tools/main.cpp, INTEGRATION.md Option A) can still pick the mode:
+//   D4ORM_DEVICE=<n>, D4ORM_PRECISION=f32|f64, D4ORM_NOISE=philox|host,
+//   D4ORM_GRAPHS=0|1.  Unset: device 0, fp32, Philox, graphs.
+GpuOptions env_defaults() {
+  GpuOptions o;
+  if (const char* e = std::getenv("D4ORM_DEVICE")) o.device = std::atoi(e);
+  if (const char* e = std::getenv("D4ORM_PRECISION")) o.precision = std::strcmp(e, "f64") == 0 ? D4ORM_PREC_F64 : D4ORM_PREC_F32;
+  if (const char* e = std::getenv("D4ORM_NOISE")) o.host_noise = std::strcmp(e, "host") == 0;
+  if (const char* e = std::getenv("D4ORM_GRAPHS")) o.graphs = std::atoi(e) != 0;
+  return o;
+}
+
+thread_local GpuOptions g_opts = env_defaults();
 
 struct CtxDeleter {
   void operator()(d4orm_cuda_ctx* c) const { d4orm_cuda_destroy(c); }
@@ -153,7 +169,8 @@ int host_noise_fn(void* user, int step, int64_t m0, int64_t count, int64_t elems
   return 0;
 }
 
-d4orm_cuda_ctx* gpu(int which, const ProblemArrays& pa, int precision, int noise, bool graphs) {
+// The slot's context with the given options (created on first use).
+d4orm_cuda_ctx* gpu_ctx(int which, int precision, int noise, bool graphs) {
   GpuSlot& s = g_slot[which];
   const GpuOptions& o = g_opts;
   if (!s.ctx || s.device != o.device) {
@@ -174,6 +191,13 @@ d4orm_cuda_ctx* gpu(int which, const ProblemArrays& pa, int precision, int noise
     s.noise = noise;
     s.graphs = graphs ? 1 : 0;
   }
+  return c;
+}
+
+// ... and the problem uploaded (only when it changed).
+d4orm_cuda_ctx* gpu(int which, const ProblemArrays& pa, int precision, int noise, bool graphs) {
+  GpuSlot& s = g_slot[which];
+  d4orm_cuda_ctx* c = gpu_ctx(which, precision, noise, graphs);
   if (s.problem_key != pa.key) {
     throw_for(d4orm_cuda_set_problem(c, &pa.p), d4orm_cuda_last_error(c));
     s.problem_key = pa.key;
@@ -580,15 +604,24 @@ Vector score_weights(const Vector& rewards, double lambda) {
   return w;
 }
 
+// mc_average (denoiser.cpp:92-108) on the GPU (d4orm_cuda_weighted_mean, K5a +
+// K5b) in the reference's fp64 arithmetic: each 256-sample chunk in ascending
+// m, the chunks by a fixed pairwise tree.
 JointControls mc_average(const std::vector<JointControls>& samples, const Vector& weights) {
   if (samples.empty()) throw std::invalid_argument("mc_average: empty sample set");
   if (static_cast<Index>(samples.size()) != weights.size())
     throw std::invalid_argument("mc_average: weight count does not match sample count");
-  double sum = 0.0;
-  for (Index j = 0; j < weights.size(); ++j) sum += weights[j];
-  if (std::abs(sum - 1.0) > 1e-9) throw std::invalid_argument("mc_average: weights must sum to 1");
-  JointControls out{samples[0].robots, samples[0].control_dim, Matrix::Zero(samples[0].u.rows(), samples[0].u.cols())};
-  for (std::size_t m = 0; m < samples.size(); ++m) out.u += weights[static_cast<Index>(m)] * samples[m].u;
+  const Index rows = samples[0].u.rows(), cols = samples[0].u.cols();
+  for (const auto& smp : samples)
+    if (smp.u.rows() != rows || smp.u.cols() != cols)
+      throw std::invalid_argument("mc_average: samples differ in shape");
+  const int64_t m = static_cast<int64_t>(samples.size()), E = static_cast<int64_t>(rows) * cols;
+  JointControls out{samples[0].robots, samples[0].control_dim, Matrix::Zero(rows, cols)};
+  if (E == 0) return out;
+  std::vector<double> flat(static_cast<size_t>(m * E));
+  for (int64_t j = 0; j < m; ++j) std::memcpy(flat.data() + j * E, samples[j].u.data(), sizeof(double) * E);
+  d4orm_cuda_ctx* c = gpu_ctx(1, D4ORM_PREC_F64, D4ORM_NOISE_HOST, false);
+  throw_for(d4orm_cuda_weighted_mean(c, flat.data(), weights.data(), m, E, out.u.data()), d4orm_cuda_last_error(c));
   return out;
 }
 

@@ -174,6 +174,19 @@ class GpuDenoiser:
         self._check(self._L.d4orm_cuda_score_weights(self._h, dptr(r), len(r), lam, dptr(w), dptr(t3)))
         return w, t3
 
+    def weighted_mean(self, samples: np.ndarray, weights: np.ndarray) -> np.ndarray:
+        """mc_average (denoiser.cpp:92-108) on the device (K5a + K5b) in the
+        context's precision: Σ_m w_m·samples[m] → samples.shape[1:]."""
+        smp = np.ascontiguousarray(samples, dtype=np.float64)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        m = smp.shape[0] if smp.ndim else 0
+        if m != len(w):
+            raise ValueError("mc_average: weight count does not match sample count")
+        out = np.empty(smp.shape[1:])
+        self._check(self._L.d4orm_cuda_weighted_mean(self._h, dptr(smp), dptr(w), m, int(np.prod(smp.shape[1:])),
+                                                     dptr(out)))
+        return out
+
     def philox_noise(self, seed: int, step: int, m0: int, count: int) -> np.ndarray:
         out = np.empty((count, self.problem.elems), dtype=np.float32)
         self._check(self._L.d4orm_cuda_philox_noise(self._h, seed, step, m0, count,

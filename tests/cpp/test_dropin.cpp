@@ -104,6 +104,29 @@ int main() {
     const std::vector<int> el = select_elites(rw, 3);
     std::printf("\"elites\": [%d, %d, %d],\n", el[0], el[1], el[2]);
   }
+  // 4c. mc_average (denoiser.cpp:92-108) through the device K5 (fp64)
+  {
+    std::vector<JointControls> smp;
+    const int M = 600;
+    for (int m = 0; m < M; ++m) {
+      JointControls c = JointControls::zeros(3, 2, 5);
+      for (Index j = 0; j < c.u.size(); ++j) c.u.data()[j] = std::sin(0.37 * m + 1.3 * j) * (1.0 + 0.01 * m);
+      smp.push_back(c);
+    }
+    Vector w(M);
+    double tot = 0.0;
+    for (int m = 0; m < M; ++m) tot += (w[m] = std::exp(-0.01 * m));
+    for (int m = 0; m < M; ++m) w[m] /= tot;
+    print_matrix("mc_avg", mc_average(smp, w).u);
+    std::string e;
+    try {
+      w[0] += 0.5;
+      mc_average(smp, w);
+    } catch (const std::invalid_argument& x) {
+      e = x.what();
+    }
+    std::printf("\"mc_err\": \"%s\",\n", e.c_str());
+  }
   // 5. throughput mode (fp32 + Philox) runs and is deterministic
   o.precision = D4ORM_PREC_F32;
   o.host_noise = false;

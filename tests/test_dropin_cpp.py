@@ -80,3 +80,16 @@ def test_baselines_correctness_mode(dropin, oracle):
     assert abs(dropin["cem_best"] - r["best_reward"]) < 1e-9
     np.testing.assert_allclose(np.array(dropin["cem_states"]), r["states"].ravel(), rtol=1e-9, atol=1e-9)
     assert dropin["elites"] == oracle.select_elites(np.array([0.5, 0.9, 0.5, -1.0, 0.9, 0.2, 0.9]), 3) == [1, 4, 6]
+
+
+def test_mc_average_on_device(dropin, oracle):
+    """d4orm::mc_average → d4orm_cuda_weighted_mean (K5a + K5b, fp64) against
+    the oracle's mc_average (pinned bitwise to the reference's)."""
+    M = 600
+    j = np.arange(30)
+    smp = np.stack([np.sin(0.37 * m + 1.3 * j) * (1.0 + 0.01 * m) for m in range(M)])
+    w = np.exp(-0.01 * np.arange(M))
+    w = w / w.sum()
+    want = oracle.mc_average(smp, w)
+    np.testing.assert_allclose(np.array(dropin["mc_avg"]), want, rtol=1e-12, atol=1e-14)
+    assert dropin["mc_err"] == "mc_average: weights must sum to 1"

@@ -195,6 +195,45 @@ def test_pin_sample_batch(oracle, reference):
     np.testing.assert_array_equal(got, want)
 
 
+def test_pin_mc_average_and_weighted_update(oracle, reference):
+    """or_mc_average is the reference's mc_average bitwise; or_weighted_update
+    (sample_batch + mc_average + denoise_step for given weights, the stage the
+    fp32 GPU parity tests feed the GPU's own rewards through) equals
+    sqrt(ab[i-1]) * mc_average(sample_batch(...)) of the reference bitwise."""
+    p = PIN_PROBLEMS["C2"]()
+    M, N, i, seed = 37, 10, 6, 99
+    cur = np.random.default_rng(4).normal(size=(p.horizon, p.robots, p.du))
+    smp = reference.sample_batch(p, cur, N, 0.05, i, M, seed)
+    w = oracle.score_weights(np.random.default_rng(5).normal(size=M), 0.1)
+    want = reference.mc_average(smp, w)
+    np.testing.assert_array_equal(oracle.mc_average(smp, w), want)
+    ab, _ = oracle.make_schedule(N, 0.05)
+    ms, sd = reference.sampling_spread(N, 0.05, i)
+    z = oracle.step_noise(seed, i, 0, M, p.elems)
+    got = oracle.weighted_update(cur, z, w, ms, sd, math.sqrt(ab[i - 1]))
+    np.testing.assert_array_equal(got, math.sqrt(ab[i - 1]) * want)
+    with pytest.raises(ValueError, match="weights must sum to 1"):
+        oracle.mc_average(smp, w * 1.01)
+
+
+def test_oracle_step_chain_equals_run_denoising(oracle):
+    """The GPU free-running parity tests drive the oracle one denoise_step at a
+    time with given noise; that chain is run_denoising bitwise."""
+    p = PIN_PROBLEMS["C4"]()
+    N, M, seed = 5, 40, 12
+    base = np.random.default_rng(6).normal(size=(p.horizon, p.robots, p.du)) * 0.3
+    cfg = make_config(N, M, seed=seed, workers=2)
+    want, tr_want = oracle.run_denoising(p, base, cfg)
+    ab, _ = oracle.make_schedule(N, 0.05)
+    v = np.zeros_like(base)
+    tr = []
+    for i in range(N, 0, -1):
+        v, _, _, rec = oracle.denoise_step(p, base, v, ab, cfg, i, oracle.step_noise(seed, i, 0, M, p.elems))
+        tr.append(rec)
+    np.testing.assert_array_equal(v, want)
+    assert tr == tr_want
+
+
 @pytest.mark.parametrize("name", ["holo2d", "C3"])
 def test_pin_solve(oracle, reference, name):
     p = PIN_PROBLEMS[name]()
