@@ -185,6 +185,26 @@ def run_reference_arm(args, rc, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    so = socket.socket()
+    so.bind(("127.0.0.1", 0))
+    port = so.getsockname()[1]
+    so.close()
+    return port
+
+
+def self_launch(args_list, n: int) -> int:
+    """--gpus N without a launcher: start N ranks (one process per GPU) with
+    torch.distributed.run on this node, exactly as the driver would, and pass
+    the exit code through.  Rank 0 prints the JSON line."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()), *args_list]
+    sys.stderr.write("bench.py: self-launching %d ranks: %s\n" % (n, " ".join(cmd)))
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -197,12 +217,30 @@ def main():
     ap.add_argument("--graphs", type=int, default=1)
     ap.add_argument("--force-comm", action="store_true",
                     help="N = 1 through the sharded protocol (1-rank NCCL communicator): exercises the N > 1 path")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check: every rank prints its rank/world/device as JSON and exits (no GPU work)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(sys.argv[1:], args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: refusing to measure a different "
+                         f"GPU count than asked\n")
+        sys.exit(2)
+    if args.dry_run:
+        print(json.dumps({"dry_run": True, "rank": rank, "world": world, "local_rank": local_rank,
+                          "device": f"cuda:{local_rank}", "impl": args.impl,
+                          "master": f"{os.environ.get('MASTER_ADDR', '-')}:{os.environ.get('MASTER_PORT', '-')}"}),
+              flush=True)
+        return
+    if world > 1:
+        # the NCCL communicator-init lines (one "Init COMPLETE" per rank) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     from paper_2503_12204_b200 import scenarios as S
     rc = S.baseline_config(args.config)
 
@@ -232,6 +270,9 @@ def main():
     Ml = M // world
     g = d4.GpuDenoiser(p, device=local_rank, rank=rank, world=world, nccl_id=nccl_id, precision=d4.PREC_F32,
                        noise=d4.NOISE_PHILOX, graphs=bool(args.graphs))
+    if world > 1:
+        sys.stderr.write(f"bench.py: rank {rank}/{world} on cuda:{local_rank}: NCCL communicator initialised "
+                         f"(samples [{rank * Ml}, {(rank + 1) * Ml}))\n")
     cfg = d4.DenoiserConfig(steps=rc.steps, batch=M, lam=rc.lam, alpha_bar_final=rc.alpha_bar_final, seed=rc.seed)
     base = np.zeros((p.horizon, p.robots, p.du))
 

@@ -102,6 +102,14 @@ typedef struct d4orm_cuda_ctx d4orm_cuda_ctx;
  * nccl_id is the 128-byte ncclUniqueId rank 0 created (d4orm_cuda_nccl_id),
  * broadcast by the caller.  world == 1: nccl_id may be NULL. */
 int d4orm_cuda_create(int device, int rank, int world, const void* nccl_id, d4orm_cuda_ctx** out);
+/* world > 1 without NCCL (nccl_id NULL): the step's two all-gathers (rewards,
+ * chunk-tree roots) go through fn, which must block until `gathered`
+ * (world x bytes, rank order) holds every rank's `local` block and return 0
+ * (e.g. MPI_Allgather, or torch.distributed over gloo).  Runs of such a
+ * context launch no CUDA graphs (the exchange is a host call mid-step).  The
+ * per-rank batch must be 256 x a power of two samples whenever world > 1. */
+typedef int (*d4orm_exchange_fn)(void* user, const void* local, int64_t bytes, void* gathered);
+int d4orm_cuda_set_exchange_fn(d4orm_cuda_ctx* ctx, d4orm_exchange_fn fn, void* user);
 int d4orm_cuda_nccl_id(void* out128);
 void d4orm_cuda_destroy(d4orm_cuda_ctx* ctx);
 const char* d4orm_cuda_last_error(const d4orm_cuda_ctx* ctx);

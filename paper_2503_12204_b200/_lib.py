@@ -26,7 +26,7 @@ EXPORTS = (
     "d4orm_cuda_run_denoising", "d4orm_cuda_denoise_step", "d4orm_cuda_rollout_fitness",
     "d4orm_cuda_score_weights", "d4orm_cuda_philox_noise", "d4orm_cuda_bench_steps",
     "d4orm_cuda_launches_per_step", "d4orm_cuda_solve", "d4orm_cuda_mppi_solve", "d4orm_cuda_cem_solve",
-    "d4orm_cuda_weighted_mean",
+    "d4orm_cuda_weighted_mean", "d4orm_cuda_set_exchange_fn",
 )
 
 
@@ -77,6 +77,7 @@ class CemConfig_C(C.Structure):
 
 
 NOISE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_double))
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 _lib = None
 
@@ -101,6 +102,7 @@ def lib() -> C.CDLL:
     L.d4orm_cuda_set_problem.argtypes = [vp, C.POINTER(Problem_C)]
     L.d4orm_cuda_set_options.argtypes = [vp, i32, i32, i32]
     L.d4orm_cuda_set_noise_fn.argtypes = [vp, NOISE_FN, vp]
+    L.d4orm_cuda_set_exchange_fn.argtypes = [vp, EXCHANGE_FN, vp]
     L.d4orm_cuda_run_denoising.argtypes = [vp, dp, C.POINTER(DenoiserConfig_C), dp, C.POINTER(TraceRec_C)]
     L.d4orm_cuda_denoise_step.argtypes = [vp, dp, dp, dp, i32, C.POINTER(DenoiserConfig_C), dp, dp, dp,
                                           C.POINTER(TraceRec_C)]

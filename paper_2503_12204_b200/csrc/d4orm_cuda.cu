@@ -141,6 +141,9 @@ struct d4orm_cuda_ctx {
   int precision = D4ORM_PREC_F32, noise_source = D4ORM_NOISE_PHILOX, use_graphs = 1;
   d4orm_noise_fn noise_fn = nullptr;
   void* noise_user = nullptr;
+  // world > 1 without NCCL: host-mediated all-gathers (d4orm_cuda_set_exchange_fn)
+  d4orm_exchange_fn xfn = nullptr;
+  void* xuser = nullptr;
 
   // device buffers (typeless where the scalar type varies)
   DevBuf<unsigned char> z[2], base, msv, bm, starts_d, goals_d, inv_d, obs_d, ocl_d, opl_d, partial, roots;
@@ -220,6 +223,30 @@ int fail(d4orm_cuda_ctx* c, int code, const char* fmt, ...) {
     if (r_ != 0) return fail(ctx, D4ORM_E_NCCL, "NCCL error %s at %s:%d", g_nccl.GetErrorString(r_), \
                              __FILE__, __LINE__);                                                      \
   } while (0)
+
+// The step's two exchanges go over NCCL (captured in the step graph) or, for
+// world > 1 without NCCL, through the caller's host exchange function (the
+// stream is synchronised around it, so such runs use no graphs).
+bool sharded(const d4orm_cuda_ctx* c) { return c->comm != nullptr || (c->world > 1 && c->xfn != nullptr); }
+bool graphs_on(const d4orm_cuda_ctx* c) { return c->use_graphs && !(c->comm == nullptr && c->xfn != nullptr && c->world > 1); }
+
+// All-gather of `count` elements of `esz` bytes from every rank (rank order)
+// into recv; send may alias recv's own slot.
+int all_gather(d4orm_cuda_ctx* ctx, const void* send, void* recv, size_t count, size_t esz, int type) {
+  if (ctx->comm) {
+    NC(g_nccl.AllGather(send, recv, count, type, ctx->comm, ctx->s_main));
+    return D4ORM_OK;
+  }
+  const size_t bytes = count * esz;
+  std::vector<unsigned char> loc(bytes), all(bytes * (size_t)ctx->world);
+  CU(cudaMemcpyAsync(loc.data(), send, bytes, cudaMemcpyDeviceToHost, ctx->s_main));
+  CU(cudaStreamSynchronize(ctx->s_main));
+  if (ctx->xfn(ctx->xuser, loc.data(), (int64_t)bytes, all.data()) != 0)
+    return fail(ctx, D4ORM_E_RUNTIME, "d4orm_cuda: exchange fn failed on rank %d", ctx->rank);
+  CU(cudaMemcpyAsync(recv, all.data(), all.size(), cudaMemcpyHostToDevice, ctx->s_main));
+  CU(cudaStreamSynchronize(ctx->s_main));
+  return D4ORM_OK;
+}
 
 bool dims_of(int kind, int* dx, int* du, int* pd) {
   static const int DX[6] = {4, 4, 6, 2, 3, 3}, DU[6] = {2, 2, 3, 2, 3, 2}, PD[6] = {2, 2, 3, 2, 3, 2};
@@ -483,8 +510,19 @@ int check_config(d4orm_cuda_ctx* ctx, const d4orm_denoiser_config* c, RunShape* 
   rs->M = c->batch;
   rs->Ml = c->batch / ctx->world;
   rs->m0 = rs->Ml * ctx->rank;
-  if (ctx->world > 1 && rs->Ml % kChunk != 0)
-    return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: per-rank batch must be a multiple of %d", kChunk);
+  if (ctx->world > 1 && !sharded(ctx))
+    return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: world %d needs an NCCL id or an exchange fn", ctx->world);
+  // G-invariance: a rank's chunk partials must form one
+  // complete subtree of the single-GPU pairwise tree, i.e. each rank owns a
+  // power-of-two count of whole 256-sample chunks (any world size then works:
+  // the tree over the G roots is the top of the single-GPU tree).
+  if (ctx->world > 1) {
+    const int64_t ch = rs->Ml / kChunk;
+    if (rs->Ml % kChunk != 0 || (ch & (ch - 1)) != 0)
+      return fail(ctx, D4ORM_E_INVALID,
+                  "d4orm_cuda: per-rank batch %lld must be %d x a power of two samples (world %d)",
+                  (long long)rs->Ml, kChunk, ctx->world);
+  }
   rs->E = elems_of(ctx);
   rs->chunks_local = (rs->Ml + kChunk - 1) / kChunk;
   rs->N = c->steps;
@@ -561,8 +599,52 @@ int launch_noise(d4orm_cuda_ctx* ctx, cudaStream_t st, int64_t count, int64_t m0
   return D4ORM_OK;
 }
 
+// fp32 candidates are clamped with FMNMX, which turns a NaN control into the
+// bound; the reference (and the fp64 path) propagate it to a non-finite state
+// and throw for the first failing sample (parallel.hpp:31-44, lowest index
+// here) at its first robot k (rollout_robot runs robots in order) and first
+// step t+1 whose control is NaN (dynamics.cpp:76-84).  So the fp32 path scans
+// what it uploads: `bv` marks elements where base or variable is NaN (every
+// sample fails there), z is this step's noise of samples m0.. .
+struct NanHit {
+  int64_t m = -1;
+  int k = 0, t = 0;
+};
+NanHit first_nan(const d4orm_problem& p, const std::vector<unsigned char>* bv, const double* z, int64_t count,
+                 int64_t m0) {
+  NanHit h;
+  const int64_t E = (int64_t)p.robots * p.du * p.horizon;
+  for (int64_t j = 0; j < count; ++j) {
+    bool any = false;
+    if (bv)
+      for (int64_t e = 0; e < E && !any; ++e) any = (*bv)[e] != 0;
+    if (z)
+      for (int64_t e = 0; e < E && !any; ++e) any = std::isnan(z[j * E + e]);
+    if (!any) continue;
+    for (int k = 0; k < p.robots; ++k)
+      for (int t = 0; t < p.horizon; ++t)
+        for (int d = 0; d < p.du; ++d) {
+          const int64_t e = ((int64_t)t * p.robots + k) * p.du + d;
+          if ((bv && (*bv)[e]) || (z && std::isnan(z[j * E + e]))) {
+            h.m = m0 + j;
+            h.k = k;
+            h.t = t + 1;
+            return h;
+          }
+        }
+  }
+  return h;
+}
+
+int nan_error(d4orm_cuda_ctx* ctx, const NanHit& h, int step, bool baseline) {
+  if (baseline)  // a sample rollout of MPPI / CEM (baselines.cpp:34, 120)
+    return fail(ctx, D4ORM_E_RUNTIME, "rollout: non-finite state for robot %d at step %d", h.k, h.t);
+  return fail(ctx, D4ORM_E_RUNTIME, "run_denoising: sample %lld at step %d: rollout: non-finite state for robot %d at step %d",
+              (long long)h.m, step, h.k, h.t);
+}
+
 int host_noise(d4orm_cuda_ctx* ctx, const RunShape& rs, int step, int64_t m0, int64_t count, const double* given,
-               void* dst) {
+               void* dst, bool baseline = false) {
   std::vector<double> buf;
   const double* src = given;
   if (!src) {
@@ -578,7 +660,12 @@ int host_noise(d4orm_cuda_ctx* ctx, const RunShape& rs, int step, int64_t m0, in
     CU(cudaStreamSynchronize(ctx->s_main));
   } else {
     std::vector<float> f(n);
-    for (size_t j = 0; j < n; ++j) f[j] = (float)src[j];
+    bool nan = false;
+    for (size_t j = 0; j < n; ++j) {
+      f[j] = (float)src[j];
+      nan |= std::isnan(src[j]);
+    }
+    if (nan) return nan_error(ctx, first_nan(ctx->prob, nullptr, src, count, m0), step, baseline);
     CU(cudaMemcpyAsync(dst, f.data(), n * sizeof(float), cudaMemcpyHostToDevice, ctx->s_main));
     CU(cudaStreamSynchronize(ctx->s_main));
   }
@@ -656,8 +743,9 @@ int enqueue_fitness(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
   if (ctx->k5_regen) f.z_keep = 2;
   CU(launch_fit<S>(ctx, f, smem, fused));
   if (timing) CU(cudaEventRecord(ctx->ev_k[1], ctx->s_main));
-  if (ctx->comm) {
-    NC(g_nccl.AllGather(ctx->rewards.p + rs.m0, ctx->rewards.p, (size_t)rs.Ml, ncclFloat64, ctx->comm, ctx->s_main));
+  if (sharded(ctx)) {
+    if (int r = all_gather(ctx, ctx->rewards.p + rs.m0, ctx->rewards.p, (size_t)rs.Ml, sizeof(double), ncclFloat64))
+      return r;
   }
   return D4ORM_OK;
 }
@@ -749,7 +837,7 @@ int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc
   CU(cudaGetLastError());
   if (timing) CU(cudaEventRecord(ctx->ev_k[3], ctx->s_main));
   const unsigned tgrid = (unsigned)((rs.E + d4k::kThreads - 1) / d4k::kThreads);
-  if (!ctx->comm) {
+  if (!sharded(ctx)) {
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
                                                                    fin, nullptr);
   } else {
@@ -757,7 +845,9 @@ int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
                                                                    fin, my_root);
     CU(cudaGetLastError());
-    NC(g_nccl.AllGather(my_root, ctx->roots.p, (size_t)rs.E, f64 ? ncclFloat64 : ncclFloat32, ctx->comm, ctx->s_main));
+    if (int r = all_gather(ctx, my_root, ctx->roots.p, (size_t)rs.E, f64 ? sizeof(double) : sizeof(float),
+                           f64 ? ncclFloat64 : ncclFloat32))
+      return r;
     d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->roots.p, ctx->world, rs.E, fin,
                                                                    nullptr);
   }
@@ -840,6 +930,12 @@ int prologue(d4orm_cuda_ctx* ctx, const RunShape& rs, const double* base_host, c
         return fail(ctx, D4ORM_E_RUNTIME, "d4orm_cuda: noise fn failed at step 0");
     }
   }
+  if (!std::is_same<S, double>::value) {  // a NaN initial draw (host provider) fails every sample at step N
+    std::vector<unsigned char> bv((size_t)E);
+    bool any = false;
+    for (int64_t e = 0; e < E; ++e) any |= (bv[e] = (unsigned char)std::isnan(v[e]));
+    if (any) return nan_error(ctx, first_nan(ctx->prob, &bv, nullptr, 1, 0), rs.N, false);
+  }
   CU(cudaMemcpyAsync(ctx->var.p, v.data(), sizeof(double) * E, cudaMemcpyHostToDevice, ctx->s_main));
   CU(init_msv<S>(ctx, E, 1.0 / std::sqrt(ctx->ab[rs.N])));
   const unsigned long long init = ~0ull;
@@ -894,7 +990,7 @@ int run_steps(d4orm_cuda_ctx* ctx, const RunShape& rs, bool philox, int i_begin,
     if (!philox) {
       if (int r = host_noise(ctx, rs, i, rs.m0, rs.Ml, given_noise, ctx->z[0].p)) return r;
     }
-    if (philox && ctx->use_graphs) {
+    if (philox && graphs_on(ctx)) {
       CU(cudaGraphLaunch(ctx->graphs[i].exec, ctx->s_main));
     } else {
       if (int r = enqueue_step<S>(ctx, rs, i, philox, false)) return r;
@@ -928,7 +1024,7 @@ int run_denoising_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoise
   const bool philox = ctx->noise_source == D4ORM_NOISE_PHILOX;
   if (int r = ensure_buffers(ctx, rs, false, philox)) return r;
   if (int r = prologue<S>(ctx, rs, base, c, philox)) return r;
-  if (philox && ctx->use_graphs) {
+  if (philox && graphs_on(ctx)) {
     if (int r = ensure_graphs<S>(ctx, rs)) return r;
   }
   if (int r = run_steps<S>(ctx, rs, philox, rs.N, 1, nullptr)) return r;
@@ -1110,7 +1206,7 @@ int solve_t(d4orm_cuda_ctx* ctx, const d4orm_solve_config* sc, double* best_stat
     CU(cudaMemcpyAsync(ctx->sst.p, &st0, sizeof st0, cudaMemcpyHostToDevice, ctx->s_main));
     CU(cudaStreamSynchronize(ctx->s_main));
   }
-  const bool graphs = philox && ctx->use_graphs;
+  const bool graphs = philox && graphs_on(ctx);
   if (graphs) {
     if (int r = ensure_iter_graph<S>(ctx, rs, sc)) return r;
   }
@@ -1207,7 +1303,7 @@ int enqueue_baseline_iteration(d4orm_cuda_ctx* ctx, const RunShape& rs, const Ba
                                                     ctx->errw.p);
   CU(cudaGetLastError());
   if (!philox) {  // host noise of iteration it: NormalStream(mix_seed(seed, it, m))
-    if (int r = host_noise(ctx, rs, it, rs.m0, rs.Ml, nullptr, ctx->z[0].p)) return r;
+    if (int r = host_noise(ctx, rs, it, rs.m0, rs.Ml, nullptr, ctx->z[0].p, true)) return r;
   }
   StepConsts sc;
   sc.sd = b.sigma;
@@ -1324,7 +1420,7 @@ int baseline_solve_t(d4orm_cuda_ctx* ctx, BaselineSpec b, double* best_states, d
     }
     CU(cudaStreamSynchronize(ctx->s_main));
   }
-  const bool graphs = philox && ctx->use_graphs;
+  const bool graphs = philox && graphs_on(ctx);
   if (graphs) {
     char extra[200];
     snprintf(extra, sizeof extra, "|baseline/%d/%.17g/%.17g/%lld/%.17g/%d/%p/%p/%p/%p/%p", b.cem ? 1 : 0, b.sigma,
@@ -1413,19 +1509,16 @@ int d4orm_cuda_create(int device, int rank, int world, const void* nccl_id, d4or
   CU(cudaEventCreate(&c->ev_t1));
   c->ev_k.resize(5);
   for (auto& e : c->ev_k) CU(cudaEventCreate(&e));
-  if (world > 1 || nccl_id) {  // a 1-rank communicator exercises the same protocol on one GPU
+  if (nccl_id) {  // (world 1: a 1-rank communicator exercises the same protocol on one GPU)
     std::string e;
-    if (!g_nccl.load(&e) || !nccl_id) {
-      c.release();
-      return D4ORM_E_NCCL;
-    }
+    if (!g_nccl.load(&e)) return D4ORM_E_NCCL;
     ncclUniqueId id;
     std::memcpy(&id, nccl_id, sizeof id);
     if (g_nccl.CommInitRank(&c->comm, world, id, rank) != 0) {
-      c.release();
+      c->comm = nullptr;
       return D4ORM_E_NCCL;
     }
-  }
+  }  // world > 1 without an id: d4orm_cuda_set_exchange_fn before the first run
   *out = c.release();
   return D4ORM_OK;
 }
@@ -1453,6 +1546,13 @@ int d4orm_cuda_set_options(d4orm_cuda_ctx* ctx, int precision, int noise_source,
 int d4orm_cuda_set_noise_fn(d4orm_cuda_ctx* ctx, d4orm_noise_fn fn, void* user) {
   ctx->noise_fn = fn;
   ctx->noise_user = user;
+  return D4ORM_OK;
+}
+
+int d4orm_cuda_set_exchange_fn(d4orm_cuda_ctx* ctx, d4orm_exchange_fn fn, void* user) {
+  if (ctx->comm) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: the context already exchanges over NCCL");
+  ctx->xfn = fn;
+  ctx->xuser = user;
   return D4ORM_OK;
 }
 
@@ -1589,6 +1689,12 @@ int denoise_step_t(d4orm_cuda_ctx* ctx, const double* base, const double* var_in
   const int64_t E = rs.E;
   std::vector<double> b(E, 0.0);
   if (rs.mode == D4ORM_DEFORMATION) std::memcpy(b.data(), base, sizeof(double) * E);
+  if (!std::is_same<S, double>::value) {  // NaN in base / variable: every sample fails (see first_nan)
+    std::vector<unsigned char> bv((size_t)E);
+    bool any = false;
+    for (int64_t e = 0; e < E; ++e) any |= (bv[e] = (unsigned char)(std::isnan(b[e]) || std::isnan(var_in[e])));
+    if (any) return nan_error(ctx, first_nan(ctx->prob, &bv, nullptr, 1, rs.m0), i, false);
+  }
   CU((upload_as<S>(ctx->base, b.data(), E, ctx->s_main)));
   CU(cudaMemcpyAsync(ctx->var.p, var_in, sizeof(double) * E, cudaMemcpyHostToDevice, ctx->s_main));
   CU(init_msv<S>(ctx, E, 1.0 / std::sqrt(ctx->ab[i])));
@@ -1782,10 +1888,13 @@ int weighted_mean_t(d4orm_cuda_ctx* ctx, const double* samples, const double* we
   fin.base = (const S*)ctx->base.p;
   fin.bm = nullptr;
   ncclComm_t comm = ctx->comm;  // single-process operator: no root exchange
+  d4orm_exchange_fn xfn = ctx->xfn;
   ctx->comm = nullptr;
+  ctx->xfn = nullptr;
   ctx->k5_regen = false;
   const int r = enqueue_reduce<S>(ctx, rs, sc, 0, fin, false);
   ctx->comm = comm;
+  ctx->xfn = xfn;
   if (r) return r;
   CU(cudaStreamSynchronize(ctx->s_main));
   CU(cudaMemcpy(out, ctx->var.p, sizeof(double) * E, cudaMemcpyDeviceToHost));
@@ -1836,7 +1945,7 @@ int d4orm_cuda_k5_regen(const d4orm_cuda_ctx* ctx) {
 
 int d4orm_cuda_launches_per_step(const d4orm_cuda_ctx* ctx) {
   // K2+K3, K4, K5 partial, K5 tree (+ K1 on the fp64 path, + the root tree when sharded)
-  return 4 + (ctx->precision == D4ORM_PREC_F64 ? 1 : 0) + (ctx->comm ? 1 : 0);
+  return 4 + (ctx->precision == D4ORM_PREC_F64 ? 1 : 0) + (sharded(ctx) ? 1 : 0);
 }
 
 extern "C++" template <typename S>

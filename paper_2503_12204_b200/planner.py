@@ -57,7 +57,11 @@ def make_schedule(steps: int, alpha_bar_final: float) -> np.ndarray:
 class GpuDenoiser:
     def __init__(self, problem: Problem | None = None, device: int = 0, rank: int = 0, world: int = 1,
                  nccl_id: bytes | None = None, precision: int = PREC_F32, noise: int = NOISE_PHILOX,
-                 graphs: bool = True):
+                 graphs: bool = True, exchange=None):
+        """world > 1: the step's two all-gathers run over NCCL (nccl_id, the
+        128 bytes rank 0 got from d4orm_cuda_nccl_id) or through `exchange`,
+        a host function exchange(local: bytes) -> bytes (all ranks' blocks
+        concatenated in rank order), e.g. torch.distributed over gloo."""
         L = lib()
         self._L = L
         h = C.c_void_p()
@@ -69,7 +73,10 @@ class GpuDenoiser:
         self.world, self.rank = world, rank
         self._noise_cb = None
         self._noise_provider = None
+        self._xcb = None
         self.problem = None
+        if exchange is not None:
+            self.set_exchange(exchange)
         self.set_options(precision, noise, graphs)
         if problem is not None:
             self.set_problem(problem)
@@ -110,6 +117,21 @@ class GpuDenoiser:
         pc.goal_tolerance, pc.obstacle_weight, pc.effort_weight = p.goal_tolerance, p.obstacle_weight, p.effort_weight
         self._check(self._L.d4orm_cuda_set_problem(self._h, C.byref(pc)))
         self.problem = p
+
+    def set_exchange(self, fn):
+        """Host-mediated all-gather for world > 1 without NCCL (see __init__)."""
+        def cb(user, local, nbytes, gathered):
+            try:
+                out = fn(C.string_at(local, nbytes))
+                if len(out) != nbytes * self.world:
+                    return 1
+                C.memmove(gathered, out, len(out))
+                return 0
+            except Exception:
+                return 1
+
+        self._xcb = _lib.EXCHANGE_FN(cb)
+        self._check(self._L.d4orm_cuda_set_exchange_fn(self._h, self._xcb, None))
 
     def set_noise_provider(self, fn):
         """fn(step, m0, count, elems) -> (count, elems) float64 normals (host noise mode)."""

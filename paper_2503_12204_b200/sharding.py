@@ -11,8 +11,11 @@ NCCL inside each step's CUDA graph (csrc/d4orm_cuda.cu, enqueue_step):
 * Σ_m w_m·sample_m is summed per chunk of CHUNK samples and the chunk partials
   are combined by a binary-counter pairwise tree (k_wmean_tree).  A rank owns an
   aligned power-of-two block of chunks, so its local root is one subtree of the
-  single-GPU tree; after all-gathering the G roots every rank finishes the same
-  tree — the result is bitwise identical for G = 1, 2, 4, 8.
+  single-GPU tree (the binary counter only merges equal-size subtrees, and a
+  block of 2^k leaves closes exactly one); after all-gathering the G roots every
+  rank finishes the same tree — the top of the single-GPU tree for any G — so
+  the result is bitwise identical for every G whose per-rank chunk count is a
+  power of two (G = 1, 2, 4, 8 at C5, and e.g. G = 3 at M = 3·2^k·256).
 """
 from __future__ import annotations
 
@@ -26,8 +29,10 @@ def shard_range(M: int, world: int, rank: int) -> tuple[int, int]:
     if M % world:
         raise ValueError(f"batch {M} not divisible by world {world}")
     Ml = M // world
-    if world > 1 and Ml % CHUNK:
-        raise ValueError(f"per-rank batch must be a multiple of {CHUNK}")
+    if world > 1:
+        ch = Ml // CHUNK
+        if Ml % CHUNK or ch & (ch - 1):
+            raise ValueError(f"per-rank batch {Ml} must be {CHUNK} x a power of two samples (world {world})")
     return rank * Ml, Ml
 
 

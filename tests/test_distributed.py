@@ -17,14 +17,15 @@ import torch.multiprocessing as mp
 from paper_2503_12204_b200 import scenarios as S
 from paper_2503_12204_b200.sharding import CHUNK, chunk_partials, pairwise_tree, shard_range
 
-M, N, I, SEED = 1024, 8, 5, 3
+N, I, SEED = 8, 5, 3
+M = 1024
 
 
 def problem():
     return S.baseline_config(1).problem.with_horizon(12)
 
 
-def local_step(oracle, p, base, var, rank, world, gather):
+def local_step(oracle, p, base, var, rank, world, gather, M=M):
     """One denoising step i=I from `var`, samples [m0, m0+Ml) computed here."""
     ab, _ = oracle.make_schedule(N, 0.05)
     ms, sd = 1 / math.sqrt(ab[I]), math.sqrt(1 / ab[I] - 1)
@@ -42,7 +43,7 @@ def local_step(oracle, p, base, var, rank, world, gather):
     return math.sqrt(ab[I - 1]) * pairwise_tree(list(roots)), all_rewards
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, M=M):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle.oracle import Oracle
@@ -58,7 +59,7 @@ def _worker(rank, world, port, q):
         dist.all_gather(out, t)
         return torch.cat(out).numpy()
 
-    v, r = local_step(oracle, p, base, var, rank, world, gather)
+    v, r = local_step(oracle, p, base, var, rank, world, gather, M)
     q.put((rank, v, r))
     dist.barrier()
     dist.destroy_process_group()
@@ -72,12 +73,14 @@ def _free_port():
     return port
 
 
-def test_sharded_step_is_world_invariant(oracle):
+@pytest.mark.parametrize("world,M", [(2, 1024), (3, 1536)])
+def test_sharded_step_is_world_invariant(oracle, world, M):
+    """world 3 at M = 1536: two chunks per rank (a power of two), so the three
+    roots are subtrees of the single-GPU tree although G is not."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    world = 2
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, M)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=240) for _ in range(world)]
@@ -85,15 +88,16 @@ def test_sharded_step_is_world_invariant(oracle):
         pr.join(timeout=60)
         assert pr.exitcode == 0
     res.sort(key=lambda t: t[0])
-    v0, v1 = res[0][1], res[1][1]
-    np.testing.assert_array_equal(v0, v1)               # every rank holds the same variable
+    v0 = res[0][1]
+    for r in range(1, world):
+        np.testing.assert_array_equal(v0, res[r][1])    # every rank holds the same variable
 
     # world = 1 with the same protocol: bitwise the same result
     p = problem()
     rng = np.random.default_rng(0)
     base = 0.2 * rng.normal(size=p.elems)
     var = 0.1 * rng.normal(size=p.elems)
-    v_single, r_single = local_step(oracle, p, base, var, 0, 1, lambda a: np.asarray(a, dtype=np.float64))
+    v_single, r_single = local_step(oracle, p, base, var, 0, 1, lambda a: np.asarray(a, dtype=np.float64), M)
     np.testing.assert_array_equal(v0, v_single)
     np.testing.assert_array_equal(res[0][2], r_single)
 
@@ -111,9 +115,19 @@ def test_shard_ranges():
         shard_range(1000, 3, 0)
     with pytest.raises(ValueError):
         shard_range(1024, 8, 0)  # 128 per rank is not a whole chunk
+    with pytest.raises(ValueError, match="power of two"):
+        shard_range(1536, 2, 0)  # 3 chunks per rank: not one subtree of the single-GPU tree
+    assert shard_range(1536, 3, 2) == (1024, 512)
+    # why: the single tree over 6 chunks groups (c0..c3)(c4,c5); ranks of 3 chunks would group (c0..c2)(c3..c5)
+    parts6 = [float(x) for x in np.random.default_rng(2).normal(size=6)]
+    assert pairwise_tree(parts6) == ((parts6[0] + parts6[1]) + (parts6[2] + parts6[3])) + (parts6[4] + parts6[5])
     parts = [float(x) for x in np.random.default_rng(1).normal(size=16)]
     full = pairwise_tree(parts)
     for g in (2, 4, 8):
         roots = [pairwise_tree(parts[r * 16 // g:(r + 1) * 16 // g]) for r in range(g)]
         assert pairwise_tree(roots) == full
+    parts24 = [float(x) for x in np.random.default_rng(3).normal(size=24)]
+    for g in (3, 6, 12):  # 8, 4, 2 leaves per rank
+        roots = [pairwise_tree(parts24[r * 24 // g:(r + 1) * 24 // g]) for r in range(g)]
+        assert pairwise_tree(roots) == pairwise_tree(parts24)
     assert CHUNK == 256

@@ -105,3 +105,48 @@ def test_fused_path_reports_nonfinite_state(gpu, kind):
     gpu.set_problem(p)
     with pytest.raises(d4.D4ormError, match="run_denoising: sample 0 at step 5: rollout: non-finite state for robot 2 at step 8"):
         gpu.run_denoising(base, d4.DenoiserConfig(steps=5, batch=64, seed=1))
+
+
+def _nan_msg(gpu, prec, p, base, var, i, cfg, noise):
+    gpu.set_options(prec, d4.NOISE_HOST)
+    gpu.set_problem(p)
+    with pytest.raises(d4.D4ormError) as e:
+        gpu.denoise_step(base, var, i, cfg, noise)
+    return str(e.value)
+
+
+@pytest.mark.parametrize("where", ["noise", "variable", "base"])
+def test_f32_nan_inputs_fail_like_the_reference(gpu, oracle, where):
+    """A NaN in the noise, the variable or the base reaches a candidate control;
+    the reference's clamp (cwiseMax/cwiseMin) keeps it and the rollout throws
+    for the first failing sample at its first NaN robot/step
+    (dynamics.cpp:76-84, denoiser.cpp:163-164).  The fp32 path clamps with
+    FMNMX, so it scans its inputs: same message as the fp64 path and the
+    oracle."""
+    p = CASES_NAN()
+    M, N, i = 64, 6, 4
+    cfg = d4.DenoiserConfig(steps=N, batch=M, seed=2)
+    base = np.zeros((p.horizon, p.robots, p.du))
+    var = 0.1 * np.ones_like(base)
+    noise = oracle.step_noise(2, i, 0, M, p.elems)
+    if where == "noise":
+        noise.reshape(M, p.horizon, p.robots, p.du)[37, 5, 2, 1] = np.nan
+        noise.reshape(M, p.horizon, p.robots, p.du)[41, 1, 0, 0] = np.nan
+        want = "run_denoising: sample 37 at step 4: rollout: non-finite state for robot 2 at step 6"
+    elif where == "variable":
+        var[9, 1, 0] = np.nan
+        want = "run_denoising: sample 0 at step 4: rollout: non-finite state for robot 1 at step 10"
+    else:
+        base[3, 3, 1] = np.nan
+        want = "run_denoising: sample 0 at step 4: rollout: non-finite state for robot 3 at step 4"
+    m32 = _nan_msg(gpu, d4.PREC_F32, p, base, var, i, cfg, noise)
+    m64 = _nan_msg(gpu, d4.PREC_F64, p, base, var, i, cfg, noise)
+    from oracle.oracle import make_config
+    ab, _ = oracle.make_schedule(N, 0.05)
+    with pytest.raises(RuntimeError) as e:
+        oracle.denoise_step(p, base, var, ab, make_config(N, M, seed=2), i, noise)
+    assert m32 == m64 == str(e.value) == want, (m32, m64, str(e.value))
+
+
+def CASES_NAN():
+    return S.antipodal_circle(5, 4.0, S.HOLO2D_VEL, robot_radius=0.1, horizon=12, lower=[-1, -1], upper=[1, 1])
