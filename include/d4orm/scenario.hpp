@@ -70,7 +70,3 @@ nlohmann::json scenario_to_json(const Scenario& scenario);
 Scenario scenario_from_json(const nlohmann::json& j);
 }  // namespace d4orm
 #endif
-
-namespace d4orm {
-
-}  // namespace d4orm

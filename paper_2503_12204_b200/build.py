@@ -66,8 +66,7 @@ def build(verbose: bool = False, jobs: int | None = None, defines: tuple[str, ..
         o = obj_dir / (s.name + ".o")
         objs.append(o)
         if _newer(s, o, headers):
-            lang = [] if s.suffix == ".cu" else ["-x", "cu"] if False else []
-            cmds.append([nvcc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], *lang, "-c", str(s), "-o", str(o)])
+            cmds.append([nvcc, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-c", str(s), "-o", str(o)])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

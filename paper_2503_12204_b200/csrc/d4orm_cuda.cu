@@ -119,6 +119,8 @@ struct StepGraph {
 
 struct d4orm_cuda_ctx {
   int device = 0, rank = 0, world = 1;
+  int num_sms = 148;     // queried at create (cudaDevAttrMultiProcessorCount)
+  int k4_coop_cap = 148; // K4 grid: CTAs one cooperative launch may use (queried at create)
   cudaStream_t s_main = nullptr, s_noise = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_t0 = nullptr, ev_t1 = nullptr;
   std::vector<cudaEvent_t> ev_k;  // instrumented per-kernel timing
@@ -281,6 +283,14 @@ int choose_tc(d4orm_cuda_ctx* ctx, int* tc_out, size_t* smem_out) {
   while (fit_smem<S>(ctx, TC) > 100 * 1024 && TC / 2 >= d4k::kPF && (TC / 2) % d4k::kPF == 0 &&
          (TC / 2 >= Rp || (Rp % (TC / 2) == 0 && Rp / (TC / 2) <= 4)))
     TC /= 2;
+  // The fp32 fused rollout of the two-control kinds draws kPFf = 2·kPF steps
+  // per block (k23.cuh); a chunk that is not a whole number of blocks runs
+  // the partial-block path (and discards draws) on every chunk, so widen TC
+  // to a multiple of both Rp and 2·kPF when the tile still fits.
+  if (std::is_same<S, float>::value && !pl && ctx->prob.du != 3 && TC >= Rp && TC % (2 * d4k::kPF) != 0) {
+    const int wide = TC * 2;  // TC is a multiple of kPF, so 2·TC is one of 2·kPF (and of Rp)
+    if (fit_smem<S>(ctx, wide) <= 100 * 1024) TC = wide;
+  }
   if (TC % d4k::kPF != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d not a multiple of %d", TC, d4k::kPF);
   if (pl && TC != 64) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: pair-list path needs TC = 64, got %d", TC);
   if (TC >= Rp && TC % Rp != 0) return fail(ctx, D4ORM_E_UNSUPPORTED, "internal: TC %d vs Rp %d", TC, Rp);
@@ -469,7 +479,7 @@ bool use_seg(const d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f) {
   const d4orm_problem& p = ctx->prob;
   if (!d4k::seg_supported(p.kind, p.robots, p.horizon, p.du)) return false;
   if (const char* e = std::getenv("D4ORM_SEG")) return std::atoi(e) != 0;
-  return (f.M + ctx->spc - 1) / ctx->spc < 2 * 148;
+  return (f.M + ctx->spc - 1) / ctx->spc < 2 * ctx->num_sms;
 }
 
 template <typename S>
@@ -589,7 +599,7 @@ int launch_noise(d4orm_cuda_ctx* ctx, cudaStream_t st, int64_t count, int64_t m0
   const d4orm_problem& p = ctx->prob;
   const int G = (p.horizon * p.du + 3) / 4;
   const unsigned gx = (unsigned)((p.robots * G + d4k::kThreads - 1) / d4k::kThreads);
-  int64_t gy = (148LL * 16 + gx - 1) / gx;
+  int64_t gy = ((int64_t)ctx->num_sms * 16 + gx - 1) / gx;
   if (gy > count) gy = count;
   if (gy > 65535) gy = 65535;
   if (gy < 1) gy = 1;
@@ -771,12 +781,18 @@ int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
     CU(cudaLaunchKernel(fn, dim3(1), dim3(nt), args1, 0, ctx->s_main));
     return D4ORM_OK;
   }
-  // 2 rewards per thread (16 beyond 148·2048 samples) held in registers;
-  // one CTA → plain launch, several → cooperative launch (grid.sync)
-  const bool big = rs.M > 148LL * d4k::kWThreads * 2;
+  // 2 rewards per thread (16 beyond cap·2048 samples) held in registers;
+  // one CTA → plain launch, several → cooperative launch (grid.sync), at most
+  // one wave of co-resident CTAs (and the 160 slots of the fold scratch)
+  const int64_t cap = ctx->k4_coop_cap;
+  const bool big = rs.M > cap * d4k::kWThreads * 2;
   const int64_t per_cta = (int64_t)d4k::kWThreads * (big ? 16 : 2);
   const unsigned g = (unsigned)((rs.M + per_cta - 1) / per_cta);
-  if (g > 148) return fail(ctx, D4ORM_E_UNSUPPORTED, "score_weights: batch %lld too large", (long long)rs.M);
+  if (g > cap) {  // beyond one cooperative wave: the single-CTA loop over any M (same semantics, slower)
+    d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
+    CU(cudaGetLastError());
+    return D4ORM_OK;
+  }
   double* scratch = ctx->wscratch.p;
   const void* fn = big ? (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 16>
                        : (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 2>;
@@ -952,12 +968,19 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
     std::memcpy(&v, &a, sizeof v);
     h = (h ^ v) * 1099511628211ull;
   }
+  // the tuning knobs read while a step is enqueued (captured into the graph)
+  std::string knobs = "|TC" + std::to_string(ctx->TC32) + "," + std::to_string(ctx->TC64) + "|sms" +
+                      std::to_string(ctx->num_sms);
+  for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN"}) {
+    const char* v = std::getenv(k);
+    knobs += std::string("|") + (v ? v : "-");
+  }
   char b[600];
   snprintf(b, sizeof b, "%d/%llx/%lld/%d/%.17g/%.17g/%d/%d/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p/%p",
            ctx->regen_ok ? 1 : 0, (unsigned long long)h, (long long)rs.M, rs.N, rs.abf, rs.lambda, ctx->precision, rs.mode, (void*)ctx->z[0].p, (void*)ctx->z[1].p, (void*)ctx->partial.p,
            (void*)ctx->base.p, (void*)ctx->msv.p, (void*)ctx->var.p, (void*)ctx->rewards.p, (void*)ctx->w64.p,
            (void*)ctx->w32.p, (void*)ctx->trace.p, (void*)ctx->keys.p, (void*)ctx->errw.p, (void*)ctx->roots.p);
-  return b;
+  return b + knobs;
 }
 
 // Per-step CUDA graphs for Philox mode (one graph per denoising index i; the
@@ -1078,7 +1101,7 @@ cudaError_t launch_iter_begin(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   ip.st = reinterpret_cast<const d4k::SolveState*>(ctx->sst.p);
   ip.err = ctx->errw.p;
   const int64_t need = std::max<int64_t>(rs.E, rs.N + 1);
-  const unsigned g = (unsigned)std::min<int64_t>((need + 255) / 256, 148 * 8);
+  const unsigned g = (unsigned)std::min<int64_t>((need + 255) / 256, (int64_t)ctx->num_sms * 8);
   d4k::k_iter_begin<S><<<g, 256, 0, ctx->s_main>>>(ip);
   return cudaGetLastError();
 }
@@ -1501,6 +1524,15 @@ int d4orm_cuda_create(int device, int rank, int world, const void* nccl_id, d4or
   c->rank = rank;
   c->world = world;
   CU(cudaSetDevice(device));
+  CU(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  {  // K4: CTAs one cooperative launch may hold (co-resident; ≤ the 160 fold-scratch slots)
+    int a = 0, b = 0;
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, d4k::k_score_weights_grid<d4k::kWThreads, 16>,
+                                                     d4k::kWThreads, 0));
+    CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, d4k::k_score_weights_grid<d4k::kWThreads, 2>,
+                                                     d4k::kWThreads, 0));
+    c->k4_coop_cap = std::max(1, std::min(160, c->num_sms * std::min(a, b)));
+  }
   CU(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&c->s_noise, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
@@ -1820,14 +1852,11 @@ int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t
   CU(ctx->errw.ensure(1));
   CU(cudaMemcpyAsync(ctx->rewards.p, rewards, sizeof(double) * m, cudaMemcpyHostToDevice, ctx->s_main));
   CU(ctx->wscratch.ensure((size_t)d4k::kWScratch));
-  if (m <= 148LL * d4k::kWThreads * 16) {  // the denoising step's own K4 dispatch
+  {  // the denoising step's own K4 dispatch (falls back to the single-CTA loop beyond one cooperative wave)
     RunShape rs;
     rs.M = m;
     rs.lambda = lambda;
     if (int r = enqueue_weights(ctx, rs, StepConsts{})) return r;
-  } else {  // beyond one cooperative wave: the single-CTA loop over any M
-    d4k::WeightParams wp{ctx->rewards.p, m, lambda, ctx->w64.p, ctx->w32.p, ctx->trace.p, 0, ctx->errw.p, 1};
-    d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
   }
   CU(cudaGetLastError());
   CU(cudaStreamSynchronize(ctx->s_main));

@@ -1,11 +1,12 @@
-"""Per-iteration outcome of one executed trajectory (host side, O(R²T) once per
-iteration): objective (reward.cpp:136-156) and check_success
-(reward.cpp:162-200) with the reference's messages."""
+"""TEST HELPER: a numpy restatement of the per-iteration outcome of one
+executed trajectory — objective (reward.cpp:136-156) and check_success
+(reward.cpp:162-200) with the reference's messages — used by the GPU tests to
+re-check the device's K6 outcome on a returned trajectory."""
 from __future__ import annotations
 
 import numpy as np
 
-from .scenarios import Problem
+from paper_2503_12204_b200.scenarios import Problem
 
 
 def objective(p: Problem, states: np.ndarray) -> float:

@@ -88,7 +88,7 @@ def test_baseline_argument_errors(gpu):
 def test_baselines_philox_throughput_mode(gpu, method):
     """fp32 + Philox, one graph per iteration: deterministic, best = max, and
     the device outcome equals the host restatement on the returned trajectory."""
-    from paper_2503_12204_b200.outcome import check_success, objective
+    from outcome_model import check_success, objective
     p = CASES["C2"]()
     gpu.set_problem(p)
     gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX)

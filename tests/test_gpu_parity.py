@@ -28,6 +28,8 @@ CASES = {
     "C4": lambda: S.baseline_config(4).problem.with_horizon(40),
     "C5": lambda: S.baseline_config(5).problem.with_horizon(24),
     "R40": lambda: S.random_square(40, 8.0, 3, S.HOLO2D_VEL, robot_radius=0.15, horizon=16, lower=[-1, -1], upper=[1, 1]),
+    # 20 robots: a tile width that is not a multiple of the 16-step rollout block (TC widened, choose_tc)
+    "R20": lambda: S.random_square(20, 7.0, 5, S.HOLO2D_VEL, robot_radius=0.15, horizon=40, lower=[-1, -1], upper=[1, 1]),
 }
 
 
@@ -398,7 +400,7 @@ def test_device_solve_philox_stops_on_success(gpu):
     if r1.success:
         assert r1.per_iteration[-1][2] and not any(it[2] for it in r1.per_iteration[:-1])
     # the device outcome equals the host restatement on the returned trajectory
-    from paper_2503_12204_b200.outcome import check_success, objective
+    from outcome_model import check_success, objective
     assert check_success(p, r1.best_states)[0] == r1.success
     best_it = rewards.index(r1.best_reward)
     assert objective(p, r1.best_states) == r1.per_iteration[best_it][1]
