@@ -177,7 +177,10 @@ def run_reference_arm(args, rc, rank: int, world: int):
     sample = (f"{batch} of {rc.samples} samples per step ({what}; velocity-input/unicycle kinds via the "
               f"reference's rk4_with extension point), run_denoising steps=1, workers=0 (all {cores} threads)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "warmup": args.warmup,
+            # a full step of the config at the measured rate; the bounded sample's own time beside it
+            "ms_per_step": 1e3 * rc.samples / value, "sample_ms_per_step": 1e3 * total / args.steps,
+            "sample_per_step": batch, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_json(rc, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
@@ -214,6 +217,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1-C4 step-latency keys")
     ap.add_argument("--graphs", type=int, default=1)
     ap.add_argument("--force-comm", action="store_true",
                     help="N = 1 through the sharded protocol (1-rank NCCL communicator): exercises the N > 1 path")
@@ -299,9 +303,15 @@ def main():
         g.run_denoising(base, cfg)
         dt = reduce_max(dist, time.perf_counter() - t0)
         E = p.elems
-        e2e = {"value": M * cfg.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(E * 4 + E * 8 + (cfg.steps + 1) * 8 + 8),
-               "d2h_bytes_per_step": int(E * 8 + cfg.steps * 32 + 8),
-               "step": f"one run_denoising call = {cfg.steps} denoising steps, host base in, host variable+trace out",
+        # per call: base (fp32 upload of the fp64 host array), variable init, Philox key table, error word in;
+        # variable + trace + error word out.  The noise never crosses the bus (drawn in-kernel).
+        h2d_call = int(E * 4 + E * 8 + (cfg.steps + 1) * 8 + 8)
+        d2h_call = int(E * 8 + cfg.steps * 32 + 8)
+        e2e = {"value": M * cfg.steps / dt, "unit": UNIT, "h2d_bytes_per_step": h2d_call / cfg.steps,
+               "d2h_bytes_per_step": d2h_call / cfg.steps, "h2d_bytes_per_call": h2d_call,
+               "d2h_bytes_per_call": d2h_call,
+               "step": f"one public call d4orm_cuda_run_denoising = {cfg.steps} denoising steps (host base in, host "
+                       f"variable + trace out); bytes per step = per call / {cfg.steps}",
                "ms_per_call": dt * 1e3}
 
     # the anytime loop (solve, optimizer.cpp:49-102) on the device: every
@@ -322,14 +332,17 @@ def main():
     F = algorithmic_flops_per_eval(p)
     k23_ms = kms[1]
     achieved = Ml * F / (k23_ms * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_src = None, None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(rc.name)
+        tj = json.loads(tf.read_text())
+        traffic, traffic_src = tj.get(rc.name), tj.get("_source")
     E = p.elems
     # K5a: algorithmic bytes (every sample's z row) and the bytes it actually
-    # moves — z rows of samples with a non-zero fp32 weight only (K4 zeroes
-    # weights below 2^-48 of the largest; DESIGN.md §3), + weights + partials
+    # moves — z rows of samples with a non-zero fp32 weight only (K4's floor:
+    # for shapes whose K5a skips zero weights — E >= 16384 or du = 3, C4/C5 —
+    # the adaptive floor dropping <= 2^-30 of the weight mass; elsewhere
+    # weights below 2^-48 of the largest; DESIGN.md §7), + weights + partials
     parts = (Ml + 255) // 256 * E * 4
     k5_alg = Ml * E * 4 + Ml * 4 + parts
     k5_nz = float(kms[5])
@@ -355,7 +368,8 @@ def main():
         "dtype": "f32", "data": "synthetic (seeded scenario generators, Philox noise)", "config": config_json(rc, world),
         "roofline": {"kernel": "k_rollout_fitness (K2+K3)", "bound": "fp32", "achieved": achieved, "peak": peak_tf.value,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf.value if peak_tf.value else None,
-                     "traffic": traffic, "flops_per_eval": F, "evals_per_launch": Ml, "launch_ms": k23_ms,
+                     "traffic": traffic, "traffic_source": traffic_src, "flops_per_eval": F, "evals_per_launch": Ml,
+                     "launch_ms": k23_ms, "ncu": _ncu_summary(rc.name),
                      "peak_source": "measured live: d4orm_cuda_fp32_peak (FFMA2 over all SMs); MEASURED_PEAKS.json has no FP32 figure",
                      "note": "achieved = SURVEY 8d algorithmic FLOPs (every unordered pair and robot-obstacle test counted) / "
                              "launch time; the kernel culls tests exactly, so the executed FMA-pipe utilisation is lower "
@@ -372,6 +386,8 @@ def main():
         line["e2e"] = e2e
     if solve:
         line["solve"] = solve
+    if world == 1 and args.config == 5 and not args.no_configs:
+        line["configs"] = other_configs(d4, local_rank, args)
     if rank == 0 and world == 1 and not args.no_cpu:
         ref, kind, what = reference_checker()
         batch, t = size_cpu_sample(ref, p, M, 2.0)
@@ -386,6 +402,42 @@ def main():
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def other_configs(d4, device: int, args) -> dict:
+    """BASELINE's second metric, denoise-step latency, on C1-C4 (full shapes,
+    fp32, Philox, CUDA graphs), measured in this run like the headline: W
+    warm-up steps, then K steps timed with CUDA events on the context stream."""
+    from paper_2503_12204_b200 import scenarios as S
+    out = {}
+    for ci in (1, 2, 3, 4):
+        rc = S.baseline_config(ci)
+        p = rc.problem
+        g = d4.GpuDenoiser(p, device=device, precision=d4.PREC_F32, noise=d4.NOISE_PHILOX, graphs=True)
+        cfg = d4.DenoiserConfig(steps=rc.steps, batch=rc.samples, lam=rc.lam, alpha_bar_final=rc.alpha_bar_final,
+                                seed=rc.seed)
+        base = np.zeros((p.horizon, p.robots, p.du))
+        ms, kms = g.bench_steps(base, cfg, args.warmup, args.steps, kernels=True)
+        F = algorithmic_flops_per_eval(p)
+        out[f"C{ci}"] = {"workload": rc.name, "ms_per_step": ms / args.steps,
+                         "value": rc.samples * args.steps / (ms / 1e3), "unit": UNIT,
+                         "k23_ms": kms[1], "k4_ms": kms[2], "k5a_ms": kms[3], "k5b_ms": kms[4],
+                         "k23_tflops": rc.samples * F / (kms[1] * 1e-3) / 1e12,
+                         "gpu_launches_per_step": g.launches_per_step()}
+        g.close()
+    return out
+
+
+def _ncu_summary(name: str):
+    """Hardware counters of K2+K3 from this round's committed `ncu --set full`
+    capture (profiles/ncu_summary.json): FMA-pipe and issue utilisation beside
+    the algorithmic fraction (the kernel culls pair tests exactly, so executed
+    FMA work is below the algorithmic count)."""
+    f = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        return json.loads(f.read_text()).get(name)
+    except Exception:
+        return None
 
 
 def _hbm_peak():

@@ -55,7 +55,7 @@ def build(verbose: bool = False, jobs: int | None = None, defines: tuple[str, ..
     """Build the library.  ``defines``/``out`` produce experiment variants
     (``-D`` flags, separate object dir and output .so) for tools/."""
     nvcc = _nvcc()
-    obj_dir = OBJ if not defines else OBJ.parent / ("build_" + "_".join(d.split("=")[0].lower() for d in defines))
+    obj_dir = OBJ if not defines else OBJ.parent / ("build_" + "_".join(d.lower().replace("=", "") for d in defines))
     lib = out or LIB
     obj_dir.mkdir(exist_ok=True)
     headers = list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + list((ROOT / "include").rglob("*.h*"))

@@ -6,8 +6,11 @@ Tolerances (written here):
     sin/cos kinds differ from glibc by ulps), rewards abs 1e-12, collision /
     obstacle counts exact, weights rel 1e-9, variable rel 1e-9.
   * fp32 throughput mode: states abs 2e-5 m, rewards abs 2e-5 (+ one
-    w_t/(R·T) per explained decision flip), weights compared as log-weights
-    where w > 1e-6, variable rel 1e-4 of its scale.
+    w_t/(R·T) per explained decision flip) for arbitrary control batches; a
+    denoising step: rewards 1e-6 after whole flips, ≤ 2 % flips, K4 on the
+    GPU's rewards 1e-11 rel, K5 on them 5e-6 of max|v|, the whole step 1e-4 of
+    max|v| without flips, else the flips' own effect + 5e-6
+    (tests/e2e_f32.py::check_step_f32).
 """
 import numpy as np
 import pytest
@@ -172,6 +175,8 @@ def test_denoise_step_teacher_forced(gpu, oracle, case, prec):
     base = controls_for(p, 1, 3, scale=0.3)[0]
     var = 0.2 * rng.normal(size=base.shape)
     noise = oracle.step_noise(11, i, 0, M, p.elems)
+    if prec == d4.PREC_F32:  # the fp32 path consumes fp32 normals: give the oracle exactly those
+        noise = noise.astype(np.float32).astype(np.float64)
     gpu.set_options(prec, d4.NOISE_HOST)
     gpu.set_problem(p)
     v_g, r_g, w_g, rec_g = gpu.denoise_step(base, var, i, cfg, noise)
@@ -181,13 +186,9 @@ def test_denoise_step_teacher_forced(gpu, oracle, case, prec):
         np.testing.assert_allclose(w_g, w_o, rtol=1e-8, atol=1e-300)
         np.testing.assert_allclose(v_g, v_o, rtol=1e-9, atol=1e-12)
     else:
-        unit = max(p.w_t, p.obstacle_weight) / (p.robots * p.horizon)
-        dr = np.abs(r_g - r_o)
-        assert (dr <= 2e-5 + 4 * unit).all(), dr.max()
-        assert (dr <= 2e-5).mean() > 0.95
-        scale = np.abs(v_o).max()
-        # weights are sharp (λ=0.1 on z-scores); compare the averaged variable
-        np.testing.assert_allclose(v_g, v_o, atol=2e-3 * scale)
+        from e2e_f32 import check_step_f32
+        m = check_step_f32(oracle, p, var, i, ab, cfg.lam, noise, v_g, r_g, w_g, v_o, r_o, tag=case)
+        print(case, m)
     assert rec_g[0] == i
 
 
