@@ -479,7 +479,10 @@ bool use_seg(const d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f) {
   const d4orm_problem& p = ctx->prob;
   if (!d4k::seg_supported(p.kind, p.robots, p.horizon, p.du)) return false;
   if (const char* e = std::getenv("D4ORM_SEG")) return std::atoi(e) != 0;
-  return (f.M + ctx->spc - 1) / ctx->spc < 2 * ctx->num_sms;
+  // decided on the GLOBAL batch (f.M is this rank's share): every rank then
+  // runs the kernel a single GPU would, so results stay GPU-count invariant
+  const int64_t Mg = f.M * ctx->world;
+  return (Mg + ctx->spc - 1) / ctx->spc < 2 * ctx->num_sms;
 }
 
 template <typename S>
