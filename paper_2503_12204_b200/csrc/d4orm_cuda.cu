@@ -24,6 +24,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "k_seg.cuh"
 #include "../../include/d4orm_cuda.h"
 #include "d4orm_kernels.cuh"
@@ -112,6 +114,16 @@ constexpr int64_t kPartLargeE = 16384;  // E at which K5 switches to one sequent
 constexpr int kWeightThreads = 1024;
 
 }  // namespace
+
+// NVTX ranges around every public call (and each denoising step / solve
+// iteration inside one), so an nsys / ncu --nvtx timeline shows the reference
+// operator each kernel belongs to.  Header-only NVTX v3: free without a tool.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct StepGraph {
   cudaGraphExec_t exec = nullptr;
@@ -1013,6 +1025,7 @@ int ensure_graphs(d4orm_cuda_ctx* ctx, const RunShape& rs) {
 template <typename S>
 int run_steps(d4orm_cuda_ctx* ctx, const RunShape& rs, bool philox, int i_begin, int i_end, const double* given_noise) {
   for (int i = i_begin; i >= i_end; --i) {
+    NvtxRange nvtx_("d4orm.denoising_step");
     if (!philox) {
       if (int r = host_noise(ctx, rs, i, rs.m0, rs.Ml, given_noise, ctx->z[0].p)) return r;
     }
@@ -1592,6 +1605,7 @@ int d4orm_cuda_set_exchange_fn(d4orm_cuda_ctx* ctx, d4orm_exchange_fn fn, void* 
 }
 
 int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* p) {
+  NvtxRange nvtx_("d4orm.set_problem");
   int dx, du, pd;
   if (!dims_of(p->kind, &dx, &du, &pd)) return fail(ctx, D4ORM_E_INVALID, "unknown model kind: %d", p->kind);
   if (p->dx != dx || p->du != du || p->pdim != pd)
@@ -1651,6 +1665,7 @@ int d4orm_cuda_set_problem(d4orm_cuda_ctx* ctx, const d4orm_problem* p) {
 
 int d4orm_cuda_run_denoising(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* config,
                              double* out_variable, d4orm_trace_rec* trace) {
+  NvtxRange nvtx_("d4orm.run_denoising");
   CU(cudaSetDevice(ctx->device));
   return ctx->precision == D4ORM_PREC_F64 ? run_denoising_t<double>(ctx, base, config, out_variable, trace)
                                           : run_denoising_t<float>(ctx, base, config, out_variable, trace);
@@ -1659,6 +1674,7 @@ int d4orm_cuda_run_denoising(d4orm_cuda_ctx* ctx, const double* base, const d4or
 int d4orm_cuda_mppi_solve(d4orm_cuda_ctx* ctx, const d4orm_mppi_config* config, double* best_states,
                           double* best_controls, d4orm_iteration_rec* per_iteration, int* iterations_used,
                           double* best_reward, int* success) {
+  NvtxRange nvtx_("d4orm.mppi_solve");
   CU(cudaSetDevice(ctx->device));
   if (!config) return fail(ctx, D4ORM_E_INVALID, "mppi_solve: null config");
   BaselineSpec b;
@@ -1680,6 +1696,7 @@ int d4orm_cuda_mppi_solve(d4orm_cuda_ctx* ctx, const d4orm_mppi_config* config, 
 int d4orm_cuda_cem_solve(d4orm_cuda_ctx* ctx, const d4orm_cem_config* config, double* best_states,
                          double* best_controls, d4orm_iteration_rec* per_iteration, int* iterations_used,
                          double* best_reward, int* success) {
+  NvtxRange nvtx_("d4orm.cem_solve");
   CU(cudaSetDevice(ctx->device));
   if (!config) return fail(ctx, D4ORM_E_INVALID, "cem_solve: null config");
   BaselineSpec b;
@@ -1703,6 +1720,7 @@ int d4orm_cuda_cem_solve(d4orm_cuda_ctx* ctx, const d4orm_cem_config* config, do
 int d4orm_cuda_solve(d4orm_cuda_ctx* ctx, const d4orm_solve_config* config, double* best_states,
                      double* best_controls, d4orm_iteration_rec* per_iteration, d4orm_trace_rec* traces,
                      int* iterations_used, double* best_reward, int* success) {
+  NvtxRange nvtx_("d4orm.solve");
   CU(cudaSetDevice(ctx->device));
   if (!config) return fail(ctx, D4ORM_E_INVALID, "solve: null config");
   return ctx->precision == D4ORM_PREC_F64
@@ -1756,6 +1774,7 @@ int denoise_step_t(d4orm_cuda_ctx* ctx, const double* base, const double* var_in
 int d4orm_cuda_denoise_step(d4orm_cuda_ctx* ctx, const double* base, const double* variable_in, const double* noise,
                             int i, const d4orm_denoiser_config* config, double* variable_out, double* rewards,
                             double* weights, d4orm_trace_rec* rec) {
+  NvtxRange nvtx_("d4orm.denoise_step");
   CU(cudaSetDevice(ctx->device));
   return ctx->precision == D4ORM_PREC_F64
              ? denoise_step_t<double>(ctx, base, variable_in, noise, i, config, variable_out, rewards, weights, rec)
@@ -1835,6 +1854,7 @@ int rollout_fitness_t(d4orm_cuda_ctx* ctx, const double* u, int64_t count, doubl
 
 int d4orm_cuda_rollout_fitness(d4orm_cuda_ctx* ctx, const double* u, int64_t count, double* states, double* controls,
                                double* rewards, int64_t* counts) {
+  NvtxRange nvtx_("d4orm.rollout_fitness");
   CU(cudaSetDevice(ctx->device));
   return ctx->precision == D4ORM_PREC_F64 ? rollout_fitness_t<double>(ctx, u, count, states, controls, rewards, counts)
                                           : rollout_fitness_t<float>(ctx, u, count, states, controls, rewards, counts);
@@ -1842,6 +1862,7 @@ int d4orm_cuda_rollout_fitness(d4orm_cuda_ctx* ctx, const double* u, int64_t cou
 
 int d4orm_cuda_score_weights(d4orm_cuda_ctx* ctx, const double* rewards, int64_t m, double lambda, double* weights,
                              double* trace3) {
+  NvtxRange nvtx_("d4orm.score_weights");
   CU(cudaSetDevice(ctx->device));
   if (m < 2) return fail(ctx, D4ORM_E_INVALID, "score_weights: need at least 2 rewards");
   if (!(lambda > 0.0)) return fail(ctx, D4ORM_E_INVALID, "score_weights: lambda must be positive");
@@ -1935,12 +1956,14 @@ int weighted_mean_t(d4orm_cuda_ctx* ctx, const double* samples, const double* we
 
 int d4orm_cuda_weighted_mean(d4orm_cuda_ctx* ctx, const double* samples, const double* weights, int64_t m,
                              int64_t elems, double* out) {
+  NvtxRange nvtx_("d4orm.weighted_mean");
   CU(cudaSetDevice(ctx->device));
   return ctx->precision == D4ORM_PREC_F64 ? weighted_mean_t<double>(ctx, samples, weights, m, elems, out)
                                           : weighted_mean_t<float>(ctx, samples, weights, m, elems, out);
 }
 
 int d4orm_cuda_philox_noise(d4orm_cuda_ctx* ctx, uint64_t seed, int step, int64_t m0, int64_t count, float* out) {
+  NvtxRange nvtx_("d4orm.philox_noise");
   CU(cudaSetDevice(ctx->device));
   if (!ctx->has_problem) return fail(ctx, D4ORM_E_INVALID, "d4orm_cuda: set_problem not called");
   RunShape rs;
@@ -2044,6 +2067,7 @@ int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config
 
 int d4orm_cuda_bench_steps(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config* config, int warmup,
                            int steps, double* ms_total, double* kernel_ms) {
+  NvtxRange nvtx_("d4orm.bench_steps");
   CU(cudaSetDevice(ctx->device));
   return ctx->precision == D4ORM_PREC_F64 ? bench_t<double>(ctx, base, config, warmup, steps, ms_total, kernel_ms)
                                           : bench_t<float>(ctx, base, config, warmup, steps, ms_total, kernel_ms);

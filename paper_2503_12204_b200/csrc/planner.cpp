@@ -79,6 +79,13 @@ void throw_for(int code, const std::string& msg) {
   throw std::runtime_error(msg);
 }
 
+// The status of a C-ABI call on context c, as the reference's exception.  The
+// message is read only after the call returned (a `throw_for(call(c), last_error(c))`
+// may evaluate last_error first and report the previous error).
+void check_rc(d4orm_cuda_ctx* c, int code) {
+  if (code != D4ORM_OK) throw_for(code, d4orm_cuda_last_error(c));
+}
+
 int kind_dims(ModelKind kind, int* dx, int* du, int* pd) {
   static const int DX[6] = {4, 4, 6, 2, 3, 3}, DU[6] = {2, 2, 3, 2, 3, 2}, PD[6] = {2, 2, 3, 2, 3, 2};
   const int k = static_cast<int>(kind);
@@ -186,7 +193,7 @@ d4orm_cuda_ctx* gpu_ctx(int which, int precision, int noise, bool graphs) {
   }
   d4orm_cuda_ctx* c = s.ctx.get();
   if (s.precision != precision || s.noise != noise || s.graphs != (graphs ? 1 : 0)) {
-    throw_for(d4orm_cuda_set_options(c, precision, noise, graphs ? 1 : 0), d4orm_cuda_last_error(c));
+    check_rc(c, d4orm_cuda_set_options(c, precision, noise, graphs ? 1 : 0));
     s.precision = precision;
     s.noise = noise;
     s.graphs = graphs ? 1 : 0;
@@ -199,7 +206,7 @@ d4orm_cuda_ctx* gpu(int which, const ProblemArrays& pa, int precision, int noise
   GpuSlot& s = g_slot[which];
   d4orm_cuda_ctx* c = gpu_ctx(which, precision, noise, graphs);
   if (s.problem_key != pa.key) {
-    throw_for(d4orm_cuda_set_problem(c, &pa.p), d4orm_cuda_last_error(c));
+    check_rc(c, d4orm_cuda_set_problem(c, &pa.p));
     s.problem_key = pa.key;
   }
   return c;
@@ -600,7 +607,7 @@ Vector score_weights(const Vector& rewards, double lambda) {
     c = s.ctx.get();
   }
   Vector w(m);
-  throw_for(d4orm_cuda_score_weights(c, rewards.data(), m, lambda, w.data(), nullptr), d4orm_cuda_last_error(c));
+  check_rc(c, d4orm_cuda_score_weights(c, rewards.data(), m, lambda, w.data(), nullptr));
   return w;
 }
 
@@ -621,7 +628,7 @@ JointControls mc_average(const std::vector<JointControls>& samples, const Vector
   std::vector<double> flat(static_cast<size_t>(m * E));
   for (int64_t j = 0; j < m; ++j) std::memcpy(flat.data() + j * E, samples[j].u.data(), sizeof(double) * E);
   d4orm_cuda_ctx* c = gpu_ctx(1, D4ORM_PREC_F64, D4ORM_NOISE_HOST, false);
-  throw_for(d4orm_cuda_weighted_mean(c, flat.data(), weights.data(), m, E, out.u.data()), d4orm_cuda_last_error(c));
+  check_rc(c, d4orm_cuda_weighted_mean(c, flat.data(), weights.data(), m, E, out.u.data()));
   return out;
 }
 
@@ -649,7 +656,7 @@ DenoiseResult run_denoising(const JointControls& base, const Scenario& scenario,
   d4orm_cuda_ctx* c = gpu(0, pa, g_opts.precision, host ? D4ORM_NOISE_HOST : D4ORM_NOISE_PHILOX, g_opts.graphs);
   if (host) {
     g_noise = {config.seed, config.workers};
-    throw_for(d4orm_cuda_set_noise_fn(c, host_noise_fn, &g_noise), d4orm_cuda_last_error(c));
+    check_rc(c, d4orm_cuda_set_noise_fn(c, host_noise_fn, &g_noise));
   }
   d4orm_denoiser_config dc{};
   dc.steps = config.steps;
@@ -662,7 +669,7 @@ DenoiseResult run_denoising(const JointControls& base, const Scenario& scenario,
   DenoiseResult res;
   res.variable = {base.robots, base.control_dim, Matrix(base.u.rows(), base.u.cols())};
   std::vector<d4orm_trace_rec> tr(static_cast<size_t>(config.steps));
-  throw_for(d4orm_cuda_run_denoising(c, base.u.data(), &dc, res.variable.u.data(), tr.data()), d4orm_cuda_last_error(c));
+  check_rc(c, d4orm_cuda_run_denoising(c, base.u.data(), &dc, res.variable.u.data(), tr.data()));
   res.trace.steps.reserve(tr.size());
   for (const auto& t : tr) res.trace.steps.push_back({t.step, t.best_reward, t.mean_reward, t.weight_entropy});
   return res;
@@ -725,7 +732,7 @@ SolveResult solve(const Scenario& scenario, const DynamicsModel& model, const Op
   d4orm_cuda_ctx* c = gpu(0, pa, g_opts.precision, host ? D4ORM_NOISE_HOST : D4ORM_NOISE_PHILOX, g_opts.graphs);
   if (host) {
     g_noise = {dcfg.seed, dcfg.workers};
-    throw_for(d4orm_cuda_set_noise_fn(c, host_noise_fn, &g_noise), d4orm_cuda_last_error(c));
+    check_rc(c, d4orm_cuda_set_noise_fn(c, host_noise_fn, &g_noise));
   }
   d4orm_solve_config sc{};
   sc.max_iterations = config.max_iterations;
@@ -749,9 +756,8 @@ SolveResult solve(const Scenario& scenario, const DynamicsModel& model, const Op
   std::vector<d4orm_trace_rec> tr(static_cast<size_t>(config.max_iterations) * dcfg.steps);
   int used = 0, ok = 0;
   double best = 0.0;
-  throw_for(d4orm_cuda_solve(c, &sc, result.best_trajectory.states.data(), result.best_trajectory.controls.data(),
-                             recs.data(), tr.data(), &used, &best, &ok),
-            d4orm_cuda_last_error(c));
+  check_rc(c, d4orm_cuda_solve(c, &sc, result.best_trajectory.states.data(), result.best_trajectory.controls.data(),
+                             recs.data(), tr.data(), &used, &best, &ok));
   for (int it = 0; it < used; ++it) {
     result.per_iteration.push_back({recs[it].reward, recs[it].objective, recs[it].success != 0, recs[it].elapsed});
     DenoiseTrace t;
@@ -792,7 +798,7 @@ SolveResult baseline_result(const Scenario& scenario, const DynamicsModel& model
   d4orm_cuda_ctx* c = gpu(0, pa, g_opts.precision, host ? D4ORM_NOISE_HOST : D4ORM_NOISE_PHILOX, g_opts.graphs);
   if (host) {  // the provider's step is the iteration: NormalStream(mix_seed(seed, it, m))
     g_noise = {seed, workers};
-    throw_for(d4orm_cuda_set_noise_fn(c, host_noise_fn, &g_noise), d4orm_cuda_last_error(c));
+    check_rc(c, d4orm_cuda_set_noise_fn(c, host_noise_fn, &g_noise));
   }
   const auto t0 = std::chrono::steady_clock::now();
   const int R = scenario.robots;
@@ -803,9 +809,8 @@ SolveResult baseline_result(const Scenario& scenario, const DynamicsModel& model
   std::vector<d4orm_iteration_rec> recs(static_cast<size_t>(std::max(iterations, 1)));
   int used = 0, ok = 0;
   double best = 0.0;
-  throw_for(call(c, result.best_trajectory.states.data(), result.best_trajectory.controls.data(), recs.data(), &used,
-                 &best, &ok),
-            d4orm_cuda_last_error(c));
+  check_rc(c, call(c, result.best_trajectory.states.data(), result.best_trajectory.controls.data(), recs.data(), &used,
+                   &best, &ok));
   for (int it = 0; it < used; ++it)
     result.per_iteration.push_back({recs[it].reward, recs[it].objective, recs[it].success != 0, recs[it].elapsed});
   result.best_reward = best;

@@ -171,8 +171,10 @@ def test_cli_solve_parity_mode_matches_reference(tmp_path, k):
     """`d4orm solve` — the reference's cmd_solve (main.cpp:330-380) unchanged —
     through the GPU drop-in in parity mode vs the reference's own build."""
     args = ["solve", *SOLVE_CASES[k], "--stop-on-success", "false"]
-    run(REF_CLI, [*args, "--out", str(tmp_path / "ref")], tmp_path)
-    run(B200_CLI, [*args, "--out", str(tmp_path / "b200")], tmp_path, env=PARITY)
+    # cmd_solve exits 2 when the best trajectory is not a success (main.cpp:383): compare, don't require 0
+    ra = run(REF_CLI, [*args, "--out", str(tmp_path / "ref")], tmp_path, check=False)
+    rb = run(B200_CLI, [*args, "--out", str(tmp_path / "b200")], tmp_path, env=PARITY, check=False)
+    assert ra.returncode == rb.returncode and ra.returncode in (0, 2), (ra.stderr, rb.stderr)
     a, b = _traj(tmp_path / "b200"), _traj(tmp_path / "ref")
     for key in ("success", "iterations"):
         assert a["result"][key] == b["result"][key], key
@@ -222,8 +224,8 @@ def test_cli_solve_default_fp32_philox(tmp_path):
     from paper_2503_12204_b200 import scenarios as S
     args = ["solve", "--scenario", "antipodal-circle", "--n", "4", "--model", "holo2d", "--N", "20", "--M", "1024",
             "--iters", "3", "--out", str(tmp_path / "f32")]
-    r = run(B200_CLI, args, tmp_path)
-    assert "success=" in r.stdout
+    r = run(B200_CLI, args, tmp_path, check=False)
+    assert r.returncode in (0, 2) and "success=" in r.stdout, r.stderr
     t = _traj(tmp_path / "f32")
     assert (tmp_path / "f32" / "denoise_trace.csv").exists()
     assert t["result"]["iterations"] >= 1 and np.isfinite(t["result"]["reward"])
