@@ -83,6 +83,15 @@ def build(verbose: bool = False, jobs: int | None = None, defines: tuple[str, ..
     return lib
 
 
+CHECKED_LIB = PKG / "libd4orm_b200_checked.so"
+
+
+def build_checked(verbose: bool = False) -> Path:
+    """The same library with the device-side bounds checks on (-DD4K_CHECKED,
+    d4orm_common.cuh): test infrastructure for tests/test_gpu_checked.py."""
+    return build(verbose=verbose, defines=("D4K_CHECKED",), out=CHECKED_LIB)
+
+
 def build_oracle() -> None:
     """Test-only checker: oracle/build/libd4orm_oracle.so and, where
     /root/reference exists, oracle/_ref/libd4orm_ref.so."""

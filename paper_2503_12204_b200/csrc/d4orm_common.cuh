@@ -2,8 +2,29 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include <type_traits>
+
+// Checked builds (-DD4K_CHECKED: libd4orm_b200_checked.so, run over
+// tools/sanitize.py by tests/test_gpu_checked.py): device-side bounds checks
+// on the shared-memory tiles, the pair-list window boxes, K4's octave bins,
+// K5a's compaction and K5b's stack.  (compute-sanitizer is not available on
+// the GPU pool; these are the repo's own substitute.)  No-ops otherwise.
+#ifdef D4K_CHECKED
+#define D4K_CHECK(cond)                                                                                   \
+  do {                                                                                                    \
+    if (!(cond)) {                                                                                        \
+      printf("d4k check failed: %s:%d: %s (block %d,%d thread %d)\n", __FILE__, __LINE__, #cond,         \
+             (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                                         \
+      __trap();                                                                                           \
+    }                                                                                                     \
+  } while (0)
+#else
+#define D4K_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
 
 namespace d4k {
 

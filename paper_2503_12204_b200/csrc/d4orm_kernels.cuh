@@ -70,7 +70,9 @@ constexpr int kWScratch = 6 * 160 + 80;               // grid folds + the bin co
 __device__ __forceinline__ int wbin(double e) {  // e ∈ (0, 1]: octave below the max
   if (!(e >= 0x1p-128)) return 128;
   const int ex = (int)((__double_as_longlong(e) >> 52) & 0x7ff) - 1023;  // ilogb, e normal
-  return ex >= -1 ? 0 : -ex - 1;
+  const int b = ex >= -1 ? 0 : -ex - 1;
+  D4K_CHECK(b >= 0 && b < kWBins);
+  return b;
 }
 
 // Floor from the bin counts, by one warp (all 32 lanes; the same fixed-order
@@ -623,6 +625,7 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
     }
     if (nz) {
       const int pos = off + __popc(bal & ((1u << lane) - 1u));
+      D4K_CHECK(pos >= 0 && pos < kPartLanes);
       s_idx[pos] = threadIdx.x;
       s_w[pos] = wm;
     }
@@ -795,6 +798,7 @@ __global__ void __launch_bounds__(256) k_wmean_regen(const RegenArgs a, const fl
       tot += s_cnt[i];
     }
     const int pos = off + __popc(bal & ((1u << lane) - 1u));
+    D4K_CHECK(pos >= 0 && pos < 256 && tot <= 256);
     s_pos[tid] = pos;
     if (nz) {
       s_idx[pos] = tid;
@@ -908,11 +912,13 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree(const S* __restrict__ p
     for (int j = 0; j < 8; ++j) v8[j] = partial[(8 * b + j) * elems + e];
     S v = xadd(xadd(xadd(v8[0], v8[1]), xadd(v8[2], v8[3])), xadd(xadd(v8[4], v8[5]), xadd(v8[6], v8[7])));
     for (int64_t k = b; k & 1; k >>= 1) v = xadd(stack[--top], v);  // merge equal-size subtrees
+    D4K_CHECK(top >= 0 && top < 40);
     stack[top++] = v;
   }
   for (int64_t cnt = 8 * nblk; cnt < nchunks; ++cnt) {  // leaves past the last whole block
     S v = partial[cnt * elems + e];
     for (int64_t k = cnt; k & 1; k >>= 1) v = xadd(stack[--top], v);
+    D4K_CHECK(top >= 0 && top < 40);
     stack[top++] = v;
   }
   S total = stack[--top];

@@ -96,8 +96,9 @@ struct FitSmem {
   double* red;   // [nthreads]
   double* eff;   // [nthreads]
   int* cnt;      // [2·nthreads]
-  int RS, TC, spc, Rp, nthreads;
+  int RS, TC, spc, Rp, nthreads, npd = 3;
   __device__ __forceinline__ S* row(int c, int s, int tc) const {
+    D4K_CHECK(c >= 0 && c < npd && s >= 0 && s < spc && tc >= 0 && tc < TC);
     return pos + ((size_t)(c * spc + s) * TC + tc) * RS;
   }
 };
@@ -797,6 +798,7 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
   float chk = 0.f;
   float4 bx = empty_box();
   float4* pbw = PL ? sm.pbox + (size_t)sA * (sm.TC / 32) * sm.Rp + rA : nullptr;  // window 0 box slot
+  D4K_CHECK(rA >= 0 && rA < sm.Rp && nsteps >= 1 && nsteps <= sm.TC);
   for (int tc = 0; tc < nsteps; tc += KPF) {
     const int nb = nsteps - tc;
     const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
@@ -809,6 +811,7 @@ __device__ __forceinline__ float rollout_fused(const FitParams<float>& p, const 
     }
     if constexpr (PL) {
       if (((tc + KPF) & 31) == 0 || tc + KPF >= nsteps) {  // end of a warp window (or of the steps)
+        D4K_CHECK(pbw < sm.pbox + (size_t)(sA + 1) * (sm.TC / 32) * sm.Rp);
         *pbw = bx;
         pbw += sm.Rp;
         bx = empty_box();
@@ -880,6 +883,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? D4K_MINB16 : D4K_MI
   const int R = p.R, Rp = PL ? 64 : p.Rp, TC = PL ? 64 : p.TC, spc = PL ? 2 : p.spc, T = p.T;
 
   FitSmem<S> sm;
+  sm.npd = PD;
   sm.RS = Rp + 2;
   sm.TC = TC;
   sm.spc = spc;
@@ -1032,6 +1036,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? D4K_MINB16 : D4K_MI
           yi ^= (yi >> 31) & 0x7fffffff;
           const uint32_t yu = (uint32_t)yi ^ 0x80000000u;
           me = robotA ? (int)(((yu >> 10) << 6) | (uint32_t)kA) : (int)(0x7fffffc0u | (uint32_t)kA);
+          D4K_CHECK(rA >= 0 && rA < Rp);
           sm.key[sA * Rp + rA] = me;
         }
         __syncthreads();
@@ -1104,6 +1109,7 @@ __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? D4K_MINB16 : D4K_MI
               atomicMin(p.err, key);
             }
             if constexpr (F32) goal_acc<PD>(x, ng, ginv, gsd);
+            D4K_CHECK(rA >= 0 && rA < Rp);
             sm.row(0, sA, tc + j)[rA] = x[0];
             sm.row(1, sA, tc + j)[rA] = x[1];
             if constexpr (PD == 3) sm.row(2, sA, tc + j)[rA] = x[2];
