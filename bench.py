@@ -218,6 +218,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1-C4 step-latency keys")
+    ap.add_argument("--no-f64", action="store_true", help="skip the fp64 (reference arithmetic) throughput key")
     ap.add_argument("--graphs", type=int, default=1)
     ap.add_argument("--force-comm", action="store_true",
                     help="N = 1 through the sharded protocol (1-rank NCCL communicator): exercises the N > 1 path")
@@ -388,6 +389,8 @@ def main():
         line["solve"] = solve
     if world == 1 and args.config == 5 and not args.no_configs:
         line["configs"] = other_configs(d4, local_rank, args)
+    if world == 1 and not args.no_f64:
+        line["f64"] = f64_throughput(d4, rc, local_rank)
     if rank == 0 and world == 1 and not args.no_cpu:
         ref, kind, what = reference_checker()
         batch, t = size_cpu_sample(ref, p, M, 2.0)
@@ -426,6 +429,23 @@ def other_configs(d4, device: int, args) -> dict:
                          "gpu_launches_per_step": g.launches_per_step()}
         g.close()
     return out
+
+
+def f64_throughput(d4, rc, device: int) -> dict:
+    """The same workload in the fp64 parity instantiation (the reference's
+    arithmetic: separately rounded mul/add, no FMA contraction, the reference's
+    loop/break order in the fitness), W = 3 warm-up + 2 timed steps: the speed-up
+    at the reference's own precision."""
+    p = rc.problem
+    g = d4.GpuDenoiser(p, device=device, precision=d4.PREC_F64, noise=d4.NOISE_PHILOX, graphs=True)
+    cfg = d4.DenoiserConfig(steps=rc.steps, batch=rc.samples, lam=rc.lam, alpha_bar_final=rc.alpha_bar_final,
+                            seed=rc.seed)
+    steps = 2
+    ms, _ = g.bench_steps(np.zeros((p.horizon, p.robots, p.du)), cfg, 3, steps, kernels=False)
+    g.close()
+    return {"value": rc.samples * steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "warmup": 3, "dtype": "f64",
+            "note": "fp64 parity instantiation (PREC_F64: z stored and read, no culling, reference loop order)"}
 
 
 def _ncu_summary(name: str):

@@ -267,5 +267,12 @@ __device__ __forceinline__ float4 philox_normals(const PhiloxKeys& ks, uint64_t 
   const float2 a = box_muller(r.x, r.y), b = box_muller(r.z, r.w);
   return make_float4(a.x, a.y, b.x, b.y);
 }
+// ... with the sample index as its two counter words (m = m_hi·2^32 + m_lo)
+__device__ __forceinline__ float4 philox_normals(const PhiloxKeys& ks, uint32_t m_hi, uint32_t m_lo, uint32_t k,
+                                                 uint32_t g) {
+  const uint4 r = ks.gen(make_uint4(k, g, m_hi, m_lo));
+  const float2 a = box_muller(r.x, r.y), b = box_muller(r.z, r.w);
+  return make_float4(a.x, a.y, b.x, b.y);
+}
 
 }  // namespace d4k

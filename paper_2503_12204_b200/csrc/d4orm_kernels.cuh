@@ -777,8 +777,7 @@ template <int SUB>
 __global__ void __launch_bounds__(256) k_wmean_regen(const RegenArgs a, const float* __restrict__ w) {
   constexpr int GROUPS = 256 / SUB, LANES = 256 / SUB;
   __shared__ float red[SUB][GROUPS][4];
-  __shared__ int s_idx[256];
-  __shared__ float s_w[256];
+  __shared__ int2 s_iw[256];  // compacted (sample offset in the chunk, fp32 weight bits)
   __shared__ int s_pos[257];
   __shared__ int s_cnt[8];
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -800,10 +799,7 @@ __global__ void __launch_bounds__(256) k_wmean_regen(const RegenArgs a, const fl
     const int pos = off + __popc(bal & ((1u << lane) - 1u));
     D4K_CHECK(pos >= 0 && pos < 256 && tot <= 256);
     s_pos[tid] = pos;
-    if (nz) {
-      s_idx[pos] = tid;
-      s_w[pos] = wm;
-    }
+    if (nz) s_iw[pos] = make_int2(tid, __float_as_int(wm));
     if (tid == 0) s_pos[256] = tot;
     __syncthreads();
   }
@@ -833,11 +829,16 @@ __global__ void __launch_bounds__(256) k_wmean_regen(const RegenArgs a, const fl
     const PhiloxKeys ks(key);
     const float sd = a.sd;
     const int q0 = s_pos[sr * LANES], q1 = s_pos[(sr + 1) * LANES];
+    // chunks start at multiples of 256 samples (a rank's first sample too), so
+    // m = mg + offset never carries into the counter's high word
     const uint64_t mg = (uint64_t)(a.m_global0 + mc);
-#pragma unroll 2
+    D4K_CHECK((mg & 255u) == 0 && q0 >= 0 && q1 <= 256);
+    const uint32_t m_hi = (uint32_t)(mg >> 32), m_lo = (uint32_t)mg;
+#pragma unroll 4
     for (int q = q0; q < q1; ++q) {
-      const float wm = s_w[q];
-      const float4 v = philox_normals(ks, mg + (uint64_t)s_idx[q], (uint32_t)k, (uint32_t)gg);
+      const int2 iw = s_iw[q];  // one LDS.64: offset + weight
+      const float wm = __int_as_float(iw.y);
+      const float4 v = philox_normals(ks, m_hi, m_lo + (uint32_t)iw.x, (uint32_t)k, (uint32_t)gg);
       acc[0] = fmaf(wm, fmaf(sd, v.x, mv[0]), acc[0]);
       acc[1] = fmaf(wm, fmaf(sd, v.y, mv[1]), acc[1]);
       acc[2] = fmaf(wm, fmaf(sd, v.z, mv[2]), acc[2]);
