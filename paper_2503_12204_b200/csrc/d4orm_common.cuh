@@ -3,8 +3,10 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <type_traits>
+#include <utility>
 
 // Checked builds (-DD4K_CHECKED: libd4orm_b200_checked.so, run over
 // tools/sanitize.py by tests/test_gpu_checked.py): device-side bounds checks
@@ -27,6 +29,50 @@
 #endif
 
 namespace d4k {
+
+// ------------------------------------------------- programmatic dependent launch
+// The four kernels of a denoising step form a strict chain (K2+K3 → K4 → K5a →
+// K5b → next step's K2+K3).  They are launched with programmatic stream
+// serialization (sm_90+), so a kernel is scheduled while its predecessor's last
+// blocks drain instead of after the grid-completion round trip; each waits in
+// pdl_wait() — before touching anything its predecessor writes — until the
+// predecessor grid has completed and its memory is visible.  Knob D4ORM_PDL=0.
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("D4ORM_PDL");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+// Launch a step kernel (PDL when enabled; the cooperative attribute for grid-
+// synchronising kernels, which are launched without PDL).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_step(void (*fn)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                               bool cooperative, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  if (cooperative) {
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+  } else {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = (cooperative || pdl_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
+}
 
 enum Kind { DIFFDRIVE = 0, HOLO2D = 1, HOLO3D = 2, HOLO2D_VEL = 3, HOLO3D_VEL = 4, UNICYCLE = 5 };
 

@@ -788,12 +788,11 @@ int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
   if (rs.M <= 8LL * d4k::kWThreads) {
     // ≤ 2048 rewards: 256 threads (8-warp folds), else 1024
     const int nt = rs.M <= 2048 ? 256 : d4k::kWThreads;
-    const void* fn = rs.M <= 1024   ? (const void*)d4k::k_score_weights_cta<256, 4>
-                     : rs.M <= 2048 ? (const void*)d4k::k_score_weights_cta<256, 8>
-                     : rs.M <= 4096 ? (const void*)d4k::k_score_weights_cta<d4k::kWThreads, 4>
-                                    : (const void*)d4k::k_score_weights_cta<d4k::kWThreads, 8>;
-    void* args1[] = {(void*)&wp};
-    CU(cudaLaunchKernel(fn, dim3(1), dim3(nt), args1, 0, ctx->s_main));
+    void (*fn)(const d4k::WeightParams) = rs.M <= 1024   ? d4k::k_score_weights_cta<256, 4>
+                                          : rs.M <= 2048 ? d4k::k_score_weights_cta<256, 8>
+                                          : rs.M <= 4096 ? d4k::k_score_weights_cta<d4k::kWThreads, 4>
+                                                         : d4k::k_score_weights_cta<d4k::kWThreads, 8>;
+    CU(d4k::launch_step(fn, dim3(1), dim3(nt), 0, ctx->s_main, false, wp));
     return D4ORM_OK;
   }
   // 2 rewards per thread (16 beyond cap·2048 samples) held in registers;
@@ -804,19 +803,15 @@ int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
   const int64_t per_cta = (int64_t)d4k::kWThreads * (big ? 16 : 2);
   const unsigned g = (unsigned)((rs.M + per_cta - 1) / per_cta);
   if (g > cap) {  // beyond one cooperative wave: the single-CTA loop over any M (same semantics, slower)
-    d4k::k_score_weights<kWeightThreads><<<1, kWeightThreads, 0, ctx->s_main>>>(wp);
-    CU(cudaGetLastError());
+    CU(d4k::launch_step(d4k::k_score_weights<kWeightThreads>, dim3(1), dim3(kWeightThreads), 0, ctx->s_main, false,
+                        wp));
     return D4ORM_OK;
   }
   double* scratch = ctx->wscratch.p;
-  const void* fn = big ? (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 16>
-                       : (const void*)d4k::k_score_weights_grid<d4k::kWThreads, 2>;
-  void* args[] = {(void*)&wp, (void*)&scratch};
-  if (g == 1) {
-    CU(cudaLaunchKernel(fn, dim3(1), dim3(d4k::kWThreads), args, 0, ctx->s_main));
-  } else {
-    CU(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(d4k::kWThreads), args, 0, ctx->s_main));
-  }
+  void (*fn)(const d4k::WeightParams, double*) = big ? d4k::k_score_weights_grid<d4k::kWThreads, 16>
+                                                     : d4k::k_score_weights_grid<d4k::kWThreads, 2>;
+  // one CTA: a plain (PDL) launch; several: cooperative (grid.sync), no PDL
+  CU(d4k::launch_step(fn, dim3(g), dim3(d4k::kWThreads), 0, ctx->s_main, g > 1, wp, scratch));
   return D4ORM_OK;
 }
 
@@ -834,17 +829,22 @@ int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc
     const dim3 pgrid((unsigned)((rs.E + 4 * Sh::GROUPS - 1) / (4 * Sh::GROUPS)), (unsigned)rs.chunks_local);
     d4k::PartArgs<S> pa{(const S*)ctx->z[0].p, (const S*)ctx->msv.p, (S)sc.sd, (const S*)sc.sdv, fin.nm_in, rs.Ml,
                         rs.E, (S*)ctx->partial.p};
+    const dim3 blk(Sh::THREADS);
+    const double* w64 = ctx->w64.p + rs.m0;
+    const float* w32 = ctx->w32.p + rs.m0;
+    cudaError_t e;
     if (f64) {
       if (dev_mode)
-        d4k::k_wmean_partial<S, double, SUB, 1><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w64.p + rs.m0);
+        e = d4k::launch_step(d4k::k_wmean_partial<S, double, SUB, 1>, pgrid, blk, 0, ctx->s_main, false, pa, w64);
       else
-        d4k::k_wmean_partial<S, double, SUB, 0><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w64.p + rs.m0);
+        e = d4k::launch_step(d4k::k_wmean_partial<S, double, SUB, 0>, pgrid, blk, 0, ctx->s_main, false, pa, w64);
     } else {
       if (dev_mode)
-        d4k::k_wmean_partial<S, float, SUB, 1><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w32.p + rs.m0);
+        e = d4k::launch_step(d4k::k_wmean_partial<S, float, SUB, 1>, pgrid, blk, 0, ctx->s_main, false, pa, w32);
       else
-        d4k::k_wmean_partial<S, float, SUB, 0><<<pgrid, Sh::THREADS, 0, ctx->s_main>>>(pa, ctx->w32.p + rs.m0);
+        e = d4k::launch_step(d4k::k_wmean_partial<S, float, SUB, 0>, pgrid, blk, 0, ctx->s_main, false, pa, w32);
     }
+    return e;
   };
   auto regen = [&](auto sub_tag) {
     constexpr int SUB = decltype(sub_tag)::value;
@@ -852,35 +852,40 @@ int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc
     const unsigned gx = (unsigned)(((int64_t)ctx->prob.robots * G + 256 / SUB - 1) / (256 / SUB));
     d4k::RegenArgs ra{(const float*)ctx->msv.p, (float)sc.sd, rs.Ml, rs.m0, rs.E, ctx->prob.robots,
                       ctx->prob.horizon, ctx->prob.du, ctx->keys.p, sc.key_i, (float*)ctx->partial.p};
-    d4k::k_wmean_regen<SUB><<<dim3(gx, (unsigned)rs.chunks_local), 256, 0, ctx->s_main>>>(ra, ctx->w32.p + rs.m0);
+    const float* w32 = ctx->w32.p + rs.m0;
+    return d4k::launch_step(d4k::k_wmean_regen<SUB>, dim3(gx, (unsigned)rs.chunks_local), dim3(256), 0, ctx->s_main,
+                            false, ra, w32);
   };
   // (the flag is set by this step's enqueue_fitness: fp32, Philox, scalar std)
   const bool use_regen = !f64 && dev_mode == 0 && ctx->k5_regen;
   ctx->k5_regen = false;
   if (use_regen) {
-    if (rs.E >= kPartLargeE) regen(std::integral_constant<int, 1>{});
-    else regen(std::integral_constant<int, 16>{});
+    if (rs.E >= kPartLargeE) CU(regen(std::integral_constant<int, 1>{}));
+    else CU(regen(std::integral_constant<int, 16>{}));
   } else if (rs.E >= kPartLargeE) {
-    partial(std::integral_constant<int, 1>{});
+    CU(partial(std::integral_constant<int, 1>{}));
   } else {
-    partial(std::integral_constant<int, 16>{});
+    CU(partial(std::integral_constant<int, 16>{}));
   }
-  CU(cudaGetLastError());
   if (timing) CU(cudaEventRecord(ctx->ev_k[3], ctx->s_main));
   const unsigned tgrid = (unsigned)((rs.E + d4k::kThreads - 1) / d4k::kThreads);
+  const S* parts = (const S*)ctx->partial.p;
+  const dim3 tblk(d4k::kThreads);
   if (!sharded(ctx)) {
-    d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
-                                                                   fin, nullptr);
+    S* none = nullptr;
+    CU(d4k::launch_step(d4k::k_wmean_tree<S>, dim3(tgrid), tblk, 0, ctx->s_main, false, parts, rs.chunks_local, rs.E,
+                        fin, none));
   } else {
     S* my_root = (S*)ctx->roots.p + (size_t)ctx->rank * rs.E;
-    d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->partial.p, rs.chunks_local, rs.E,
-                                                                   fin, my_root);
-    CU(cudaGetLastError());
+    CU(d4k::launch_step(d4k::k_wmean_tree<S>, dim3(tgrid), tblk, 0, ctx->s_main, false, parts, rs.chunks_local, rs.E,
+                        fin, my_root));
     if (int r = all_gather(ctx, my_root, ctx->roots.p, (size_t)rs.E, f64 ? sizeof(double) : sizeof(float),
                            f64 ? ncclFloat64 : ncclFloat32))
       return r;
-    d4k::k_wmean_tree<S><<<tgrid, d4k::kThreads, 0, ctx->s_main>>>((const S*)ctx->roots.p, ctx->world, rs.E, fin,
-                                                                   nullptr);
+    const S* roots = (const S*)ctx->roots.p;
+    S* none = nullptr;
+    CU(d4k::launch_step(d4k::k_wmean_tree<S>, dim3(tgrid), tblk, 0, ctx->s_main, false, roots, (int64_t)ctx->world,
+                        rs.E, fin, none));
   }
   CU(cudaGetLastError());
   if (timing) CU(cudaEventRecord(ctx->ev_k[4], ctx->s_main));
@@ -986,7 +991,7 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   // the tuning knobs read while a step is enqueued (captured into the graph)
   std::string knobs = "|TC" + std::to_string(ctx->TC32) + "," + std::to_string(ctx->TC64) + "|sms" +
                       std::to_string(ctx->num_sms);
-  for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN"}) {
+  for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN", "D4ORM_PDL"}) {
     const char* v = std::getenv(k);
     knobs += std::string("|") + (v ? v : "-");
   }

@@ -216,6 +216,7 @@ __device__ __forceinline__ void grid_fold_n(double* v, double* sh, double* scrat
 
 template <int NT, int kWPer>
 __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p, double* scratch) {
+  pdl_wait();
   static_assert(NT == kWThreads, "k_score_weights_grid block size");
   __shared__ double sh[3 * 32];
   __shared__ unsigned s_hist[kWBins];
@@ -377,6 +378,7 @@ __device__ __forceinline__ void cta_fold_n(double* v, double* sh) {
 
 template <int NT, int PER>
 __global__ void __launch_bounds__(NT, 1) k_score_weights_cta(const WeightParams p) {
+  pdl_wait();
   __shared__ double sh[3 * 32 + 4];
   __shared__ unsigned s_hist[kWBins];
   __shared__ double s_floor;
@@ -482,6 +484,7 @@ __global__ void __launch_bounds__(NT, 1) k_score_weights_cta(const WeightParams 
 // Single-CTA variant (kept for d4orm_cuda_score_weights on arbitrary M).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_score_weights(const WeightParams p) {
+  pdl_wait();
   __shared__ double sh[NT / 32 + 1];
   const int tid = threadIdx.x;
   const int64_t per = (p.M + NT - 1) / NT;
@@ -593,6 +596,7 @@ struct PartArgs {
 template <typename S, typename W, int SUB, int DEV>
 __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const PartArgs<S> a,
                                                                            const W* __restrict__ w) {
+  pdl_wait();
   constexpr int kPartGroups = PartShape<SUB>::GROUPS, kPartSub = SUB, kPartLanes = PartShape<SUB>::LANES;
   __shared__ S red[kPartSub][kPartGroups][4];
   const S* __restrict__ z = a.z;
@@ -775,6 +779,7 @@ struct RegenArgs {
 
 template <int SUB>
 __global__ void __launch_bounds__(256) k_wmean_regen(const RegenArgs a, const float* __restrict__ w) {
+  pdl_wait();
   constexpr int GROUPS = 256 / SUB, LANES = 256 / SUB;
   __shared__ float red[SUB][GROUPS][4];
   __shared__ int2 s_iw[256];  // compacted (sample offset in the chunk, fp32 weight bits)
@@ -899,6 +904,7 @@ template <typename S>
 __global__ void __launch_bounds__(kThreads) k_wmean_tree(const S* __restrict__ partial, int64_t nchunks,
                                                          int64_t elems, const TreeFinal<S> f,
                                                          S* __restrict__ root_out) {
+  pdl_wait();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= elems) return;
   S stack[40];

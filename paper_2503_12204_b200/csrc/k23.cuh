@@ -872,6 +872,7 @@ __device__ __noinline__ void rollout_check(const FitParams<float>& p, int kA, in
 
 template <typename S, int KIND, int TB, int MAXW, int NOISE, bool PL = false>
 __global__ void __launch_bounds__(kFitMaxThreads, TB >= 16 ? D4K_MINB16 : D4K_MINB8) k_rollout_fitness(const __grid_constant__ FitParams<S> p) {
+  pdl_wait();
   static_assert(!PL || (std::is_same<S, float>::value && ModelDims<KIND>::PD == 2 && MAXW == 2),
                 "pair-list path: fp32, planar kinds, Rp = 64");
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;

@@ -14,8 +14,7 @@ cudaError_t launch_k23_tb(dim3 grid, int threads, size_t smem, cudaStream_t st, 
   auto fn = k_rollout_fitness<S, KIND, TB, MAXW, NOISE, PL>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  fn<<<grid, threads, smem, st>>>(p);
-  return cudaGetLastError();
+  return launch_step(fn, grid, dim3(threads), smem, st, false, p);
 }
 
 template <typename S, int KIND, int NOISE>

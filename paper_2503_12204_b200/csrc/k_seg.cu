@@ -37,6 +37,7 @@ constexpr int kSegMaxL = 16;   // steps per segment (T ≤ 128)
 
 template <int PD, int NOISE>
 __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_constant__ FitParams<float> p) {
+  pdl_wait();
   constexpr int DU = PD;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* pos = reinterpret_cast<float*>(smem_raw);  // [spc][T+1][R][PD]
@@ -249,11 +250,11 @@ cudaError_t launch_seg(int kind, bool philox, int64_t M, cudaStream_t st, const 
   const dim3 grid((unsigned)((M + spc - 1) / spc));
   const size_t smem = seg_smem_bytes(f.R, f.T, kind == HOLO3D_VEL ? 3 : 2);
   if (kind == HOLO2D_VEL) {
-    if (philox) k_rollout_fitness_seg<2, 1><<<grid, 128, smem, st>>>(f);
-    else k_rollout_fitness_seg<2, 0><<<grid, 128, smem, st>>>(f);
+    if (philox) return launch_step(k_rollout_fitness_seg<2, 1>, grid, dim3(128), smem, st, false, f);
+    else return launch_step(k_rollout_fitness_seg<2, 0>, grid, dim3(128), smem, st, false, f);
   } else {
-    if (philox) k_rollout_fitness_seg<3, 1><<<grid, 128, smem, st>>>(f);
-    else k_rollout_fitness_seg<3, 0><<<grid, 128, smem, st>>>(f);
+    if (philox) return launch_step(k_rollout_fitness_seg<3, 1>, grid, dim3(128), smem, st, false, f);
+    else return launch_step(k_rollout_fitness_seg<3, 0>, grid, dim3(128), smem, st, false, f);
   }
   return cudaGetLastError();
 }
