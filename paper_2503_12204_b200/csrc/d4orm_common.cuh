@@ -37,6 +37,8 @@ namespace d4k {
 // blocks drain instead of after the grid-completion round trip; each waits in
 // pdl_wait() — before touching anything its predecessor writes — until the
 // predecessor grid has completed and its memory is visible.  Knob D4ORM_PDL=0.
+// (An early griddepcontrol.launch_dependents at block start was measured
+// slightly slower: C1 0.0187 -> 0.0196 ms, C4 0.152 -> 0.154 ms.)
 __device__ __forceinline__ void pdl_wait() {
 #if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
   asm volatile("griddepcontrol.wait;" ::: "memory");

@@ -785,13 +785,18 @@ int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
                        sc.trace_step, ctx->errw.p, (rs.E == 0 || k5_skips_class(ctx, rs)) ? 1 : 0};
   // M ≤ 8192 (C1, C2): one CTA, ≤ 8 rewards per thread, shared-memory folds
   // (beyond that one SM's fp64 exp throughput loses to the cooperative grid)
-  if (rs.M <= 8LL * d4k::kWThreads) {
+  static const int64_t cta_max = [] {  // experiment knob: largest batch for the single-CTA K4
+    const char* e = std::getenv("D4ORM_K4CTA");
+    return e ? (int64_t)std::atoll(e) : (int64_t)8 * d4k::kWThreads;
+  }();
+  if (rs.M <= cta_max && rs.M <= 16LL * d4k::kWThreads) {
     // ≤ 2048 rewards: 256 threads (8-warp folds), else 1024
     const int nt = rs.M <= 2048 ? 256 : d4k::kWThreads;
     void (*fn)(const d4k::WeightParams) = rs.M <= 1024   ? d4k::k_score_weights_cta<256, 4>
                                           : rs.M <= 2048 ? d4k::k_score_weights_cta<256, 8>
                                           : rs.M <= 4096 ? d4k::k_score_weights_cta<d4k::kWThreads, 4>
-                                                         : d4k::k_score_weights_cta<d4k::kWThreads, 8>;
+                                          : rs.M <= 8192 ? d4k::k_score_weights_cta<d4k::kWThreads, 8>
+                                                         : d4k::k_score_weights_cta<d4k::kWThreads, 16>;
     CU(d4k::launch_step(fn, dim3(1), dim3(nt), 0, ctx->s_main, false, wp));
     return D4ORM_OK;
   }
