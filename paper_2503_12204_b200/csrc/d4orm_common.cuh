@@ -76,6 +76,26 @@ inline cudaError_t launch_step(void (*fn)(KArgs...), dim3 grid, dim3 block, size
   return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
 }
 
+// ... as a grid of thread-block clusters (cluster = `cluster` CTAs)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_step_cluster(void (*fn)(KArgs...), dim3 grid, dim3 block, dim3 cluster, cudaStream_t st,
+                                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster.x;
+  at[0].val.clusterDim.y = cluster.y;
+  at[0].val.clusterDim.z = cluster.z;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
+}
+
 enum Kind { DIFFDRIVE = 0, HOLO2D = 1, HOLO3D = 2, HOLO2D_VEL = 3, HOLO3D_VEL = 4, UNICYCLE = 5 };
 
 template <int KIND>

@@ -376,12 +376,14 @@ __device__ __forceinline__ void cta_fold_n(double* v, double* sh) {
   __syncthreads();
 }
 
+// The body, shared with the fused small-batch step tail (k_small_step_tail):
+// `writer` CTAs write w64 / w32 / trace / the error word; s_w32 (optional,
+// shared memory) receives the fp32 weights.  Returns false on a non-finite
+// reward.  sh: 3·32 + 4 doubles, s_hist: kWBins.
 template <int NT, int PER>
-__global__ void __launch_bounds__(NT, 1) k_score_weights_cta(const WeightParams p) {
-  pdl_wait();
-  __shared__ double sh[3 * 32 + 4];
-  __shared__ unsigned s_hist[kWBins];
-  __shared__ double s_floor;
+__device__ __forceinline__ bool score_weights_cta_body(const WeightParams& p, bool writer, float* s_w32, double* sh,
+                                                       unsigned* s_hist, double* s_floor_p) {
+  double& s_floor = *s_floor_p;
   const int tid = threadIdx.x;
   if (tid < kWBins) s_hist[tid] = 0u;
   double r[PER];
@@ -403,8 +405,8 @@ __global__ void __launch_bounds__(NT, 1) k_score_weights_cta(const WeightParams 
   double f3[3] = {finite ? 0.0 : 1.0, s, best};
   cta_fold_n<3, 4, NT>(f3, sh);
   if (f3[0] != 0.0) {
-    if (tid == 0) atomicMin(p.err, 0xFFFFFFFFFFFFFFFEull);
-    return;
+    if (writer && tid == 0) atomicMin(p.err, 0xFFFFFFFFFFFFFFFEull);
+    return false;
   }
   const double mean = f3[1] / (double)p.M;
   best = f3[2];
@@ -425,17 +427,20 @@ __global__ void __launch_bounds__(NT, 1) k_score_weights_cta(const WeightParams 
     for (int q = 0; q < PER; ++q) {
       const int64_t j = tid + (int64_t)q * NT;
       if (j < p.M) {
-        p.w64[j] = u;
-        p.w32[j] = (float)u;
+        if (writer) {
+          p.w64[j] = u;
+          p.w32[j] = (float)u;
+        }
+        if (s_w32) s_w32[j] = (float)u;
       }
     }
-    if (tid == 0) {
+    if (writer && tid == 0) {
       p.trace[0] = p.step;
       p.trace[1] = best;
       p.trace[2] = mean;
       p.trace[3] = -(double)p.M * u * log(u);
     }
-    return;
+    return true;
   }
   const double inv = 1.0 / (std_dev * p.lambda);
   const double max_scaled = (best - mean) * inv;
@@ -469,16 +474,30 @@ __global__ void __launch_bounds__(NT, 1) k_score_weights_cta(const WeightParams 
     const int64_t j = tid + (int64_t)q * NT;
     if (j < p.M) {
       const double w = r[q] * rsum;
-      p.w64[j] = w;
-      p.w32[j] = r[q] >= floor32 ? (float)w : 0.f;  // adaptive floor (kW32Mass)
+      const float w32 = r[q] >= floor32 ? (float)w : 0.f;  // adaptive floor (kW32Mass)
+      if (writer) {
+        p.w64[j] = w;
+        p.w32[j] = w32;
+      }
+      if (s_w32) s_w32[j] = w32;
     }
   }
-  if (tid == 0) {
+  if (writer && tid == 0) {
     p.trace[0] = p.step;
     p.trace[1] = best;
     p.trace[2] = mean;
     p.trace[3] = log(sum) - f2[1] / sum;
   }
+  return true;
+}
+
+template <int NT, int PER>
+__global__ void __launch_bounds__(NT, 1) k_score_weights_cta(const WeightParams p) {
+  pdl_wait();
+  __shared__ double sh[3 * 32 + 4];
+  __shared__ unsigned s_hist[kWBins];
+  __shared__ double s_floor;
+  score_weights_cta_body<NT, PER>(p, true, nullptr, sh, s_hist, &s_floor);
 }
 
 // Single-CTA variant (kept for d4orm_cuda_score_weights on arbitrary M).
@@ -953,6 +972,127 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree(const S* __restrict__ p
     f.msv[e] = f.nm_s[e];
     if (f.bm) f.bm[e] = f.base[e] + f.nm_s[e];
   }
+}
+
+// ------------------------------------------------- fused small-batch step tail
+// For latency-bound batches (M ≤ 2048 samples, fp32, stored z, one rank — C1)
+// the step's K4 → K5a → K5b chain is one launch of a thread-block-cluster
+// grid: CTA (x, c) owns elements [64x, 64x + 64) of chunk c, and the cluster
+// spans the chunks (≤ 8).  Every CTA computes the z-scored softmax weights of
+// all M rewards itself (score_weights_cta_body — the standalone K4's
+// arithmetic; CTA (0, 0) writes w64 / w32 / trace), then its chunk partial
+// exactly as k_wmean_partial<float, float, 16, 0> (16 sub-ranges of 16
+// samples, fmaf chains, pairwise combine) into its shared memory; after a
+// cluster barrier the cluster's rank-0 CTA reads the chunk partials over
+// distributed shared memory and folds them exactly as k_wmean_tree (8-leaf
+// blocks, binary counter), then the FIN_UPDATE.  Bitwise the three-kernel
+// path's result (tests/test_gpu_tail.py); two launches fewer per step.
+constexpr int kTailMaxChunks = 8;
+struct TailArgs {
+  WeightParams wp;
+  const float* z;    // [M][E] this step's noise
+  const float* msv;  // [E]
+  float sd;
+  int64_t E, nchunks;
+  TreeFinal<float> fin;
+};
+
+template <int PER>
+__global__ void __launch_bounds__(256, 1) k_small_step_tail(const TailArgs a) {
+  pdl_wait();
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  __shared__ double sh[3 * 32 + 4];
+  __shared__ unsigned s_hist[kWBins];
+  __shared__ double s_floor;
+  __shared__ float s_w32[256 * PER];
+  __shared__ float red[16][16][4];
+  __shared__ float s_part[64];
+  const bool ok = score_weights_cta_body<256, PER>(a.wp, blockIdx.x == 0 && blockIdx.y == 0, s_w32, sh, s_hist,
+                                                   &s_floor);
+  const int64_t M = a.wp.M, E = a.E;
+  const int64_t c = blockIdx.y;  // this CTA's chunk = its rank in the cluster
+  D4K_CHECK(a.nchunks >= 1 && a.nchunks <= kTailMaxChunks && (int)cluster.block_index().y == (int)c);
+  const int g = threadIdx.x % 16, sr = threadIdx.x / 16;
+  const int64_t e0 = ((int64_t)blockIdx.x * 16 + g) * 4;
+  const bool live = ok && e0 < E;  // E % 4 == 0 (host): a live group has 4 elements
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (live) {
+    const float sd = a.sd;
+    float mv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) mv[j] = a.msv[e0 + j];
+    const int64_t mb = c * 256 + (int64_t)sr * 16;
+    float4 v[16];
+    float wv[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int64_t m = mb + q;
+      if (m < M) {
+        v[q] = __ldcs(reinterpret_cast<const float4*>(a.z + m * E + e0));
+        wv[q] = s_w32[m];
+      } else {
+        v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        wv[q] = 0.f;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      acc[0] = fmaf(wv[q], fmaf(sd, v[q].x, mv[0]), acc[0]);
+      acc[1] = fmaf(wv[q], fmaf(sd, v[q].y, mv[1]), acc[1]);
+      acc[2] = fmaf(wv[q], fmaf(sd, v[q].z, mv[2]), acc[2]);
+      acc[3] = fmaf(wv[q], fmaf(sd, v[q].w, mv[3]), acc[3]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) red[sr][g][j] = acc[j];
+  __syncthreads();
+#pragma unroll
+  for (int s = 1; s < 16; s <<= 1) {  // k_wmean_partial's pairwise order
+    if ((sr & (2 * s - 1)) == 0) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[sr][g][j] = red[sr][g][j] + red[sr + s][g][j];
+    }
+    __syncthreads();
+  }
+  if (sr == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s_part[g * 4 + j] = red[0][g][j];
+  }
+  cluster.sync();  // every chunk partial of this element block is in its CTA's shared memory
+  const int t = threadIdx.x;
+  const int64_t e = (int64_t)blockIdx.x * 64 + t;
+  if (ok && c == 0 && t < 64 && e < E) {
+    // k_wmean_tree's order over the chunk partials (read over DSMEM), then the update
+    float stack[4];
+    int top = 0;
+    auto leaf = [&](int64_t ch) { return cluster.map_shared_rank(s_part, (unsigned)ch)[t]; };
+    const int64_t nblk = a.nchunks / 8;
+    for (int64_t b = 0; b < nblk; ++b) {
+      float v8[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v8[j] = leaf(8 * b + j);
+      float v = ((v8[0] + v8[1]) + (v8[2] + v8[3])) + ((v8[4] + v8[5]) + (v8[6] + v8[7]));
+      for (int64_t k = b; k & 1; k >>= 1) v = stack[--top] + v;
+      D4K_CHECK(top >= 0 && top < 4);
+      stack[top++] = v;
+    }
+    for (int64_t cnt = 8 * nblk; cnt < a.nchunks; ++cnt) {
+      float v = leaf(cnt);
+      for (int64_t k = cnt; k & 1; k >>= 1) v = stack[--top] + v;
+      D4K_CHECK(top >= 0 && top < 4);
+      stack[top++] = v;
+    }
+    float total = stack[--top];
+    while (top > 0) total = stack[--top] + total;
+    const TreeFinal<float>& f = a.fin;  // FIN_UPDATE (the host selects this kernel for it only)
+    const double nv = f.scale * (double)total;
+    f.var[e] = nv;
+    const float m = (float)(f.next_ms * nv);
+    f.msv[e] = m;
+    if (f.bm) f.bm[e] = f.base[e] + m;
+  }
+  cluster.sync();  // keep every CTA's shared partials alive until rank 0 has read them
 }
 
 template <typename S>

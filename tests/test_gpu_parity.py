@@ -307,7 +307,9 @@ def test_nccl_protocol_on_one_rank():
     b = d4.GpuDenoiser(p, rank=0, world=1, nccl_id=bytes(buf.raw))
     va, ta = a.run_denoising(base, cfg)
     vb, tb = b.run_denoising(base, cfg)
-    assert b.launches_per_step() == a.launches_per_step() + 1
+    # sharded: K2+K3, K4, K5a, K5b, root tree; one GPU: the same 4, or K2+K3 +
+    # the fused small-batch tail (bitwise the same result, checked below)
+    assert b.launches_per_step() == 5 and a.launches_per_step() in (2, 4)
     np.testing.assert_array_equal(va, vb)
     assert ta == tb
     a.close()

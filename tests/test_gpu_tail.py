@@ -1,0 +1,64 @@
+"""The fused small-batch step tail (d4k::k_small_step_tail: K4 + K5a + K5b in
+one launch for M ≤ 2048, fp32, stored noise, one rank — C1) against the
+three-kernel path (D4ORM_FUSE_TAIL=0): bitwise the same variable, rewards,
+weights and trace, over batch sizes below / at / across the 256-sample chunk
+and up to the 2048 limit, both noise sources."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+pytestmark = pytest.mark.gpu
+
+CHILD = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2503_12204_b200 as d4
+from paper_2503_12204_b200 import scenarios as S
+out = {}
+for name, p in (("C1", S.baseline_config(1).problem),
+                ("C2s", S.baseline_config(2).problem.with_horizon(24)),
+                ("C3s", S.baseline_config(3).problem.with_horizon(20))):
+    for M in (2, 255, 300, 1024, 2048):
+        g = d4.GpuDenoiser(p)
+        base = 0.1 * np.cos(np.arange(p.elems)).reshape(p.horizon, p.robots, p.du)
+        v, tr = g.run_denoising(base, d4.DenoiserConfig(steps=5, batch=M, seed=M))
+        out[f"{name}_{M}_run"] = v
+        out[f"{name}_{M}_trace"] = np.array(tr, dtype=float)
+        g.set_options(d4.PREC_F32, d4.NOISE_HOST, False)
+        z = np.random.default_rng(M).normal(size=(M, p.elems))
+        v2, r2, w2, rec = g.denoise_step(base, 0.2 * base, 3, d4.DenoiserConfig(steps=5, batch=M, seed=1), z)
+        out[f"{name}_{M}_step"] = v2
+        out[f"{name}_{M}_r"] = r2
+        out[f"{name}_{M}_w"] = w2
+        out[f"{name}_{M}_rec"] = np.array(rec, dtype=float)
+        out[f"{name}_{M}_launches"] = np.array(g.launches_per_step())
+        g.close()
+np.savez(sys.argv[2], **out)
+'''
+
+
+def _run(fuse, path):
+    env = dict(os.environ, D4ORM_FUSE_TAIL=str(fuse))
+    r = subprocess.run([sys.executable, "-c", CHILD, str(ROOT), str(path)], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(path)
+
+
+def test_fused_tail_is_bitwise_the_three_kernel_path(tmp_path):
+    fused = _run(1, tmp_path / "fused.npz")
+    plain = _run(0, tmp_path / "plain.npz")
+    assert set(fused.files) == set(plain.files)
+    n_fused = 0
+    for k in fused.files:
+        if k.endswith("_launches"):
+            assert int(plain[k]) == 4
+            n_fused += int(fused[k]) == 2
+            continue
+        np.testing.assert_array_equal(fused[k], plain[k], err_msg=k)
+    assert n_fused >= 10  # the fused tail actually ran

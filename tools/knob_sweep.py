@@ -11,11 +11,15 @@ rc = S.baseline_config(int(sys.argv[1]))
 p = rc.problem
 g = d4.GpuDenoiser(p)
 cfg = d4.DenoiserConfig(steps=rc.steps, batch=rc.samples, seed=0)
-best = None
-for _ in range(3):
-    ms, k = g.bench_steps(np.zeros((p.horizon, p.robots, p.du)), cfg, 3, 10)
-    best = (ms / 10, k) if best is None or k[1] < best[1][1] else best
-print("step %.4f ms  K23 %.4f ms  K5a %.4f ms  K4 %.4f ms" % (best[0], best[1][1], best[1][3], best[1][2]))
+import os
+reps, n = int(os.environ.get("KS_REPS", "3")), int(os.environ.get("KS_STEPS", "10"))
+best, steps = None, []
+for _ in range(reps):
+    ms, k = g.bench_steps(np.zeros((p.horizon, p.robots, p.du)), cfg, 3, n)
+    steps.append(ms / n)
+    best = (ms / n, k) if best is None or k[1] < best[1][1] else best
+print("step %.4f ms (min %.4f median %.4f)  K23 %.4f ms  K5a %.4f ms  K4 %.4f ms" % (
+    best[0], min(steps), sorted(steps)[len(steps) // 2], best[1][1], best[1][3], best[1][2]))
 '''
 cfg = sys.argv[1]
 for spec in sys.argv[2:]:
