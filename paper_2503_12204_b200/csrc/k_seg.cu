@@ -27,15 +27,20 @@
 // in tests/test_gpu_seg.py.
 #include "k_seg.cuh"
 
+#include <cstdlib>
+
 #include "d4orm_common.cuh"
 #include "k23.cuh"
 
 namespace d4k {
 
-constexpr int kSegs = 8;       // threads per robot (a shuffle group)
-constexpr int kSegMaxL = 16;   // steps per segment (T ≤ 128)
+constexpr int kSegMaxL = 16;   // steps per segment (T ≤ 128 at 8 segments)
 
-template <int PD, int NOISE>
+// kSegs threads per robot (a shuffle group): 8.  16 (knob D4ORM_SEGS=16, where
+// the horizon splits into whole Philox groups) halves each thread's serial
+// chain but was measured slower on C1 (0.0164 → 0.0214 ms per step: twice the
+// CTAs, and the per-thread pair loop does not shrink with the segment).
+template <int PD, int NOISE, int kSegs>
 __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_constant__ FitParams<float> p) {
   pdl_wait();
   constexpr int DU = PD;
@@ -233,30 +238,44 @@ __global__ void __launch_bounds__(128) k_rollout_fitness_seg(const __grid_consta
   }
 }
 
+namespace {
+bool segs_ok(int segs, int R, int T, int du) {
+  if (R < 1 || R * segs > 128 || 128 % (R * segs) != 0) return false;
+  if (T % segs != 0 || T / segs > kSegMaxL) return false;
+  return ((T / segs) * du) % 4 == 0;  // segments start on a Philox group
+}
+int segs_for(int R, int T, int du) {
+  if (const char* e = std::getenv("D4ORM_SEGS")) {
+    const int v = std::atoi(e);
+    if ((v == 8 || v == 16) && segs_ok(v, R, T, du)) return v;
+  }
+  return 8;
+}
+}  // namespace
+
 size_t seg_smem_bytes(int R, int T, int pdim) {
-  const int spc = 128 / (R * kSegs);
+  const int spc = 128 / (R * segs_for(R, T, pdim));
   return (size_t)spc * (T + 1) * R * pdim * sizeof(float) + 8 * sizeof(double) + 8 * sizeof(int);
 }
 
 bool seg_supported(int kind, int R, int T, int du) {
   if (kind != HOLO2D_VEL && kind != HOLO3D_VEL) return false;
-  if (R < 1 || R * kSegs > 128 || 128 % (R * kSegs) != 0) return false;  // R ∈ {1, 2, 4, 8, 16}
-  if (T % kSegs != 0 || T / kSegs > kSegMaxL) return false;
-  return ((T / kSegs) * du) % 4 == 0;  // segments start on a Philox group
+  return segs_ok(8, R, T, du);  // R ∈ {1, 2, 4, 8, 16}, T % 8 == 0, T ≤ 128
 }
 
 cudaError_t launch_seg(int kind, bool philox, int64_t M, cudaStream_t st, const FitParams<float>& f) {
-  const int spc = 128 / (f.R * kSegs);
+  const int du = kind == HOLO3D_VEL ? 3 : 2;
+  const int segs = segs_for(f.R, f.T, du);
+  const int spc = 128 / (f.R * segs);
   const dim3 grid((unsigned)((M + spc - 1) / spc));
-  const size_t smem = seg_smem_bytes(f.R, f.T, kind == HOLO3D_VEL ? 3 : 2);
+  const size_t smem = seg_smem_bytes(f.R, f.T, du);
+  auto go = [&](auto k) { return launch_step(k, grid, dim3(128), smem, st, false, f); };
   if (kind == HOLO2D_VEL) {
-    if (philox) return launch_step(k_rollout_fitness_seg<2, 1>, grid, dim3(128), smem, st, false, f);
-    else return launch_step(k_rollout_fitness_seg<2, 0>, grid, dim3(128), smem, st, false, f);
-  } else {
-    if (philox) return launch_step(k_rollout_fitness_seg<3, 1>, grid, dim3(128), smem, st, false, f);
-    else return launch_step(k_rollout_fitness_seg<3, 0>, grid, dim3(128), smem, st, false, f);
+    if (segs == 16) return philox ? go(k_rollout_fitness_seg<2, 1, 16>) : go(k_rollout_fitness_seg<2, 0, 16>);
+    return philox ? go(k_rollout_fitness_seg<2, 1, 8>) : go(k_rollout_fitness_seg<2, 0, 8>);
   }
-  return cudaGetLastError();
+  if (segs == 16) return philox ? go(k_rollout_fitness_seg<3, 1, 16>) : go(k_rollout_fitness_seg<3, 0, 16>);
+  return philox ? go(k_rollout_fitness_seg<3, 1, 8>) : go(k_rollout_fitness_seg<3, 0, 8>);
 }
 
 }  // namespace d4k
