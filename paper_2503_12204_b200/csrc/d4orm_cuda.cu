@@ -821,6 +821,15 @@ int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
                         wp));
     return D4ORM_OK;
   }
+  static const bool cluster_ok = [] {
+    const char* e = std::getenv("D4ORM_K4CLUSTER");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (cluster_ok && !big && g > 1 && g <= 8) {  // one thread-block cluster: DSMEM folds, no grid barriers
+    CU(d4k::launch_step_cluster(d4k::k_score_weights_cluster<d4k::kWThreads, 2>, dim3(g), dim3(d4k::kWThreads),
+                                dim3(g, 1, 1), ctx->s_main, wp));
+    return D4ORM_OK;
+  }
   double* scratch = ctx->wscratch.p;
   void (*fn)(const d4k::WeightParams, double*) = big ? d4k::k_score_weights_grid<d4k::kWThreads, 16>
                                                      : d4k::k_score_weights_grid<d4k::kWThreads, 2>;
@@ -1035,7 +1044,7 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   std::string knobs = "|TC" + std::to_string(ctx->TC32) + "," + std::to_string(ctx->TC64) + "|sms" +
                       std::to_string(ctx->num_sms);
   for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN", "D4ORM_PDL",
-                        "D4ORM_FUSE_TAIL"}) {
+                        "D4ORM_FUSE_TAIL", "D4ORM_K4CLUSTER", "D4ORM_K4CTA", "D4ORM_SEGS"}) {
     const char* v = std::getenv(k);
     knobs += std::string("|") + (v ? v : "-");
   }

@@ -171,8 +171,12 @@ constexpr int kWThreads = 1024;  // PER (rewards per thread) is 2 or 16, see the
 
 // N reductions with one grid barrier: v[i] is summed, or max-ed where MAXMASK
 // has bit i.  Fixed fold order (warp tree, CTA tree, CTAs in index order).
-template <int N, int MAXMASK>
-__device__ __forceinline__ void grid_fold_n(double* v, double* sh, double* scratch, int slot) {
+// CL = false: the CTA partials go through `scratch` (global) and a cooperative
+// grid barrier.  CL = true (the whole grid is one thread-block cluster, ≤ 8
+// CTAs): through each CTA's shared `cl` slots and a cluster barrier, read over
+// distributed shared memory in the same CTA order — the same numbers.
+template <int N, int MAXMASK, bool CL = false>
+__device__ __forceinline__ void grid_fold_n(double* v, double* sh, double* scratch, int slot, double* cl = nullptr) {
   namespace cg = cooperative_groups;
   const int tid = threadIdx.x;
 #pragma unroll
@@ -196,35 +200,53 @@ __device__ __forceinline__ void grid_fold_n(double* v, double* sh, double* scrat
         const double u = __shfl_xor_sync(0xffffffffu, r, o);
         r = mx ? fmax(r, u) : r + u;
       }
-      if (tid == 0) scratch[(slot + i) * gridDim.x + blockIdx.x] = r;
+      if (tid == 0) {
+        if constexpr (CL) cl[slot + i] = r;
+        else scratch[(slot + i) * gridDim.x + blockIdx.x] = r;
+      }
     }
   }
-  if (gridDim.x > 1) cg::this_grid().sync();  // cooperative launch only when G > 1
-  else __syncthreads();
+  if constexpr (CL) {
+    cg::this_cluster().sync();  // (distinct slots per fold: no later overwrite)
+    cg::cluster_group cluster = cg::this_cluster();
 #pragma unroll
-  for (int i = 0; i < N; ++i) {
-    const bool mx = (MAXMASK >> i) & 1;
-    double r = scratch[(slot + i) * gridDim.x];
-    for (unsigned b = 1; b < gridDim.x; ++b) {
-      const double u = scratch[(slot + i) * gridDim.x + b];
-      r = mx ? fmax(r, u) : r + u;
+    for (int i = 0; i < N; ++i) {
+      const bool mx = (MAXMASK >> i) & 1;
+      double r = cluster.map_shared_rank(cl, 0u)[slot + i];
+      for (unsigned b = 1; b < gridDim.x; ++b) {
+        const double u = cluster.map_shared_rank(cl, b)[slot + i];
+        r = mx ? fmax(r, u) : r + u;
+      }
+      v[i] = r;
     }
-    v[i] = r;
+  } else {
+    if (gridDim.x > 1) cg::this_grid().sync();  // cooperative launch only when G > 1
+    else __syncthreads();
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const bool mx = (MAXMASK >> i) & 1;
+      double r = scratch[(slot + i) * gridDim.x];
+      for (unsigned b = 1; b < gridDim.x; ++b) {
+        const double u = scratch[(slot + i) * gridDim.x + b];
+        r = mx ? fmax(r, u) : r + u;
+      }
+      v[i] = r;
+    }
   }
   __syncthreads();
 }
 
-template <int NT, int kWPer>
-__global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p, double* scratch) {
-  pdl_wait();
+template <int NT, int kWPer, bool CL>
+__device__ __forceinline__ void score_weights_grid_body(const WeightParams& p, double* scratch) {
   static_assert(NT == kWThreads, "k_score_weights_grid block size");
   __shared__ double sh[3 * 32];
   __shared__ unsigned s_hist[kWBins];
   __shared__ double s_floor;
-  unsigned* g_hist = reinterpret_cast<unsigned*>(scratch + 6 * 160);
+  __shared__ double cl[6];  // CL: this CTA's fold partials (slots 0..5)
+  unsigned* g_hist = CL ? nullptr : reinterpret_cast<unsigned*>(scratch + 6 * 160);
   if (threadIdx.x < kWBins) {
     s_hist[threadIdx.x] = 0u;
-    if (blockIdx.x == 0) g_hist[threadIdx.x] = 0u;  // added to only after two grid barriers
+    if (!CL && blockIdx.x == 0) g_hist[threadIdx.x] = 0u;  // added to only after two grid barriers
   }
   const int64_t stride = (int64_t)gridDim.x * kWThreads;
   const int64_t g0 = (int64_t)blockIdx.x * kWThreads + threadIdx.x;
@@ -246,11 +268,11 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
   }
   // three grid barriers in all: {non-finite count, Σr, max r}, {Σ(r−mean)²}, {Σe, Σe·s}
   double f3[3] = {finite ? 0.0 : 1.0, s, best};
-  grid_fold_n<3, 4>(f3, sh, scratch, 0);
+  grid_fold_n<3, 4, CL>(f3, sh, scratch, 0, cl);
   const double nf = f3[0];
   if (nf != 0.0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicMin(p.err, 0xFFFFFFFFFFFFFFFEull);
-    return;
+    return;  // (CL: the caller's final cluster barrier keeps the slots alive)
   }
   const double mean = f3[1] / (double)p.M;
   best = f3[2];
@@ -263,7 +285,7 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
     }
   }
   double f1[1] = {v};
-  grid_fold_n<1, 0>(f1, sh, scratch, 3);
+  grid_fold_n<1, 0, CL>(f1, sh, scratch, 3, cl);
   const double std_dev = sqrt(f1[0] / (double)p.M);
   const bool head = blockIdx.x == 0 && threadIdx.x == 0;
   if (std_dev < 1e-8) {  // degenerate batch → uniform (denoiser.cpp:74-77)
@@ -302,20 +324,39 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
     }
   }
   __syncthreads();
-  if (p.adaptive && threadIdx.x < kWBins && s_hist[threadIdx.x]) atomicAdd(&g_hist[threadIdx.x], s_hist[threadIdx.x]);
+  if (!CL && p.adaptive && threadIdx.x < kWBins && s_hist[threadIdx.x])
+    atomicAdd(&g_hist[threadIdx.x], s_hist[threadIdx.x]);
   double f2[2] = {sum, es};
-  grid_fold_n<2, 0>(f2, sh, scratch, 4);  // (its grid barrier also completes g_hist)
+  grid_fold_n<2, 0, CL>(f2, sh, scratch, 4, cl);  // (its barrier also completes g_hist / every s_hist)
   sum = f2[0];
   double floor32 = kW32Floor;
   if (p.adaptive) {
-    if (threadIdx.x < kWBins) s_hist[threadIdx.x] = __ldcg(&g_hist[threadIdx.x]);
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      const double f = w32_floor_warp(s_hist, sum);
-      if (threadIdx.x == 0) s_floor = f;
+    if constexpr (CL) {  // the cluster's integer counts summed over DSMEM (order-free)
+      __shared__ unsigned s_tot[kWBins];
+      if (threadIdx.x < kWBins) {
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        unsigned t = 0;
+        for (unsigned b = 0; b < gridDim.x; ++b) t += cluster.map_shared_rank(s_hist, b)[threadIdx.x];
+        s_tot[threadIdx.x] = t;
+      }
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const double fl = w32_floor_warp(s_tot, sum);
+        if (threadIdx.x == 0) s_floor = fl;
+      }
+      __syncthreads();
+      floor32 = s_floor;
+    } else {
+      if (threadIdx.x < kWBins) s_hist[threadIdx.x] = __ldcg(&g_hist[threadIdx.x]);
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        const double f = w32_floor_warp(s_hist, sum);
+        if (threadIdx.x == 0) s_floor = f;
+      }
+      __syncthreads();
+      floor32 = s_floor;
     }
-    __syncthreads();
-    floor32 = s_floor;
   }
   const double rsum = 1.0 / sum, lsum = log(sum);
   // entropy −Σ w·log w with log w = s − log Σe: log Σe − Σe·s / Σe (terms with
@@ -336,6 +377,22 @@ __global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p,
     p.trace[2] = mean;
     p.trace[3] = h;
   }
+}
+
+template <int NT, int kWPer>
+__global__ void __launch_bounds__(NT) k_score_weights_grid(const WeightParams p, double* scratch) {
+  pdl_wait();
+  score_weights_grid_body<NT, kWPer, false>(p, scratch);
+}
+
+// The same as one thread-block cluster of G ≤ 8 CTAs (M ≤ 8·2048: C3, C4):
+// cluster barriers and DSMEM instead of a cooperative grid's global scratch
+// and grid barriers — the same fold order, so the same weights.
+template <int NT, int kWPer>
+__global__ void __launch_bounds__(NT) k_score_weights_cluster(const WeightParams p) {
+  pdl_wait();
+  score_weights_grid_body<NT, kWPer, true>(p, nullptr);
+  cooperative_groups::this_cluster().sync();  // every CTA's shared slots stay alive until all have read them
 }
 
 // Small batches (M ≤ 8192, C1 and C2): the same computation in ONE CTA of

@@ -62,3 +62,42 @@ def test_fused_tail_is_bitwise_the_three_kernel_path(tmp_path):
             continue
         np.testing.assert_array_equal(fused[k], plain[k], err_msg=k)
     assert n_fused >= 10  # the fused tail actually ran
+
+
+CHILD_K4 = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2503_12204_b200 as d4
+from paper_2503_12204_b200 import scenarios as S
+out = {}
+g = d4.GpuDenoiser()
+for M in (2049, 5000, 12000, 16384):
+    for kind, r in (("normal", np.random.default_rng(M).normal(size=M) * 0.01 + 0.3),
+                    ("skewed", np.random.default_rng(M + 1).exponential(size=M) * 0.05),
+                    ("flat", np.full(M, 0.25))):
+        w, t3 = g.score_weights(r, 0.1)
+        out[f"{M}_{kind}_w"] = w
+        out[f"{M}_{kind}_w32"] = g.last_w32(M)
+        out[f"{M}_{kind}_t"] = t3
+p = S.baseline_config(4).problem.with_horizon(32)   # du = 3: the adaptive floor
+g.set_problem(p)
+v, r, w, rec = g.denoise_step(np.zeros((32, 8, 3)), np.full((32, 8, 3), 0.1), 4, d4.DenoiserConfig(steps=6, batch=16384, seed=3))
+out["step_v"], out["step_w"], out["step_rec"] = v, w, np.array(rec, dtype=float)
+np.savez(sys.argv[2], **out)
+'''
+
+
+def test_cluster_k4_is_bitwise_the_grid_k4(tmp_path):
+    """K4 for 2048 < M ≤ 16384 as one thread-block cluster (DSMEM folds) vs the
+    cooperative grid (global scratch + grid barriers): the same fold order, so
+    bitwise the same weights, fp32 weights (incl. the adaptive floor), trace."""
+    res = []
+    for on in (1, 0):
+        env = dict(os.environ, D4ORM_K4CLUSTER=str(on))
+        f = tmp_path / f"k4_{on}.npz"
+        r = subprocess.run([sys.executable, "-c", CHILD_K4, str(ROOT), str(f)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res.append(np.load(f))
+    for k in res[0].files:
+        np.testing.assert_array_equal(res[0][k], res[1][k], err_msg=k)
