@@ -338,7 +338,7 @@ def main():
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         tj = json.loads(tf.read_text())
-        traffic, traffic_src = tj.get(rc.name), tj.get("_source")
+        traffic, traffic_src = tj.get(rc.name), (tj.get("_sources") or {}).get(rc.name)
     E = p.elems
     # K5a: algorithmic bytes (every sample's z row) and the bytes it actually
     # moves — z rows of samples with a non-zero fp32 weight only (K4's floor:

@@ -838,6 +838,31 @@ int enqueue_weights(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& s
   return D4ORM_OK;
 }
 
+// K5b: the pairwise tree over nchunks partials (+ finalisation or root_out);
+// the block roots in parallel (k_wmean_tree_par) when there are ≥ 2 whole
+// 8-leaf blocks, else the serial walk.  Knob D4ORM_TREEPAR=0.
+template <typename S>
+int launch_tree(d4orm_cuda_ctx* ctx, const S* parts, int64_t nchunks, int64_t E, const d4k::TreeFinal<S>& fin,
+                S* root_out) {
+  static const bool par_ok = [] {
+    const char* e = std::getenv("D4ORM_TREEPAR");
+    return !e || std::atoi(e) != 0;
+  }();
+  const int64_t nblk = nchunks / 8;
+  int P = 1;
+  while (P < 8 && 2 * P <= nblk) P *= 2;
+  const size_t smem = (size_t)(d4k::kThreads / P) * (size_t)nblk * sizeof(S);
+  if (par_ok && nblk >= 2 && smem <= 48 * 1024) {
+    const int EB = d4k::kThreads / P;
+    CU(d4k::launch_step(d4k::k_wmean_tree_par<S>, dim3((unsigned)((E + EB - 1) / EB)), dim3(d4k::kThreads), smem,
+                        ctx->s_main, false, parts, nchunks, E, fin, root_out, P));
+  } else {
+    CU(d4k::launch_step(d4k::k_wmean_tree<S>, dim3((unsigned)((E + d4k::kThreads - 1) / d4k::kThreads)),
+                        dim3(d4k::kThreads), 0, ctx->s_main, false, parts, nchunks, E, fin, root_out));
+  }
+  return D4ORM_OK;
+}
+
 // K5: Σ_m w_m·f(sample_m) over this rank's samples (chunk partials), then the
 // deterministic pairwise tree (+ the root all-gather when sharded) and the
 // finalisation `fin` (the denoiser / MPPI update, or the CEM mean / variance).
@@ -891,26 +916,17 @@ int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc
     CU(partial(std::integral_constant<int, 16>{}));
   }
   if (timing) CU(cudaEventRecord(ctx->ev_k[3], ctx->s_main));
-  const unsigned tgrid = (unsigned)((rs.E + d4k::kThreads - 1) / d4k::kThreads);
   const S* parts = (const S*)ctx->partial.p;
-  const dim3 tblk(d4k::kThreads);
   if (!sharded(ctx)) {
-    S* none = nullptr;
-    CU(d4k::launch_step(d4k::k_wmean_tree<S>, dim3(tgrid), tblk, 0, ctx->s_main, false, parts, rs.chunks_local, rs.E,
-                        fin, none));
+    if (int r = launch_tree<S>(ctx, parts, rs.chunks_local, rs.E, fin, nullptr)) return r;
   } else {
     S* my_root = (S*)ctx->roots.p + (size_t)ctx->rank * rs.E;
-    CU(d4k::launch_step(d4k::k_wmean_tree<S>, dim3(tgrid), tblk, 0, ctx->s_main, false, parts, rs.chunks_local, rs.E,
-                        fin, my_root));
+    if (int r = launch_tree<S>(ctx, parts, rs.chunks_local, rs.E, fin, my_root)) return r;
     if (int r = all_gather(ctx, my_root, ctx->roots.p, (size_t)rs.E, f64 ? sizeof(double) : sizeof(float),
                            f64 ? ncclFloat64 : ncclFloat32))
       return r;
-    const S* roots = (const S*)ctx->roots.p;
-    S* none = nullptr;
-    CU(d4k::launch_step(d4k::k_wmean_tree<S>, dim3(tgrid), tblk, 0, ctx->s_main, false, roots, (int64_t)ctx->world,
-                        rs.E, fin, none));
+    if (int r = launch_tree<S>(ctx, (const S*)ctx->roots.p, (int64_t)ctx->world, rs.E, fin, nullptr)) return r;
   }
-  CU(cudaGetLastError());
   if (timing) CU(cudaEventRecord(ctx->ev_k[4], ctx->s_main));
   return D4ORM_OK;
 }
@@ -1044,7 +1060,7 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   std::string knobs = "|TC" + std::to_string(ctx->TC32) + "," + std::to_string(ctx->TC64) + "|sms" +
                       std::to_string(ctx->num_sms);
   for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN", "D4ORM_PDL",
-                        "D4ORM_FUSE_TAIL", "D4ORM_K4CLUSTER", "D4ORM_K4CTA", "D4ORM_SEGS"}) {
+                        "D4ORM_FUSE_TAIL", "D4ORM_K4CLUSTER", "D4ORM_K4CTA", "D4ORM_SEGS", "D4ORM_TREEPAR"}) {
     const char* v = std::getenv(k);
     knobs += std::string("|") + (v ? v : "-");
   }

@@ -972,6 +972,30 @@ struct TreeFinal {
   S* sdv;
 };
 
+// What K5b does with element e's total (see TreeFinal).
+template <typename S>
+__device__ __forceinline__ void tree_finalize(const TreeFinal<S>& f, int64_t e, S total) {
+  if (f.mode == FIN_UPDATE) {
+    const double nv = f.scale * (double)total;
+    f.var[e] = nv;
+    const S m = (S)(f.next_ms * nv);
+    f.msv[e] = m;
+    if (f.bm) f.bm[e] = f.base[e] + m;
+  } else if (f.mode == FIN_CEM_MEAN) {
+    const double nm = (double)total / f.kdiv;  // new_mean /= elite_count
+    f.nm64[e] = nm;
+    f.nm_s[e] = (S)nm;
+  } else {
+    const double sd = sqrt((double)total / f.kdiv);  // variance /= k; cwiseSqrt
+    const double s = sd < f.min_std ? f.min_std : sd;  // cwiseMax(min_std)
+    f.std64[e] = s;
+    f.sdv[e] = (S)s;
+    f.var[e] = f.nm64[e];  // mean.u = new_mean
+    f.msv[e] = f.nm_s[e];
+    if (f.bm) f.bm[e] = f.base[e] + f.nm_s[e];
+  }
+}
+
 // Pairwise (binary-counter) sum of the chunk partials — a balanced binary tree
 // when the chunk count is a power of two, so a rank owning an aligned block of
 // chunks computes exactly one subtree and results are identical for any GPU
@@ -1010,25 +1034,59 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree(const S* __restrict__ p
     root_out[e] = total;
     return;
   }
-  if (f.mode == FIN_UPDATE) {
-    const double nv = f.scale * (double)total;
-    f.var[e] = nv;
-    const S m = (S)(f.next_ms * nv);
-    f.msv[e] = m;
-    if (f.bm) f.bm[e] = f.base[e] + m;
-  } else if (f.mode == FIN_CEM_MEAN) {
-    const double nm = (double)total / f.kdiv;  // new_mean /= elite_count
-    f.nm64[e] = nm;
-    f.nm_s[e] = (S)nm;
-  } else {
-    const double sd = sqrt((double)total / f.kdiv);  // variance /= k; cwiseSqrt
-    const double s = sd < f.min_std ? f.min_std : sd;  // cwiseMax(min_std)
-    f.std64[e] = s;
-    f.sdv[e] = (S)s;
-    f.var[e] = f.nm64[e];  // mean.u = new_mean
-    f.msv[e] = f.nm_s[e];
-    if (f.bm) f.bm[e] = f.base[e] + f.nm_s[e];
+  tree_finalize(f, e, total);
+}
+
+// K5b with the 8-leaf block roots in parallel: P threads per element compute
+// the roots of blocks j, j + P, … (each exactly k_wmean_tree's 8-leaf subtree)
+// into shared memory, then one thread per element runs k_wmean_tree's binary
+// counter over the roots in block order, the leaves past the last whole block,
+// and the finalisation — the same additions in the same order, so bitwise
+// k_wmean_tree; P× the loads in flight (C4: 12 CTAs of 64-deep serial walks →
+// 96 CTAs).  Dynamic shared memory: (256 / P) · nblk values.
+template <typename S>
+__global__ void __launch_bounds__(kThreads) k_wmean_tree_par(const S* __restrict__ partial, int64_t nchunks,
+                                                             int64_t elems, const TreeFinal<S> f, S* __restrict__ root_out,
+                                                             int P) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char tree_smem[];
+  S* roots = reinterpret_cast<S*>(tree_smem);
+  const int EB = kThreads / P;
+  const int el = threadIdx.x / P, j = threadIdx.x % P;
+  const int64_t e = (int64_t)blockIdx.x * EB + el;
+  const int64_t nblk = nchunks / 8;
+  if (e < elems) {
+    for (int64_t b = j; b < nblk; b += P) {
+      S v8[8];  // eight loads in flight
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v8[q] = partial[(8 * b + q) * elems + e];
+      roots[(size_t)el * nblk + b] =
+          xadd(xadd(xadd(v8[0], v8[1]), xadd(v8[2], v8[3])), xadd(xadd(v8[4], v8[5]), xadd(v8[6], v8[7])));
+    }
   }
+  __syncthreads();
+  if (e >= elems || j != 0) return;
+  S stack[40];
+  int top = 0;
+  for (int64_t b = 0; b < nblk; ++b) {
+    S v = roots[(size_t)el * nblk + b];
+    for (int64_t k = b; k & 1; k >>= 1) v = xadd(stack[--top], v);  // merge equal-size subtrees
+    D4K_CHECK(top >= 0 && top < 40);
+    stack[top++] = v;
+  }
+  for (int64_t cnt = 8 * nblk; cnt < nchunks; ++cnt) {  // leaves past the last whole block
+    S v = partial[cnt * elems + e];
+    for (int64_t k = cnt; k & 1; k >>= 1) v = xadd(stack[--top], v);
+    D4K_CHECK(top >= 0 && top < 40);
+    stack[top++] = v;
+  }
+  S total = stack[--top];
+  while (top > 0) total = xadd(stack[--top], total);
+  if (root_out) {
+    root_out[e] = total;
+    return;
+  }
+  tree_finalize(f, e, total);
 }
 
 // ------------------------------------------------- fused small-batch step tail

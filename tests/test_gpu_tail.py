@@ -101,3 +101,46 @@ def test_cluster_k4_is_bitwise_the_grid_k4(tmp_path):
         res.append(np.load(f))
     for k in res[0].files:
         np.testing.assert_array_equal(res[0][k], res[1][k], err_msg=k)
+
+
+CHILD_TREE = r'''
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2503_12204_b200 as d4
+from paper_2503_12204_b200 import scenarios as S
+out = {}
+for name, p, M in (("C2", S.baseline_config(2).problem.with_horizon(32), 8192),
+                   ("C4", S.baseline_config(4).problem.with_horizon(32), 16384),
+                   ("C5", S.baseline_config(5).problem.with_horizon(32), 262144),
+                   ("odd", S.baseline_config(2).problem.with_horizon(20), 256 * 37)):
+    g = d4.GpuDenoiser(p)
+    v, tr = g.run_denoising(np.zeros((p.horizon, p.robots, p.du)), d4.DenoiserConfig(steps=3, batch=M, seed=5))
+    out[name] = v
+    for prec in (d4.PREC_F64,):
+        g.set_options(prec, d4.NOISE_HOST, False)
+        z = np.random.default_rng(1).normal(size=(min(M, 8192), p.elems))
+        v2, _, _, _ = g.denoise_step(np.zeros_like(v), 0.1 + 0 * v, 2, d4.DenoiserConfig(steps=3, batch=len(z), seed=1), z)
+        out[name + "_f64"] = v2
+    g.set_options(d4.PREC_F32, d4.NOISE_PHILOX, True)
+    mr = g.mppi_solve(batch=min(M, 8192), iterations=2, seed=3, stop_on_success=False)
+    cr = g.cem_solve(batch=min(M, 8192), iterations=2, seed=3, stop_on_success=False)
+    out[name + "_mppi"], out[name + "_cem"] = mr.best_controls, cr.best_controls
+    g.close()
+np.savez(sys.argv[2], **out)
+'''
+
+
+def test_parallel_tree_is_bitwise_the_serial_tree(tmp_path):
+    """K5b with the 8-leaf block roots in parallel vs the serial walk (D4ORM_TREEPAR=0):
+    denoising runs (fp32, fp64), MPPI and CEM (the CEM finalisations) at chunk
+    counts 32, 64, 1024 and 37 (not a power of two: leftover leaves)."""
+    res = []
+    for on in (1, 0):
+        env = dict(os.environ, D4ORM_TREEPAR=str(on))
+        f = tmp_path / f"tree_{on}.npz"
+        r = subprocess.run([sys.executable, "-c", CHILD_TREE, str(ROOT), str(f)], env=env, capture_output=True,
+                           text=True, timeout=900)
+        assert r.returncode == 0, r.stderr[-3000:]
+        res.append(np.load(f))
+    for k in res[0].files:
+        np.testing.assert_array_equal(res[0][k], res[1][k], err_msg=k)

@@ -91,8 +91,9 @@ def main():
         tj = ROOT / "profiles" / "traffic.json"
         t = json.loads(tj.read_text()) if tj.exists() else {}
         t[name] = (k23["dram_read"] or 0) + (k23["dram_write"] or 0)
-        t["_source"] = (f"profiles/{Path(md).name} (ncu --set full, one launch of k_rollout_fitness: "
-                        "dram__bytes_read.sum + dram__bytes_write.sum)")
+        t.pop("_source", None)
+        t.setdefault("_sources", {})[name] = (f"profiles/{Path(md).name} (ncu --set full, one launch of "
+                                              "k_rollout_fitness: dram__bytes_read.sum + dram__bytes_write.sum)")
         tj.write_text(json.dumps(t, indent=1) + "\n")
 
 
