@@ -736,7 +736,19 @@ StepConsts denoise_consts(const d4orm_cuda_ctx* ctx, const RunShape& rs, int i) 
 // scalar z stores per robot-step) 0.1667 → 0.1601; C1–C3 lose 2–10 µs (their
 // z stays in L2 for K5a), so they keep the stored rows.
 bool k5_skips_class(const d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  if (const char* e = std::getenv("D4ORM_K5CLASS")) return std::atoi(e) != 0;  // experiment knob
   return rs.E >= kPartLargeE || ctx->prob.du == 3;
+}
+
+// K5a's split of a 256-sample chunk into sub-ranges (summed in ascending m,
+// then pairwise): one walk per thread for large E; 4 sub-ranges of 64 samples
+// for the small-E shapes whose K5a skips zero weights (C4: the regenerating
+// K5a does ~4× the draws per thread of 16 sub-ranges: C4 step 0.1531 →
+// 0.1439 ms); 16 sub-ranges otherwise.  By shape only, so the stored and the
+// regenerating K5a of a problem sum in the same order (bitwise equal).
+int k5_sub(const d4orm_cuda_ctx* ctx, const RunShape& rs) {
+  if (rs.E >= kPartLargeE) return 1;
+  return k5_skips_class(ctx, rs) ? 4 : 16;
 }
 
 bool regen_wanted(const d4orm_cuda_ctx* ctx, const RunShape& rs) {
@@ -907,11 +919,15 @@ int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc
   // (the flag is set by this step's enqueue_fitness: fp32, Philox, scalar std)
   const bool use_regen = !f64 && dev_mode == 0 && ctx->k5_regen;
   ctx->k5_regen = false;
+  const int sub = k5_sub(ctx, rs);
   if (use_regen) {
-    if (rs.E >= kPartLargeE) CU(regen(std::integral_constant<int, 1>{}));
+    if (sub == 1) CU(regen(std::integral_constant<int, 1>{}));
+    else if (sub == 4) CU(regen(std::integral_constant<int, 4>{}));
     else CU(regen(std::integral_constant<int, 16>{}));
-  } else if (rs.E >= kPartLargeE) {
+  } else if (sub == 1) {
     CU(partial(std::integral_constant<int, 1>{}));
+  } else if (sub == 4) {
+    CU(partial(std::integral_constant<int, 4>{}));
   } else {
     CU(partial(std::integral_constant<int, 16>{}));
   }
@@ -956,8 +972,10 @@ bool tail_fusable(const d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConst
     const char* e = std::getenv("D4ORM_FUSE_TAIL");
     return !e || std::atoi(e) != 0;
   }();
+  // (the tail sums each chunk in K5a's 16-sub-range order: only where K5a uses it)
   return on && std::is_same<S, float>::value && !sharded(ctx) && !ctx->k5_regen && sc.sdv == nullptr &&
-         rs.M == rs.Ml && rs.M <= 2048 && rs.E % 4 == 0 && rs.chunks_local <= d4k::kTailMaxChunks;
+         rs.M == rs.Ml && rs.M <= 2048 && rs.E % 4 == 0 && rs.chunks_local <= d4k::kTailMaxChunks &&
+         k5_sub(ctx, rs) == 16;
 }
 
 template <typename S>
@@ -1060,7 +1078,8 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
   std::string knobs = "|TC" + std::to_string(ctx->TC32) + "," + std::to_string(ctx->TC64) + "|sms" +
                       std::to_string(ctx->num_sms);
   for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN", "D4ORM_PDL",
-                        "D4ORM_FUSE_TAIL", "D4ORM_K4CLUSTER", "D4ORM_K4CTA", "D4ORM_SEGS", "D4ORM_TREEPAR"}) {
+                        "D4ORM_FUSE_TAIL", "D4ORM_K4CLUSTER", "D4ORM_K4CTA", "D4ORM_SEGS", "D4ORM_TREEPAR",
+                        "D4ORM_K5CLASS"}) {
     const char* v = std::getenv(k);
     knobs += std::string("|") + (v ? v : "-");
   }

@@ -55,11 +55,13 @@ def pairwise_tree(parts):
 LARGE_E = 16384  # kPartLargeE in csrc/d4orm_cuda.cu
 
 
-def chunk_partials(samples: np.ndarray, weights: np.ndarray, chunk: int = CHUNK):
+def chunk_partials(samples: np.ndarray, weights: np.ndarray, chunk: int = CHUNK, du: int = 2):
     """Per-chunk Σ_m w_m·sample_m in k_wmean_partial's order: each of SUB
     sub-ranges sums its LANES samples in ascending m, then the sub-sums are
-    combined by a balanced pairwise tree (SUB = 1 when E >= LARGE_E, else 16)."""
-    SUB = 1 if samples.shape[1] >= LARGE_E else 16
+    combined by a balanced pairwise tree (k5_sub in csrc/d4orm_cuda.cu: SUB = 1
+    when E >= LARGE_E, 4 for the other shapes whose K5a skips zero weights —
+    du = 3 — else 16)."""
+    SUB = 1 if samples.shape[1] >= LARGE_E else (4 if du == 3 else 16)
     LANES = chunk // SUB
     out = []
     for c0 in range(0, samples.shape[0], chunk):
