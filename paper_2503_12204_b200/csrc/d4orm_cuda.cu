@@ -889,6 +889,14 @@ int enqueue_reduce(d4orm_cuda_ctx* ctx, const RunShape& rs, const StepConsts& sc
     const dim3 pgrid((unsigned)((rs.E + 4 * Sh::GROUPS - 1) / (4 * Sh::GROUPS)), (unsigned)rs.chunks_local);
     d4k::PartArgs<S> pa{(const S*)ctx->z[0].p, (const S*)ctx->msv.p, (S)sc.sd, (const S*)sc.sdv, fin.nm_in, rs.Ml,
                         rs.E, (S*)ctx->partial.p};
+    // z rows larger than L2: read them in the reverse of K2+K3's write order,
+    // so the rows still resident are read before the scan evicts them (an
+    // ascending re-read of a > L2 stream misses on every line).  Knob D4ORM_K5REV.
+    static const int rev_knob = [] {
+      const char* e = std::getenv("D4ORM_K5REV");
+      return e ? std::atoi(e) : -1;
+    }();
+    pa.reverse = rev_knob >= 0 ? rev_knob : 1;
     const dim3 blk(Sh::THREADS);
     const double* w64 = ctx->w64.p + rs.m0;
     const float* w32 = ctx->w32.p + rs.m0;
@@ -1079,7 +1087,7 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
                       std::to_string(ctx->num_sms);
   for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN", "D4ORM_PDL",
                         "D4ORM_FUSE_TAIL", "D4ORM_K4CLUSTER", "D4ORM_K4CTA", "D4ORM_SEGS", "D4ORM_TREEPAR",
-                        "D4ORM_K5CLASS"}) {
+                        "D4ORM_K5CLASS", "D4ORM_K5REV"}) {
     const char* v = std::getenv(k);
     knobs += std::string("|") + (v ? v : "-");
   }

@@ -663,6 +663,7 @@ struct PartArgs {
   const S* nm;       // DEV: [E] the new mean (CEM variance pass)
   int64_t M, elems;
   S* partial;        // [chunks][E]
+  int reverse = 0;   // walk the chunks last-first (the z rows K2+K3 wrote last are the ones still in L2)
 };
 
 // DEV = 0: Σ_m w_m·sample_m (mc_average, denoiser.cpp:92-108; CEM's elite sum
@@ -679,7 +680,7 @@ __global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const
   const int64_t M = a.M, elems = a.elems;
   const int g = threadIdx.x % kPartGroups, sr = threadIdx.x / kPartGroups;
   const int64_t e0 = ((int64_t)blockIdx.x * kPartGroups + g) * 4;
-  const int64_t c = blockIdx.y;
+  const int64_t c = a.reverse ? (int64_t)gridDim.y - 1 - blockIdx.y : (int64_t)blockIdx.y;
   const int64_t mb = c * (kPartSub * kPartLanes) + (int64_t)sr * kPartLanes;
   const int n = e0 < elems ? (elems - e0 < 4 ? (int)(elems - e0) : 4) : 0;
   // large E (fp32): the CTA first compacts its chunk's non-zero weights (in
