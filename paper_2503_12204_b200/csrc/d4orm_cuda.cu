@@ -2149,7 +2149,7 @@ int bench_t(d4orm_cuda_ctx* ctx, const double* base, const d4orm_denoiser_config
   if (ctx->noise_source != D4ORM_NOISE_PHILOX) return fail(ctx, D4ORM_E_INVALID, "bench requires Philox noise");
   if (int r = ensure_buffers(ctx, rs, false, true)) return r;
   if (int r = prologue<S>(ctx, rs, base, c, true)) return r;
-  if (ctx->use_graphs) {
+  if (graphs_on(ctx)) {
     if (int r = ensure_graphs<S>(ctx, rs)) return r;
   }
   // step j → denoising index i = N - (j mod N): a chain of full passes
