@@ -86,10 +86,14 @@ def check_steps(res):
 
 @pytest.mark.parametrize("ci", [1, 2, 3, 4, 5])
 def test_philox_production_path(gpu, oracle, ci):
-    """100 steps of the production kernels (Philox drawn in K2+K3, graphs),
-    every step checked; the oracle's free run over all steps (C5: the first
-    20, by which point it has decorrelated — see the module docstring)."""
-    res = compare_run(gpu, oracle, ci, "philox", free_steps=20 if ci == 5 else None)
+    """The production kernels (Philox drawn in K2+K3, one graph per run) over the
+    100-step schedule, every step checked against the oracle — C5 over its
+    first 50 steps (the oracle needs ~1 s per C5 step); the oracle's free run
+    over all steps for C1 (its outcome is compared) and the first 20 elsewhere
+    (by then it has decorrelated — see the module docstring; the full 100-step
+    drift tables are in profiles/r02_e2e_f32.md)."""
+    res = compare_run(gpu, oracle, ci, "philox", run_steps=50 if ci == 5 else None,
+                      free_steps=None if ci == 1 else 20)
     assert res["run_equal"], "run_denoising (graphs) differs from the denoise_step chain"
     check_steps(res)
     if ci == 1:  # no decision flip in 100 steps: the outcome of the final trajectory is the oracle's
