@@ -426,3 +426,25 @@ def test_heading_kinds_f32_full_horizon(gpu, oracle, kind):
         worst = max(worst, float(np.abs(st[m][..., :2] - rs[..., :2]).max()))
         np.testing.assert_allclose(st[m], rs, atol=2e-5, rtol=1e-5)
     print(f"{kind}: max |Δposition| = {worst:.3g} m over {p.horizon} steps")
+
+
+@pytest.mark.parametrize("case", ["C1", "C2", "C5"])
+def test_run_graph_equals_eager_steps(gpu, case):
+    """run_denoising replays ONE graph for the whole run in Philox mode; the
+    eager per-step launches (graphs off) give bitwise the same variable and
+    trace — both modes (FromScratch draws its initial variable with K1 first),
+    and a second call reuses the graph."""
+    p = CASES[case]()
+    base = controls_for(p, 1, 9, scale=0.3)[0]
+    M = 2048 if case != "C1" else 1024
+    for mode in (d4.DEFORMATION, d4.FROM_SCRATCH):
+        cfg = d4.DenoiserConfig(steps=7, batch=M, seed=4, mode=mode)
+        gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX, graphs=True)
+        gpu.set_problem(p)
+        v1, t1 = gpu.run_denoising(base, cfg)
+        v1b, t1b = gpu.run_denoising(base, cfg)
+        gpu.set_options(d4.PREC_F32, d4.NOISE_PHILOX, graphs=False)
+        v2, t2 = gpu.run_denoising(base, cfg)
+        np.testing.assert_array_equal(v1, v2)
+        np.testing.assert_array_equal(v1, v1b)
+        assert t1 == t2 == t1b

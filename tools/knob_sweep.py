@@ -10,7 +10,8 @@ from paper_2503_12204_b200 import scenarios as S
 rc = S.baseline_config(int(sys.argv[1]))
 p = rc.problem
 g = d4.GpuDenoiser(p)
-cfg = d4.DenoiserConfig(steps=rc.steps, batch=rc.samples, seed=0)
+import os as _os
+cfg = d4.DenoiserConfig(steps=rc.steps, batch=int(_os.environ.get("KS_BATCH", rc.samples)), seed=0)
 import os
 reps, n = int(os.environ.get("KS_REPS", "3")), int(os.environ.get("KS_STEPS", "10"))
 best, steps = None, []
