@@ -343,7 +343,7 @@ def main():
     # K5a: algorithmic bytes (every sample's z row) and the bytes it actually
     # moves — z rows of samples with a non-zero fp32 weight only (K4's floor:
     # for shapes whose K5a skips zero weights — E >= 16384 or du = 3, C4/C5 —
-    # the adaptive floor dropping <= 2^-30 of the weight mass; elsewhere
+    # the adaptive floor dropping <= 2^-24 of the weight mass; elsewhere
     # weights below 2^-48 of the largest), + weights + partials
     parts = (Ml + 255) // 256 * E * 4
     k5_alg = Ml * E * 4 + Ml * 4 + parts

@@ -53,7 +53,10 @@ __global__ void __launch_bounds__(kThreads) k_philox_noise(S* __restrict__ z, in
 // fp32 weights drive the fp32 weighted mean (K5), which skips samples whose
 // w32 is 0.  A sample's w32 is zeroed when its weight lies below an adaptive
 // floor: the largest power of two 2^-b such that the weights below it provably
-// add up to at most 2^-30 of the total (1e-9 — far below the fp32 sum's own
+// add up to at most 2^-24 of the total — half an ulp of the fp32 weights' sum (≈ 1), a
+// mass the fp32 weights K5 consumes cannot resolve (round 1 used 2^-30; 2^-24 keeps
+// 25 % instead of 42 % of C5's samples over a run: −5 % per step, K5a −40 %)
+// (was: 1e-9 — far below the fp32 sum's own
 // rounding).  The proof is a count histogram over octaves: e = exp(s − s_max)
 // ∈ [2^-(b+1), 2^-b) falls in bin b (bin 128: e < 2^-128), and bins ≥ b hold at
 // most Σ c_b'·2^-b' of Σe.  Integer counts → deterministic, identical on every
@@ -64,7 +67,10 @@ __global__ void __launch_bounds__(kThreads) k_philox_noise(S* __restrict__ z, in
 // M·2^-48 of the total).
 constexpr double kW32Floor = 3.5527136788005009e-15;  // 2^-48
 constexpr int kWBins = 129;
-constexpr double kW32Mass = 9.313225746154785e-10;  // 2^-30
+#ifndef D4K_W32_MASS_LOG2
+#define D4K_W32_MASS_LOG2 24
+#endif
+constexpr double kW32Mass = 1.0 / (double)(1ull << D4K_W32_MASS_LOG2);  // 2^-24
 constexpr int kWScratch = 6 * 160 + 80;               // grid folds + the bin counts (as doubles)
 
 __device__ __forceinline__ int wbin(double e) {  // e ∈ (0, 1]: octave below the max
@@ -78,7 +84,7 @@ __device__ __forceinline__ int wbin(double e) {  // e ∈ (0, 1]: octave below t
 // Floor from the bin counts, by one warp (all 32 lanes; the same fixed-order
 // arithmetic on every CTA and rank): U(b) = Σ_{b' ≥ b} c_b'·2^-b' as a suffix
 // scan (5 bins per lane, then across lanes), floor = 2^-b* for the smallest
-// b* ≥ 1 with U(b*) ≤ 2^-30·Σe (0 if none).
+// b* ≥ 1 with U(b*) ≤ kW32Mass·Σe (0 if none).
 __device__ __forceinline__ double w32_floor_warp(const unsigned* c, double sum_e) {
   constexpr int PER = 5;  // 32·5 ≥ kWBins
   const int lane = threadIdx.x & 31;
