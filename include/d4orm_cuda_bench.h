@@ -15,6 +15,10 @@ int d4orm_cuda_fp32_peak(int device, int reps, double* tflops, double* sm_clock_
  * (planar teams of 33..64 robots), 0 = robot tiles, -1 = no problem set. */
 struct d4orm_cuda_ctx;
 int d4orm_cuda_fitness_path(const struct d4orm_cuda_ctx* ctx);
+/* Which K2+K3 kernel the context's last fitness launch (or captured step) used:
+ * 0 = k_rollout_fitness, 1 = the time-segmented kernel, 2 = the 32-step-window
+ * pair-list kernel (k_rollout_fitness_pl32), -1 = none yet. */
+int d4orm_cuda_last_fit_kernel(const struct d4orm_cuda_ctx* ctx);
 /* How the context's last run formed the weighted mean (K5a): 1 = regenerated
  * the Philox noise (no z rows stored, k_wmean_regen), 0 = read the z rows
  * K2+K3 stored, -1 = no run yet. */

@@ -114,6 +114,7 @@ def lib() -> C.CDLL:
     L.d4orm_cuda_launches_per_step.argtypes = [vp]
     L.d4orm_cuda_fitness_path.argtypes = [vp]
     L.d4orm_cuda_k5_regen.argtypes = [vp]
+    L.d4orm_cuda_last_fit_kernel.argtypes = [vp]
     L.d4orm_cuda_last_w32.argtypes = [vp, C.POINTER(C.c_float), i64]
     L.d4orm_cuda_mppi_solve.argtypes = [vp, C.POINTER(MppiConfig_C), dp, dp, C.POINTER(IterationRec_C),
                                         C.POINTER(i32), dp, C.POINTER(i32)]

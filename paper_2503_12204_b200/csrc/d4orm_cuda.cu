@@ -37,6 +37,8 @@ namespace d4k {
 template <typename S, int KIND>
 cudaError_t launch_k23(int tb, int maxw, int noise, bool pl, dim3 grid, int threads, size_t smem, cudaStream_t st,
                        const FitParams<S>& p);
+template <int KIND>
+cudaError_t launch_pl32(cudaStream_t st, const FitParams<float>& p);  // k_pl32.cuh
 }
 
 namespace {
@@ -149,6 +151,7 @@ struct d4orm_cuda_ctx {
   std::vector<double> starts, goals, obs_c, obs_r;
   int TB = 16, Rp = 16, MAXW = 2, spc = 16, TC = 16;
   bool pl = false;  // fp32 pair-list fitness (planar, 33..64 robots)
+  int last_fit = -1;  // K2+K3 kernel of the last launch: 0 k_rollout_fitness, 1 time-segmented, 2 k_rollout_fitness_pl32
   size_t smem32 = 0, smem64 = 0;
   int TC32 = 16, TC64 = 16;
 
@@ -502,12 +505,37 @@ bool use_seg(const d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f) {
   return (Mg + ctx->spc - 1) / ctx->spc < 2 * ctx->num_sms;
 }
 
+inline bool pl32_enabled() {
+  const char* e = std::getenv("D4ORM_PL32");
+  return !e || std::atoi(e) != 0;
+}
+
 template <typename S>
 cudaError_t launch_fit(d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f, size_t smem, bool fused) {
   if constexpr (std::is_same<S, float>::value) {
-    if (use_seg(ctx, f)) return d4k::launch_seg(ctx->prob.kind, fused, f.M, ctx->s_main, f);
+    if (use_seg(ctx, f)) {
+      ctx->last_fit = 1;
+      return d4k::launch_seg(ctx->prob.kind, fused, f.M, ctx->s_main, f);
+    }
   }
+  ctx->last_fit = 0;
   const bool pl = std::is_same<S, float>::value && ctx->pl;
+  if constexpr (std::is_same<S, float>::value) {
+    // production pair-list launches (Philox drawn in the kernel, scalar std, no
+    // state/control output): the 32-step-window kernel, 16 warps per SM
+    // (k_pl32.cuh; bitwise the 64-step kernel's rewards).  Knob D4ORM_PL32=0.
+    if (pl && fused && !f.sdv && !f.states_out && !f.controls_out && pl32_enabled()) {
+      ctx->last_fit = 2;
+      switch (ctx->prob.kind) {
+        case 0: return d4k::launch_pl32<0>(ctx->s_main, f);
+        case 1: return d4k::launch_pl32<1>(ctx->s_main, f);
+        case 3: return d4k::launch_pl32<3>(ctx->s_main, f);
+        case 5: return d4k::launch_pl32<5>(ctx->s_main, f);
+        default: break;
+      }
+      ctx->last_fit = 0;
+    }
+  }
   const dim3 grid((unsigned)((f.M + ctx->spc - 1) / ctx->spc));
   const int th = ctx->spc * ctx->Rp;
   switch (ctx->prob.kind) {
@@ -1087,7 +1115,7 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
                       std::to_string(ctx->num_sms);
   for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN", "D4ORM_PDL",
                         "D4ORM_FUSE_TAIL", "D4ORM_K4CLUSTER", "D4ORM_K4CTA", "D4ORM_SEGS", "D4ORM_TREEPAR",
-                        "D4ORM_K5CLASS", "D4ORM_K5REV"}) {
+                        "D4ORM_K5CLASS", "D4ORM_K5REV", "D4ORM_PL32"}) {
     const char* v = std::getenv(k);
     knobs += std::string("|") + (v ? v : "-");
   }
@@ -2119,6 +2147,8 @@ int d4orm_cuda_fitness_path(const d4orm_cuda_ctx* ctx) {
   if (!ctx || !ctx->has_problem) return -1;
   return ctx->pl ? 1 : 0;
 }
+
+int d4orm_cuda_last_fit_kernel(const d4orm_cuda_ctx* ctx) { return ctx ? ctx->last_fit : -1; }
 
 int d4orm_cuda_last_w32(d4orm_cuda_ctx* ctx, float* out, int64_t m) {
   if (!ctx || !out || m < 0 || (size_t)m > ctx->w32.n) return D4ORM_E_INVALID;

@@ -665,14 +665,15 @@ __device__ __forceinline__ int chunk_key(float x, int k, int Rp2, bool real) {
 // Pointers advance by a stride per step (no per-step 64-bit index math).  The
 // returned value is 0 unless some state went non-finite (NaN/inf propagate
 // through fma(x, 0, acc)); the caller then replays the chunk exactly.
-template <int KIND, bool FULL, bool SDV, bool PLB>
+template <int KIND, bool FULL, bool SDV, bool PLB, int KPFT = kPFf<KIND>, int RDUC = 0>
 __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, const float* bmp, const float* sdp,
-                                            float* zp, int RDU,
+                                            float* zp, int RDU_rt,
                                             uint64_t m, int kA, uint32_t g0, uint2 key, float* px, float* py, float* pz,
                                             int RS, float* x, float& eff32, float& chk, const float* ng, float ginv,
                                             float& gsd, float4& bx) {
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
-  constexpr int KPF = kPFf<KIND>;
+  constexpr int KPF = KPFT;  // block depth (steps); RDUC: the row stride R·du when known at compile time
+  const int RDU = RDUC ? RDUC : RDU_rt;
   float bq[KPF][DU], sq[SDV ? KPF : 1][DU];
 #pragma unroll
   for (int j = 0; j < KPF; ++j) {

@@ -6,6 +6,7 @@
 #pragma once
 
 #include "d4orm_kernels.cuh"
+#include "k_pl32.cuh"
 
 namespace d4k {
 
@@ -54,6 +55,7 @@ cudaError_t launch_k23(int tb, int maxw, int noise, bool pl, dim3 grid, int thre
   template cudaError_t launch_k23<float, KIND>(int, int, int, bool, dim3, int, size_t, cudaStream_t,   \
                                                const FitParams<float>&);                                \
   template cudaError_t launch_k23<double, KIND>(int, int, int, bool, dim3, int, size_t, cudaStream_t,  \
-                                                const FitParams<double>&);
+                                                const FitParams<double>&);                               \
+  template cudaError_t launch_pl32<KIND>(cudaStream_t, const FitParams<float>&);
 
 }  // namespace d4k

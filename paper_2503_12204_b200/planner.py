@@ -242,6 +242,11 @@ class GpuDenoiser:
         """fp32 fitness form for the current problem: 1 pair list, 0 tiles."""
         return self._L.d4orm_cuda_fitness_path(self._h)
 
+    def last_fit_kernel(self) -> int:
+        """K2+K3 kernel of the last fitness launch: 0 k_rollout_fitness, 1 the
+        time-segmented kernel, 2 k_rollout_fitness_pl32 (32-step windows)."""
+        return self._L.d4orm_cuda_last_fit_kernel(self._h)
+
     # ---------------------------------------------------------- anytime loop
     def solve(self, cfg: DenoiserConfig, max_iterations: int = 10, stop_on_success: bool = True,
               deadline_seconds: float | None = None, on_iteration=None):
