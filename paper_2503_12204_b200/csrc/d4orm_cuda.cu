@@ -39,6 +39,8 @@ cudaError_t launch_k23(int tb, int maxw, int noise, bool pl, dim3 grid, int thre
                        const FitParams<S>& p);
 template <int KIND>
 cudaError_t launch_pl32(cudaStream_t st, const FitParams<float>& p);  // k_pl32.cuh
+template <int KIND>
+cudaError_t launch_small(int rp, cudaStream_t st, const FitParams<float>& p);  // k_small.cuh
 }
 
 namespace {
@@ -151,7 +153,7 @@ struct d4orm_cuda_ctx {
   std::vector<double> starts, goals, obs_c, obs_r;
   int TB = 16, Rp = 16, MAXW = 2, spc = 16, TC = 16;
   bool pl = false;  // fp32 pair-list fitness (planar, 33..64 robots)
-  int last_fit = -1;  // K2+K3 kernel of the last launch: 0 k_rollout_fitness, 1 time-segmented, 2 k_rollout_fitness_pl32
+  int last_fit = -1;  // K2+K3 kernel of the last launch: 0 k_rollout_fitness, 1 time-segmented, 2 k_rollout_fitness_pl32, 3 k_rollout_fitness_small
   size_t smem32 = 0, smem64 = 0;
   int TC32 = 16, TC64 = 16;
 
@@ -505,6 +507,11 @@ bool use_seg(const d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f) {
   return (Mg + ctx->spc - 1) / ctx->spc < 2 * ctx->num_sms;
 }
 
+inline bool small_enabled() {
+  const char* e = std::getenv("D4ORM_SMALL");
+  return !e || std::atoi(e) != 0;
+}
+
 inline bool pl32_enabled() {
   const char* e = std::getenv("D4ORM_PL32");
   return !e || std::atoi(e) != 0;
@@ -534,6 +541,21 @@ cudaError_t launch_fit(d4orm_cuda_ctx* ctx, const d4k::FitParams<S>& f, size_t s
         default: break;
       }
       ctx->last_fit = 0;
+    }
+    // ... and small teams (R <= 16: robot tiles of 8, no culling, 16-step chunks):
+    // the lean one-wave kernel (k_small.cuh; bitwise the general kernel's rewards).
+    // Knob D4ORM_SMALL=0.
+    if (!pl && fused && !f.sdv && !f.states_out && !f.controls_out && !f.cull && ctx->TB == 8 &&
+        (ctx->Rp == 8 || ctx->Rp == 16) && f.TC == 16 && small_enabled()) {
+      ctx->last_fit = 3;
+      switch (ctx->prob.kind) {
+        case 0: return d4k::launch_small<0>(ctx->Rp, ctx->s_main, f);
+        case 1: return d4k::launch_small<1>(ctx->Rp, ctx->s_main, f);
+        case 2: return d4k::launch_small<2>(ctx->Rp, ctx->s_main, f);
+        case 3: return d4k::launch_small<3>(ctx->Rp, ctx->s_main, f);
+        case 4: return d4k::launch_small<4>(ctx->Rp, ctx->s_main, f);
+        default: return d4k::launch_small<5>(ctx->Rp, ctx->s_main, f);
+      }
     }
   }
   const dim3 grid((unsigned)((f.M + ctx->spc - 1) / ctx->spc));
@@ -1115,7 +1137,7 @@ std::string graph_key_of(d4orm_cuda_ctx* ctx, const RunShape& rs) {
                       std::to_string(ctx->num_sms);
   for (const char* k : {"D4ORM_SEG", "D4ORM_CULL", "D4ORM_ZKEEP", "D4ORM_Q", "D4ORM_K5REGEN", "D4ORM_PDL",
                         "D4ORM_FUSE_TAIL", "D4ORM_K4CLUSTER", "D4ORM_K4CTA", "D4ORM_SEGS", "D4ORM_TREEPAR",
-                        "D4ORM_K5CLASS", "D4ORM_K5REV", "D4ORM_PL32"}) {
+                        "D4ORM_K5CLASS", "D4ORM_K5REV", "D4ORM_PL32", "D4ORM_SMALL"}) {
     const char* v = std::getenv(k);
     knobs += std::string("|") + (v ? v : "-");
   }

@@ -7,6 +7,7 @@
 
 #include "d4orm_kernels.cuh"
 #include "k_pl32.cuh"
+#include "k_small.cuh"
 
 namespace d4k {
 
@@ -56,6 +57,7 @@ cudaError_t launch_k23(int tb, int maxw, int noise, bool pl, dim3 grid, int thre
                                                const FitParams<float>&);                                \
   template cudaError_t launch_k23<double, KIND>(int, int, int, bool, dim3, int, size_t, cudaStream_t,  \
                                                 const FitParams<double>&);                               \
-  template cudaError_t launch_pl32<KIND>(cudaStream_t, const FitParams<float>&);
+  template cudaError_t launch_pl32<KIND>(cudaStream_t, const FitParams<float>&);                       \
+  template cudaError_t launch_small<KIND>(int, cudaStream_t, const FitParams<float>&);
 
 }  // namespace d4k

@@ -13,6 +13,7 @@ d4orm_cuda_weighted_mean, and the host-exchange multi-rank path is exercised
 by tests/test_gpu_multirank.py.  Shapes are kept tiny (racecheck is slow).
 """
 import sys
+import os
 import time
 from pathlib import Path
 
@@ -42,10 +43,14 @@ def main():
         assert np.isfinite(v).all()
 
     c5 = S.baseline_config(5).problem.with_horizon(64)
-    run("C5 pair list + K5a regen + adaptive floor (fp32, Philox)", lambda: denoise(c5, 512))
+    run("C5 pair list, 32-step windows (k_pl32) + K5a regen + adaptive floor (fp32, Philox)", lambda: denoise(c5, 512))
+    run("C5 pair list, ragged horizon / odd batch (k_pl32)", lambda: denoise(c5.with_horizon(41), 511))
+    os.environ["D4ORM_PL32"] = "0"
+    run("C5 pair list, 64-step kernel (D4ORM_PL32=0)", lambda: denoise(c5, 512))
+    os.environ.pop("D4ORM_PL32")
     run("C5 stored z (host noise)", lambda: denoise(c5, 512, noise=d4.NOISE_HOST))
     r40 = S.random_square(40, 8.0, 3, S.HOLO2D_VEL, robot_radius=0.15, horizon=32, lower=[-1, -1], upper=[1, 1])
-    run("R40 tile path, x-strip culling", lambda: denoise(r40, 512))
+    run("R40 pair list with padding lanes (k_pl32, runtime row stride)", lambda: denoise(r40, 512))
     run("C2 small tiles + obstacles", lambda: denoise(S.baseline_config(2).problem.with_horizon(32), 1024))
     run("C3 unicycle", lambda: denoise(S.baseline_config(3).problem.with_horizon(32), 1024))
     run("C4 3-D (du = 3, K5a regen)", lambda: denoise(S.baseline_config(4).problem.with_horizon(32), 1024))
