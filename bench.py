@@ -368,14 +368,15 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (seeded scenario generators, Philox noise)", "config": config_json(rc, world),
-        "roofline": {"kernel": "k_rollout_fitness (K2+K3)", "bound": "fp32", "achieved": achieved, "peak": peak_tf.value,
+        "roofline": {"kernel": K23_KERNELS.get(g.last_fit_kernel(), "k_rollout_fitness") + " (K2+K3)", "bound": "fp32", "achieved": achieved, "peak": peak_tf.value,
                      "unit": "TFLOP/s", "frac": achieved / peak_tf.value if peak_tf.value else None,
                      "traffic": traffic, "traffic_source": traffic_src, "flops_per_eval": F, "evals_per_launch": Ml,
                      "launch_ms": k23_ms, "ncu": _ncu_summary(rc.name),
                      "peak_source": "measured live: d4orm_cuda_fp32_peak (FFMA2 over all SMs); MEASURED_PEAKS.json has no FP32 figure",
                      "note": "achieved = SURVEY 8d algorithmic FLOPs (every unordered pair and robot-obstacle test counted) / "
+                             "launch time — frac can exceed 1: it is not a hardware utilisation; "
                              "launch time; the kernel culls tests exactly, so the executed FMA-pipe utilisation is lower "
-                             "(ncu, profiles/r01_ncu_k23k5_c5_v17.md)"},
+                             "(the `ncu` key: the committed ncu --set full capture of this kernel)"},
         "kernel_ms": {"K1_philox": None, "K2K3_rollout_fitness": kms[1], "K4_weights": kms[2],
                       "K5_wmean_partial": kms[3], "K5_tree_update": kms[4],
                       "note": "K1 (Philox + Box-Muller) is fused into K2+K3 on the fp32 path: the noise is drawn in "
@@ -447,6 +448,11 @@ def f64_throughput(d4, rc, device: int) -> dict:
     return {"value": rc.samples * steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
             "warmup": 3, "dtype": "f64",
             "note": "fp64 parity instantiation (PREC_F64: z stored and read, no culling, reference loop order)"}
+
+
+# d4orm_cuda_last_fit_kernel: which K2+K3 kernel the captured step launches
+K23_KERNELS = {0: "k_rollout_fitness", 1: "k_rollout_fitness_seg", 2: "k_rollout_fitness_pl32",
+               3: "k_rollout_fitness_small"}
 
 
 def _ncu_summary(name: str):

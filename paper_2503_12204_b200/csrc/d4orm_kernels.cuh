@@ -860,8 +860,13 @@ struct RegenArgs {
   float* partial;  // [chunks][E]
 };
 
+#ifdef D4K_REGEN_MINB  // experiment knob: resident CTAs per SM the kernel is register-capped for
+#define D4K_REGEN_LB __launch_bounds__(256, D4K_REGEN_MINB)
+#else
+#define D4K_REGEN_LB __launch_bounds__(256)
+#endif
 template <int SUB>
-__global__ void __launch_bounds__(256) k_wmean_regen(const RegenArgs a, const float* __restrict__ w) {
+__global__ void D4K_REGEN_LB k_wmean_regen(const RegenArgs a, const float* __restrict__ w) {
   pdl_wait();
   constexpr int GROUPS = 256 / SUB, LANES = 256 / SUB;
   __shared__ float red[SUB][GROUPS][4];

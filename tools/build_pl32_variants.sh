@@ -20,5 +20,6 @@ while [ $# -ge 2 ]; do
   wait
   OBJS=$(ls $P/build/*.o | grep -v k23_k)
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $P/libd4orm_exp_$NAME.so $OBJS $D/k23_k*.cu.o -ldl -lcudart
+  rm -rf $D
   echo built $P/libd4orm_exp_$NAME.so
 done

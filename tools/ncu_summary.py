@@ -82,7 +82,8 @@ def main():
     if k23:
         sj = ROOT / "profiles" / "ncu_summary.json"
         data = json.loads(sj.read_text()) if sj.exists() else {}
-        data[name] = {"kernel": "k_rollout_fitness (K2+K3)", "issue_active_pct": k23["issue_pct"],
+        kname = k23["kernel"].split("(")[0].replace("void ", "").strip()
+        data[name] = {"kernel": f"{kname} (K2+K3)", "issue_active_pct": k23["issue_pct"],
                       "fma_pipe_cycles_pct": k23["fma_pct"], "fma_pipe_inst_pct": k23["fma_inst_pct"],
                       "alu_pipe_pct": k23["alu_pct"],
                       "xu_pipe_pct": k23["xu_pct"], "warps_per_sm": k23["warps_per_sm"], "registers": k23["regs"],
@@ -93,7 +94,7 @@ def main():
         t[name] = (k23["dram_read"] or 0) + (k23["dram_write"] or 0)
         t.pop("_source", None)
         t.setdefault("_sources", {})[name] = (f"profiles/{Path(md).name} (ncu --set full, one launch of "
-                                              "k_rollout_fitness: dram__bytes_read.sum + dram__bytes_write.sum)")
+                                              f"{kname}: dram__bytes_read.sum + dram__bytes_write.sum)")
         tj.write_text(json.dumps(t, indent=1) + "\n")
 
 
