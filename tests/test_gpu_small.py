@@ -114,3 +114,24 @@ def test_small_not_used_for_c1_or_host_controls():
         assert g.last_fit_kernel() == 0
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("kind", [S.HOLO2D_VEL, S.UNICYCLE, S.HOLO3D])
+def test_small_reports_nonfinite_state(kind):
+    """An infinite base control with unbounded controls: the chunk's watch
+    triggers the exact replay, which reports the first failing robot and step
+    like dynamics.cpp:81-84 (second 16-step chunk, padding lanes)."""
+    p = _square(12, 8.0, 21, kind, horizon=40, robot_radius=0.2, n_obs=2)
+    du = p.du
+    p = S.Problem(kind, starts=p.starts, goals=p.goals, horizon=40, lower=[-np.inf] * du, upper=[np.inf] * du,
+                  robot_radius=0.2, obs_centers=p.obs_centers, obs_radii=p.obs_radii)
+    base = np.zeros((40, 12, du))
+    base[21, 5, 0] = np.inf
+    g = d4.GpuDenoiser(p)
+    try:
+        with pytest.raises(d4.D4ormError,
+                           match="run_denoising: sample 0 at step 5: rollout: non-finite state for robot 5 at step 22"):
+            g.run_denoising(base, d4.DenoiserConfig(steps=5, batch=8192, seed=1))
+        assert g.last_fit_kernel() == 3
+    finally:
+        g.close()
