@@ -36,6 +36,9 @@ constexpr int kPl32Threads = 128, kPl32TC = 32, kPl32Rp = 64, kPl32RS = 66, kPl3
 #ifndef D4K_PL32_KPF
 #define D4K_PL32_KPF 8
 #endif
+#ifndef D4K_PL32_RANK
+#define D4K_PL32_RANK 64  // steps between rankings (a multiple of 32)
+#endif
 #ifndef D4K_PL32_MINB
 #define D4K_PL32_MINB 5
 #endif
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
   for (int t0 = 0; t0 < T; t0 += TC) {
     // ===== every 64 steps: rank the sample's robots by x (strips of 16), then by y
     // inside a strip, so column pairs (2l, 2l+1) are neighbours in both coordinates
-    if ((t0 & 63) == 0) {
+    if ((t0 % D4K_PL32_RANK) == 0) {
       if (liveA) sm.key[tid] = chunk_key(x[0], kA, 64, robotA);
       __syncthreads();
       if (robotA) {

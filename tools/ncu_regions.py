@@ -59,6 +59,14 @@ ANCHORS = {
                 ("Exact replay of a chunk", "rollout: replay"), ("__launch_bounds__", "other (setup, barriers)"),
                 ("rank the sample's robots", "chunk ranking"), ("phase A: integrate", "rollout: controls, clamp, goal, stores, boxes"),
                 ("phase B: fitness", "phase-B glue + final reduction")],
+    "k_pl32.cuh": [("namespace d4k", "other (setup, barriers)"),
+                   ("Half h of one (sample, 32-step window) item", "fitness (pair list): boxes + self pairs"),
+                   ("pair-pair blocks (l, l + d mod 32) for this half", "fitness (pair list): pair-pair liveness + loop"),
+                   ("obstacles o ≡ h (mod 2): pair boxes", "fitness (pair list): obstacles"),
+                   ("template <int KIND, bool RFULL>", "other (setup, barriers)"),
+                   ("every 64 steps: rank the sample", "chunk ranking"),
+                   ("phase A: integrate the window", "rollout: controls, clamp, goal, stores, boxes"),
+                   ("phase B: this warp's half", "phase-B glue + final reduction")],
 }
 _tables = {}
 
