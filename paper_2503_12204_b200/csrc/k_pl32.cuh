@@ -86,13 +86,16 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
   const float4 b0 = rb[2 * lane], b1 = rb[2 * lane + 1];
   const float4 A = make_float4(fminf(b0.x, b1.x), fminf(b0.y, b1.y), fmaxf(b0.z, b1.z), fmaxf(b0.w, b1.w));
   const float4 Ai = make_float4(A.x - cmh, A.y - cmh, A.z + cmh, A.w + cmh);
+  // the robots' own boxes grown by half the margin (the votes test them against
+  // the partner pair's union box, not union against union: a pair whose union
+  // meets only the gap between this pair's two robots is no candidate)
+  const float4 b0i = make_float4(b0.x - cmh, b0.y - cmh, b0.z + cmh, b0.w + cmh);
+  const float4 b1i = make_float4(b1.x - cmh, b1.y - cmh, b1.z + cmh, b1.w + cmh);
   pb[lane] = Ai;
   pb[lane + 32] = Ai;
   if (h == 0) {  // the pair's own test (2l, 2l+1)
     uint32_t bits = full;
     if (cull) {
-      const float4 b0i = make_float4(b0.x - cmh, b0.y - cmh, b0.z + cmh, b0.w + cmh);
-      const float4 b1i = make_float4(b1.x - cmh, b1.y - cmh, b1.z + cmh, b1.w + cmh);
       bits = __ballot_sync(full, boxes_meet(b0i, b1i));
     }
     while (bits) {
@@ -115,7 +118,7 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
     const int d = 2 * i + 1 + h;
     if (cull) {
       const float4 B = pb[lane + d];
-      lv[i] = __ballot_sync(full, (d < 16 || lane < 16) && boxes_meet(Ai, B));
+      lv[i] = __ballot_sync(full, (d < 16 || lane < 16) && (boxes_meet(b0i, B) || boxes_meet(b1i, B)));
     } else {
       lv[i] = d < 16 ? full : 0xffffu;
     }
@@ -137,8 +140,11 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
     for (int q = 0; q < 8; ++q) {
       const int o = o0 + 2 * q;
       ov[q] = 0;
-      if (o < n_obs)
-        ov[q] = cull ? __ballot_sync(full, boxes_meet(A, *reinterpret_cast<const float4*>(sm.opl + 8 * o + 4))) : full;
+      if (o < n_obs) {
+        // the pair's two robot boxes, not their union: an obstacle in the gap between the two is no candidate
+        const float4 ob = *reinterpret_cast<const float4*>(sm.opl + 8 * o + 4);
+        ov[q] = cull ? __ballot_sync(full, boxes_meet(b0, ob) || boxes_meet(b1, ob)) : full;
+      }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
