@@ -21,7 +21,7 @@
 //           phase barrier (a robot-step in conflict with several others counts
 //           once, reward.cpp:104-110).
 //
-// The ranking (x strips of 16, y inside) is renewed every 64 steps and the
+// The ranking (x strips of 8, y inside) is renewed every 64 steps and the
 // per-robot fp32 goal / effort partials are folded every 64 steps, exactly as
 // the 64-step kernel does, so rewards and counts are bitwise those of
 // k_rollout_fitness<float, KIND, 16, 2, 1, true> (tests/test_gpu_pl32.py; the
@@ -35,6 +35,9 @@ namespace d4k {
 constexpr int kPl32Threads = 128, kPl32TC = 32, kPl32Rp = 64, kPl32RS = 66, kPl32Spc = 2;
 #ifndef D4K_PL32_KPF
 #define D4K_PL32_KPF 8
+#endif
+#ifndef D4K_PL32_STRIP
+#define D4K_PL32_STRIP 8  // robots per x strip of the ranking (y order inside a strip)
 #endif
 #ifndef D4K_PL32_RANK
 #define D4K_PL32_RANK 64  // steps between rankings (a multiple of 32)
@@ -224,7 +227,7 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
   __syncthreads();
 
   for (int t0 = 0; t0 < T; t0 += TC) {
-    // ===== every 64 steps: rank the sample's robots by x (strips of 16), then by y
+    // ===== every 64 steps: rank the sample's robots by x (strips of D4K_PL32_STRIP), then by y
     // inside a strip, so column pairs (2l, 2l+1) are neighbours in both coordinates
     if ((t0 % D4K_PL32_RANK) == 0) {
       if (liveA) sm.key[tid] = chunk_key(x[0], kA, 64, robotA);
@@ -252,10 +255,10 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
       }
       __syncthreads();
       if (robotA) {
-        const int4* kv = reinterpret_cast<const int4*>(sm.key + sA * Rp + (rA & ~15));
-        int r = rA & ~15;
+        const int4* kv = reinterpret_cast<const int4*>(sm.key + sA * Rp + (rA & ~(D4K_PL32_STRIP - 1)));
+        int r = rA & ~(D4K_PL32_STRIP - 1);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < D4K_PL32_STRIP / 4; ++j) {
           const int4 v = kv[j];
           r += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
         }
