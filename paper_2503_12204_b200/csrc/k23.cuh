@@ -665,7 +665,7 @@ __device__ __forceinline__ int chunk_key(float x, int k, int Rp2, bool real) {
 // Pointers advance by a stride per step (no per-step 64-bit index math).  The
 // returned value is 0 unless some state went non-finite (NaN/inf propagate
 // through fma(x, 0, acc)); the caller then replays the chunk exactly.
-template <int KIND, bool FULL, bool SDV, bool PLB, int KPFT = kPFf<KIND>, int RDUC = 0>
+template <int KIND, bool FULL, bool SDV, bool PLB, int KPFT = kPFf<KIND>, int RDUC = 0, bool EFFORT = true>
 __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, const float* bmp, const float* sdp,
                                             float* zp, int RDU_rt,
                                             uint64_t m, int kA, uint32_t g0, uint2 key, float* px, float* py, float* pz,
@@ -741,7 +741,7 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
         u[0] = fminf(fmaxf(lo_f(v), p.lower[0]), p.upper[0]);
         u[1] = fminf(fmaxf(hi_f(v), p.lower[1]), p.upper[1]);
         const uint64_t uc = pack2(u[0], u[1]);
-        eff2 = ffma2(uc, uc, eff2);
+        if constexpr (EFFORT) eff2 = ffma2(uc, uc, eff2);
         if constexpr (KIND == HOLO2D_VEL) {  // rk4: x + dt·u (fp32 velocity-input closed form)
           const uint64_t xn = ffma2(pack2(p.dt, p.dt), uc, pack2(x[0], x[1]));
           x[0] = lo_f(xn);
@@ -754,7 +754,7 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
         for (int d = 0; d < DU; ++d) {
           const float sdj = SDV ? sq[SDV ? j : 0][d] : p.sd;
           u[d] = fminf(fmaxf(fmaf(sdj, nz[j * DU + d], bq[j][d]), p.lower[d]), p.upper[d]);
-          eff32 = fmaf(u[d], u[d], eff32);
+          if constexpr (EFFORT) eff32 = fmaf(u[d], u[d], eff32);
         }
         rk4<KIND>(x, u, p.dt, p.half_dt, p.dt6);
       }

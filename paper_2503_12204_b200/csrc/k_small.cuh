@@ -37,7 +37,7 @@ __host__ __device__ inline size_t small_smem_bytes(int RP, int n_obs) {
   return (b + 15) & ~size_t(15);
 }
 
-template <int KIND, int RP>
+template <int KIND, int RP, bool EFFORT>
 __global__ void __launch_bounds__(kSmallThreads, D4K_SMALL_MINB) k_rollout_fitness_small(const __grid_constant__ FitParams<float> p) {
   pdl_wait();
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
@@ -121,10 +121,10 @@ __global__ void __launch_bounds__(kSmallThreads, D4K_SMALL_MINB) k_rollout_fitne
         const int nb = nsteps - tc;
         const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
         if (nb >= KPF)
-          fused_block<KIND, true, false, false, KPF>(p, KPF, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0, key,
+          fused_block<KIND, true, false, false, KPF, 0, EFFORT>(p, KPF, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0, key,
                                                      px, py, pz, RS, x, eff32, chk, ng, ginv, gsd, bx);
         else
-          fused_block<KIND, false, false, false, KPF>(p, nb, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0,
+          fused_block<KIND, false, false, false, KPF, 0, EFFORT>(p, nb, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0,
                                                       key, px, py, pz, RS, x, eff32, chk, ng, ginv, gsd, bx);
         bmp += KPF * RDU;
         zp += KPF * RDU;
@@ -200,8 +200,14 @@ cudaError_t launch_small(int rp, cudaStream_t st, const FitParams<float>& p) {
     if (e != cudaSuccess) return e;
     return launch_step(fn, grid, dim3(kSmallThreads), smem, st, false, p);
   };
-  if (rp == 16) return launch(k_rollout_fitness_small<KIND, 16>);
-  if (rp == 8) return launch(k_rollout_fitness_small<KIND, 8>);
+  // the effort accumulation is compiled out for the reference's reward (effort_weight = 0)
+  if (p.w_e != 0.0) {
+    if (rp == 16) return launch(k_rollout_fitness_small<KIND, 16, true>);
+    if (rp == 8) return launch(k_rollout_fitness_small<KIND, 8, true>);
+  } else {
+    if (rp == 16) return launch(k_rollout_fitness_small<KIND, 16, false>);
+    if (rp == 8) return launch(k_rollout_fitness_small<KIND, 8, false>);
+  }
   return cudaErrorInvalidValue;
 }
 
