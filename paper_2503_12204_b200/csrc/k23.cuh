@@ -665,7 +665,8 @@ __device__ __forceinline__ int chunk_key(float x, int k, int Rp2, bool real) {
 // Pointers advance by a stride per step (no per-step 64-bit index math).  The
 // returned value is 0 unless some state went non-finite (NaN/inf propagate
 // through fma(x, 0, acc)); the caller then replays the chunk exactly.
-template <int KIND, bool FULL, bool SDV, bool PLB, int KPFT = kPFf<KIND>, int RDUC = 0, bool EFFORT = true>
+template <int KIND, bool FULL, bool SDV, bool PLB, int KPFT = kPFf<KIND>, int RDUC = 0, bool EFFORT = true,
+          bool ZSTORE = true>
 __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, const float* bmp, const float* sdp,
                                             float* zp, int RDU_rt,
                                             uint64_t m, int kA, uint32_t g0, uint2 key, float* px, float* py, float* pz,
@@ -706,26 +707,26 @@ __device__ __forceinline__ void fused_block(const FitParams<float>& p, int nb, c
     nz[4 * g + 2] = v.z;
     nz[4 * g + 3] = v.w;
   }
-#ifndef D4K_EXPERIMENT_NO_ZSTORE
-  uint64_t zpol;  // L2 policy of the z stores (FitParams::z_keep)
-  if (p.z_keep == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(zpol));
-  else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(zpol));
-#pragma unroll
-  for (int j = 0; j < KPF; ++j) {
-    if (p.z_keep == 2) break;  // K5a regenerates the noise
-    if (FULL || j < nb) {
-      if constexpr (DU == 2) {
-        asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(zp + j * RDU), "f"(nz[2 * j]),
-                     "f"(nz[2 * j + 1]), "l"(zpol) : "memory");
-      } else {
-#pragma unroll
-        for (int d = 0; d < DU; ++d)
-          asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(zp + j * RDU + d), "f"(nz[j * DU + d]),
-                       "l"(zpol) : "memory");
+  if constexpr (ZSTORE) {  // ZSTORE = false: launches whose K5a regenerates the noise (z_keep == 2) carry no store code
+    uint64_t zpol;  // L2 policy of the z stores (FitParams::z_keep)
+    if (p.z_keep == 1) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(zpol));
+    else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(zpol));
+  #pragma unroll
+    for (int j = 0; j < KPF; ++j) {
+      if (p.z_keep == 2) break;  // K5a regenerates the noise
+      if (FULL || j < nb) {
+        if constexpr (DU == 2) {
+          asm volatile("st.global.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(zp + j * RDU), "f"(nz[2 * j]),
+                       "f"(nz[2 * j + 1]), "l"(zpol) : "memory");
+        } else {
+  #pragma unroll
+          for (int d = 0; d < DU; ++d)
+            asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(zp + j * RDU + d), "f"(nz[j * DU + d]),
+                         "l"(zpol) : "memory");
+        }
       }
     }
   }
-#endif
   // two-control kinds: the control pair, its effort and (velocity input) the
   // position update as packed FFMA2 — the same per-lane fma as the scalar form
   constexpr bool PK = DU == 2 && !SDV;

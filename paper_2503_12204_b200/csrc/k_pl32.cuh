@@ -169,7 +169,7 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
   }
 }
 
-template <int KIND, bool RFULL, bool EFFORT>
+template <int KIND, bool RFULL, bool LEAN>
 __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness_pl32(const __grid_constant__ FitParams<float> p) {
   pdl_wait();
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
@@ -283,10 +283,10 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
         const int nb = nsteps - tc;
         const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
         if (nb >= KPF)
-          fused_block<KIND, true, false, true, KPF, RDUC, EFFORT>(p, KPF, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0,
+          fused_block<KIND, true, false, true, KPF, RDUC, !LEAN, !LEAN>(p, KPF, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0,
                                                           key, px, py, px, kPl32RS, x, eff32, chk, ng, ginv, gsd, bx);
         else
-          fused_block<KIND, false, false, true, KPF, RDUC, EFFORT>(p, nb, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA,
+          fused_block<KIND, false, false, true, KPF, RDUC, !LEAN, !LEAN>(p, nb, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA,
                                                            g0, key, px, py, px, kPl32RS, x, eff32, chk, ng, ginv, gsd, bx);
         bmp += KPF * RDU;
         zp += KPF * RDU;
@@ -368,8 +368,9 @@ cudaError_t launch_pl32(cudaStream_t st, const FitParams<float>& p) {
       if (e != cudaSuccess) return e;
       return launch_step(fn, grid, dim3(kPl32Threads), smem, st, false, p);
     };
-    // the effort accumulation is compiled out for the reference's reward (effort_weight = 0)
-    if (p.w_e != 0.0) {
+    // LEAN: the reference's reward (effort_weight = 0) on a launch whose K5a regenerates the
+    // noise (z_keep == 2) — no effort accumulation and no z-store code in the rollout block
+    if (p.w_e == 0.0 && p.z_keep == 2) {
       if (p.R == kPl32Rp) return launch(k_rollout_fitness_pl32<KIND, true, true>);
       return launch(k_rollout_fitness_pl32<KIND, false, true>);
     }

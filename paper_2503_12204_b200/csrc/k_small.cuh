@@ -37,7 +37,7 @@ __host__ __device__ inline size_t small_smem_bytes(int RP, int n_obs) {
   return (b + 15) & ~size_t(15);
 }
 
-template <int KIND, int RP, bool EFFORT>
+template <int KIND, int RP, int LEAN>  // LEAN bit 0: no effort accumulation, bit 1: no z-store code
 __global__ void __launch_bounds__(kSmallThreads, D4K_SMALL_MINB) k_rollout_fitness_small(const __grid_constant__ FitParams<float> p) {
   pdl_wait();
   constexpr int DX = ModelDims<KIND>::DX, DU = ModelDims<KIND>::DU, PD = ModelDims<KIND>::PD;
@@ -121,10 +121,10 @@ __global__ void __launch_bounds__(kSmallThreads, D4K_SMALL_MINB) k_rollout_fitne
         const int nb = nsteps - tc;
         const uint32_t g0 = (uint32_t)((t0 + tc) * DU / 4);
         if (nb >= KPF)
-          fused_block<KIND, true, false, false, KPF, 0, EFFORT>(p, KPF, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0, key,
+          fused_block<KIND, true, false, false, KPF, 0, !(LEAN & 1), !(LEAN & 2)>(p, KPF, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0, key,
                                                      px, py, pz, RS, x, eff32, chk, ng, ginv, gsd, bx);
         else
-          fused_block<KIND, false, false, false, KPF, 0, EFFORT>(p, nb, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0,
+          fused_block<KIND, false, false, false, KPF, 0, !(LEAN & 1), !(LEAN & 2)>(p, nb, bmp, nullptr, zp, RDU, (uint64_t)(p.m_global0 + mA), kA, g0,
                                                       key, px, py, pz, RS, x, eff32, chk, ng, ginv, gsd, bx);
         bmp += KPF * RDU;
         zp += KPF * RDU;
@@ -200,13 +200,18 @@ cudaError_t launch_small(int rp, cudaStream_t st, const FitParams<float>& p) {
     if (e != cudaSuccess) return e;
     return launch_step(fn, grid, dim3(kSmallThreads), smem, st, false, p);
   };
-  // the effort accumulation is compiled out for the reference's reward (effort_weight = 0)
-  if (p.w_e != 0.0) {
-    if (rp == 16) return launch(k_rollout_fitness_small<KIND, 16, true>);
-    if (rp == 8) return launch(k_rollout_fitness_small<KIND, 8, true>);
-  } else {
-    if (rp == 16) return launch(k_rollout_fitness_small<KIND, 16, false>);
-    if (rp == 8) return launch(k_rollout_fitness_small<KIND, 8, false>);
+  // the reference's reward (effort_weight = 0) compiles the effort accumulation out; a launch
+  // whose K5a regenerates the noise (z_keep == 2, e.g. C4) also the z-store code
+  const int lean = p.w_e != 0.0 ? 0 : (p.z_keep == 2 ? 3 : 1);
+  if (rp == 16) {
+    if (lean == 3) return launch(k_rollout_fitness_small<KIND, 16, 3>);
+    if (lean == 1) return launch(k_rollout_fitness_small<KIND, 16, 1>);
+    return launch(k_rollout_fitness_small<KIND, 16, 0>);
+  }
+  if (rp == 8) {
+    if (lean == 3) return launch(k_rollout_fitness_small<KIND, 8, 3>);
+    if (lean == 1) return launch(k_rollout_fitness_small<KIND, 8, 1>);
+    return launch(k_rollout_fitness_small<KIND, 8, 0>);
   }
   return cudaErrorInvalidValue;
 }
