@@ -77,8 +77,10 @@ __device__ __forceinline__ int top_bit(uint32_t v) {  // index of the highest se
 
 // Half h of one (sample, 32-step window) item: called by all 32 lanes of a warp,
 // lane = step.  Returns the conflict / obstacle bits (bit = column) this half finds.
+template <bool CULLC>  // CULLC: culling known on at compile time (production); else `cull_rt` decides
 __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int h, int n_obs, float m2u, float cmh,
-                                          bool cull, uint64_t& conf, uint64_t& obsm) {
+                                          bool cull_rt, uint64_t& conf, uint64_t& obsm) {
+  const bool cull = CULLC || cull_rt;
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const float* X = sm.row(0, s, lane);
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
     // ===== phase B: this warp's half of the window's fitness
     uint64_t conf = 0, obsm = 0;
     if (mB < p.M) {
-      item_pl32(sm, sB, wB, hB, p.n_obs, p.margin_sq, 0.5f * p.cull_margin, p.cull != 0, conf, obsm);
+      item_pl32<LEAN>(sm, sB, wB, hB, p.n_obs, p.margin_sq, 0.5f * p.cull_margin, p.cull != 0, conf, obsm);
       if (hB == 1) sm.msk[sB * 32 + lane] = make_uint4(lo32(conf), hi32(conf), lo32(obsm), hi32(obsm));
     }
     __syncthreads();
@@ -369,8 +371,9 @@ cudaError_t launch_pl32(cudaStream_t st, const FitParams<float>& p) {
       return launch_step(fn, grid, dim3(kPl32Threads), smem, st, false, p);
     };
     // LEAN: the reference's reward (effort_weight = 0) on a launch whose K5a regenerates the
-    // noise (z_keep == 2) — no effort accumulation and no z-store code in the rollout block
-    if (p.w_e == 0.0 && p.z_keep == 2) {
+    // noise (z_keep == 2), culling on — no effort accumulation and no z-store code in the
+    // rollout block, no culling-off paths in the votes
+    if (p.w_e == 0.0 && p.z_keep == 2 && p.cull != 0) {
       if (p.R == kPl32Rp) return launch(k_rollout_fitness_pl32<KIND, true, true>);
       return launch(k_rollout_fitness_pl32<KIND, false, true>);
     }
