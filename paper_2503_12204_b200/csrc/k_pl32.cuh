@@ -98,11 +98,9 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
   const float4 b1i = make_float4(b1.x - cmh, b1.y - cmh, b1.z + cmh, b1.w + cmh);
   pb[lane] = Ai;
   pb[lane + 32] = Ai;
-  if (h == 0) {  // the pair's own test (2l, 2l+1)
-    uint32_t bits = full;
-    if (cull) {
-      bits = __ballot_sync(full, boxes_meet(b0i, b1i));
-    }
+  {  // the pairs' own tests (2l, 2l+1): both warps vote, warp h tests the pairs l ≡ h (mod 2)
+    uint32_t bits = 0x55555555u << h;
+    if (cull) bits &= __ballot_sync(full, boxes_meet(b0i, b1i));
     while (bits) {
       const int l = top_bit(bits);
       bits ^= 1u << l;
