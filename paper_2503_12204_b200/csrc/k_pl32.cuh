@@ -32,7 +32,10 @@
 
 namespace d4k {
 
-constexpr int kPl32Threads = 128, kPl32TC = 32, kPl32Rp = 64, kPl32RS = 66, kPl32Spc = 2;
+#ifndef D4K_PL32_SPC
+#define D4K_PL32_SPC 1  // samples per CTA (64 threads each)
+#endif
+constexpr int kPl32Spc = D4K_PL32_SPC, kPl32Threads = 64 * kPl32Spc, kPl32TC = 32, kPl32Rp = 64, kPl32RS = 66;
 #ifndef D4K_PL32_KPF
 #define D4K_PL32_KPF 8
 #endif
@@ -43,15 +46,16 @@ constexpr int kPl32Threads = 128, kPl32TC = 32, kPl32Rp = 64, kPl32RS = 66, kPl3
 #define D4K_PL32_RANK 64  // steps between rankings (a multiple of 32)
 #endif
 #ifndef D4K_PL32_MINB
-#define D4K_PL32_MINB 5
+#define D4K_PL32_MINB (11 / D4K_PL32_SPC)
 #endif
 
 struct Pl32Smem {
-  float* pos;     // [2 planes][2 samples][32 steps][66]
-  int* key;       // [2][64]
-  float4* rbox;   // [2][64] robot swept boxes of the window (lo.x, lo.y, hi.x, hi.y)
-  float4* pbox;   // [4 warps][64] inflated pair boxes, stored twice (index l and l + 32: no wrap)
-  uint4* msk;     // [2 samples][32 lanes] warp 1's (conflict, obstacle) masks
+  float* pos;     // [2 planes][spc samples][32 steps][66]
+  int* key;       // [spc][64] ranking keys (aliases pbox)
+  float4* rbox;   // [spc][64] robot swept boxes of the window (lo.x, lo.y, hi.x, hi.y)
+  float4* pbox;   // [spc][64] inflated pair boxes, stored twice (index l and l + 32: no wrap); a sample's two
+                  // warps both write it — the same values — and each reads after its own writes
+  uint4* msk;     // [spc][32 lanes] warp 1's (conflict, obstacle) masks
   float* opl;     // [O][8] FitParams::obs_pl
   __device__ __forceinline__ float* row(int c, int s, int tc) const {
     D4K_CHECK(c >= 0 && c < 2 && s >= 0 && s < kPl32Spc && tc >= 0 && tc < kPl32TC);
@@ -61,9 +65,8 @@ struct Pl32Smem {
 
 __host__ __device__ inline size_t pl32_smem_bytes(int n_obs) {
   size_t b = (size_t)2 * kPl32Spc * kPl32TC * kPl32RS * sizeof(float);  // pos (33 792 B; the final reduction aliases it)
-  b += (size_t)kPl32Spc * kPl32Rp * sizeof(int);                          // key
   b += (size_t)kPl32Spc * kPl32Rp * sizeof(float4);                       // rbox
-  b += (size_t)4 * 64 * sizeof(float4);                                   // pbox
+  b += (size_t)kPl32Spc * 64 * sizeof(float4);                            // pbox (the ranking keys alias it)
   b += (size_t)kPl32Spc * 32 * sizeof(uint4);                             // msk
   b += (size_t)8 * (n_obs > 0 ? n_obs : 1) * sizeof(float);               // opl
   return (b + 15) & ~size_t(15);
@@ -86,7 +89,7 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
   const float* X = sm.row(0, s, lane);
   const float* Y = sm.row(1, s, lane);
   const float4* rb = sm.rbox + s * kPl32Rp;
-  float4* pb = sm.pbox + w * 64;
+  float4* pb = sm.pbox + s * 64;
   const uint64_t nm2 = pack2(-m2u, -m2u);
   const float4 b0 = rb[2 * lane], b1 = rb[2 * lane + 1];
   const float4 A = make_float4(fminf(b0.x, b1.x), fminf(b0.y, b1.y), fmaxf(b0.z, b1.z), fmaxf(b0.w, b1.w));
@@ -183,10 +186,12 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
 
   Pl32Smem sm;
   sm.pos = reinterpret_cast<float*>(smem_raw);
-  sm.key = reinterpret_cast<int*>(sm.pos + 2 * spc * TC * kPl32RS);
-  sm.rbox = reinterpret_cast<float4*>(sm.key + spc * Rp);
+  sm.rbox = reinterpret_cast<float4*>(sm.pos + 2 * spc * TC * kPl32RS);
   sm.pbox = sm.rbox + spc * Rp;
-  sm.msk = reinterpret_cast<uint4*>(sm.pbox + 4 * 64);
+  // the ranking keys live in the pair-box array: keys are written and read between the
+  // end-of-window barrier and phase A, pair boxes between the phase barriers
+  sm.key = reinterpret_cast<int*>(sm.pbox);
+  sm.msk = reinterpret_cast<uint4*>(sm.pbox + spc * 64);
   sm.opl = reinterpret_cast<float*>(sm.msk + spc * 32);
   for (int j = tid; j < 8 * p.n_obs; j += nthreads) sm.opl[j] = p.obs_pl[j];  // (c, −L²↑, box)
 
@@ -365,6 +370,8 @@ cudaError_t launch_pl32(cudaStream_t st, const FitParams<float>& p) {
     const dim3 grid((unsigned)((p.M + kPl32Spc - 1) / kPl32Spc));
     auto launch = [&](auto fn) {
       cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
       if (e != cudaSuccess) return e;
       return launch_step(fn, grid, dim3(kPl32Threads), smem, st, false, p);
     };
