@@ -19,12 +19,15 @@
 
 namespace d4k {
 
-constexpr int kSmallThreads = 128, kSmallTC = 16, kSmallTB = 8;
+#ifndef D4K_SMALL_THREADS
+#define D4K_SMALL_THREADS 128
+#endif
+constexpr int kSmallThreads = D4K_SMALL_THREADS, kSmallTC = 16, kSmallTB = 8;
 #ifndef D4K_SMALL_KPF
-#define D4K_SMALL_KPF 4
+#define D4K_SMALL_KPF 8
 #endif
 #ifndef D4K_SMALL_MINB
-#define D4K_SMALL_MINB 7
+#define D4K_SMALL_MINB (7 * 128 / D4K_SMALL_THREADS)
 #endif
 
 template <int PD>
