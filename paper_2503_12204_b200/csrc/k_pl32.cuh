@@ -1,31 +1,36 @@
 // k_pl32.cuh — K2+K3 for planar teams of 33–64 robots on the production path
 // (fp32, Philox noise drawn in registers, scalar std): the pair-list fitness of
-// k23.cuh on 32-step chunks, sized for 5 resident CTAs per SM.
+// k23.cuh on 32-step chunks, one sample per 64-thread CTA, 11 CTAs per SM.
 //
 // k_rollout_fitness<…, PL> keeps a 64-step position tile per sample (71 KB per
 // 128-thread CTA) and 168 registers: 3 CTAs = 12 warps per SM, and ncu shows it
 // latency-bound there (issue 55 %, top stall "wait", no pipe above 40 %).  Here
-// the tile is one 32-step warp window per sample (≈ 41 KB per CTA) and the
-// dedicated kernel needs 91 registers with 8-step rollout blocks, so 5 CTAs =
-// 20 warps are resident: C5 K2+K3 18.9 → 15.7 ms (4 CTAs: 16.7 ms; 16-step
-// blocks at 4 CTAs: 16.9 ms; 4-step blocks at 5 CTAs: 16.3 ms).
+// the tile is one 32-step warp window (19.5 KB per sample) and the dedicated
+// kernel needs 79 registers with 8-step rollout blocks, so 11 CTAs = 22 warps
+// are resident: C5 K2+K3 18.9 → 13.9 ms (history in DESIGN.md §3 / §7).
 //
-//  phase A  thread = (sample, robot): 32 steps in blocks of 8 (fused_block of
-//           k23.cuh: Philox draws, controls, RK4, goal term, swept box); the
-//           row stride of base + mean-scaled variable is a compile-time
-//           constant when R = 64 (RFULL: no 64-bit address arithmetic per load).
-//  phase B  a sample's window is shared by its two warps: lane = step in both,
-//           warp h votes and tests the pair-pair offsets d ≡ h + 1 (mod 2) and
-//           the obstacles o ≡ h (mod 2); warp 1 leaves its conflict / obstacle
-//           masks in shared memory and warp 0 ORs and counts them after the
-//           phase barrier (a robot-step in conflict with several others counts
-//           once, reward.cpp:104-110).
+//  phase A  thread = robot: 32 steps in blocks of 8 (fused_block of k23.cuh:
+//           Philox draws, controls, RK4, goal term, swept box); the row stride
+//           of base + mean-scaled variable is a compile-time constant when
+//           R = 64 (RFULL: no 64-bit address arithmetic per load).  LEAN
+//           launches (the reference's reward, K5a regenerating the noise,
+//           culling on) carry no effort accumulation, no z-store code and no
+//           culling-off paths.
+//  phase B  the window is shared by the sample's two warps: lane = step in both,
+//           warp h votes and tests the pair-pair offsets d ≡ h + 1 (mod 2), the
+//           obstacles o ≡ h (mod 2) and the own pairs l ≡ h (mod 2); warp 1
+//           leaves its conflict / obstacle masks in shared memory and warp 0 ORs
+//           and counts them after the phase barrier (a robot-step in conflict
+//           with several others counts once, reward.cpp:104-110).  Votes test
+//           this pair's two robot boxes (not their union) against the partner
+//           pair's union box / the obstacle's box.
 //
 // The ranking (x strips of 8, y inside) is renewed every 64 steps and the
 // per-robot fp32 goal / effort partials are folded every 64 steps, exactly as
-// the 64-step kernel does, so rewards and counts are bitwise those of
-// k_rollout_fitness<float, KIND, 16, 2, 1, true> (tests/test_gpu_pl32.py; the
-// effort sum differs by fp32 association where effort_weight ≠ 0).
+// the 64-step kernel does, and all culling is exact, so rewards and counts are
+// bitwise those of k_rollout_fitness<float, KIND, 16, 2, 1, true>
+// (tests/test_gpu_pl32.py; the effort sum differs by fp32 association where
+// effort_weight ≠ 0).
 #pragma once
 
 #include "k23.cuh"
@@ -362,7 +367,7 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
   }
 }
 
-// Launch (grid = ⌈M / 2⌉ CTAs of 128 threads).  Planar two-control kinds only.
+// Launch (grid = ⌈M / spc⌉ CTAs of 64·spc threads).  Planar two-control kinds only.
 template <int KIND>
 cudaError_t launch_pl32(cudaStream_t st, const FitParams<float>& p) {
   if constexpr (ModelDims<KIND>::PD == 2 && ModelDims<KIND>::DU == 2) {

@@ -8,7 +8,9 @@
 // the same arithmetic — fused_block for the rollout, item_f32 (robot tiles of
 // 8, expanded-form pair tests) for the fitness, 16-step chunks — with nothing
 // else in it, so that it fits 7 CTAs per SM (72 registers): 1036 slots, every
-// CTA of C2–C4 resident in one wave at 28 warps per SM.
+// CTA of C2–C4 resident in one wave at 28 warps per SM.  LEAN instantiations drop
+// the effort accumulation (effort_weight = 0) and, where K5a regenerates the
+// noise (C4), the z-store code.
 //
 // Same chunk length and fold order as the general kernel: rewards and counts are
 // bitwise equal to it (tests/test_gpu_small.py; the effort sum of the
