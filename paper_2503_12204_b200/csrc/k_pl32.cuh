@@ -96,6 +96,7 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
   const float4* rb = sm.rbox + s * kPl32Rp;
   float4* pb = sm.pbox + s * 64;
   const uint64_t nm2 = pack2(-m2u, -m2u);
+  D4K_CHECK(s >= 0 && s < kPl32Spc && (h == 0 || h == 1) && n_obs >= 0);
   const float4 b0 = rb[2 * lane], b1 = rb[2 * lane + 1];
   const float4 A = make_float4(fminf(b0.x, b1.x), fminf(b0.y, b1.y), fmaxf(b0.z, b1.z), fmaxf(b0.w, b1.w));
   const float4 Ai = make_float4(A.x - cmh, A.y - cmh, A.z + cmh, A.w + cmh);
@@ -128,6 +129,7 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
   for (int i = 0; i < 8; ++i) {
     const int d = 2 * i + 1 + h;
     if (cull) {
+      D4K_CHECK(lane + d < 64);
       const float4 B = pb[lane + d];
       lv[i] = __ballot_sync(full, (d < 16 || lane < 16) && (boxes_meet(b0i, B) || boxes_meet(b1i, B)));
     } else {
@@ -240,39 +242,53 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
     // ===== every 64 steps: rank the sample's robots by x (strips of D4K_PL32_STRIP), then by y
     // inside a strip, so column pairs (2l, 2l+1) are neighbours in both coordinates
     if ((t0 % D4K_PL32_RANK) == 0) {
-      if (liveA) sm.key[tid] = chunk_key(x[0], kA, 64, robotA);
-      __syncthreads();
-      if (robotA) {
-        const int me = sm.key[tid];
-        const int4* kv = reinterpret_cast<const int4*>(sm.key + sA * Rp);
-        int r = 0;
-#pragma unroll 4
-        for (int j = 0; j < Rp / 4; ++j) {
-          const int4 v = kv[j];
-          r += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
-        }
-        rA = r;
+      // keys are 31-bit unsigned (order-preserving float bits >> 1, low 6 bits = lane: unique),
+      // so "k < me" is the top bit of k − me: two instructions per key (IADD + LEA.HI into
+      // one of four independent counters) instead of a compare-select chain
+      if (liveA) {
+        int xi = __float_as_int(x[0]);
+        xi ^= (xi >> 31) & 0x7fffffff;
+        const uint32_t xu = robotA ? (((uint32_t)xi ^ 0x80000000u) >> 1) : 0x7fffffffu;  // padding sorts last
+        sm.key[tid] = (int)((xu & ~63u) | (uint32_t)kA);
       }
       __syncthreads();
-      int me = 0;
+      if (robotA) {
+        const uint32_t me = (uint32_t)sm.key[tid];
+        const uint4* kv = reinterpret_cast<const uint4*>(sm.key + sA * Rp);
+        uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll 4
+        for (int j = 0; j < Rp / 4; ++j) {
+          const uint4 v = kv[j];
+          r0 += (v.x - me) >> 31;
+          r1 += (v.y - me) >> 31;
+          r2 += (v.z - me) >> 31;
+          r3 += (v.w - me) >> 31;
+        }
+        rA = (int)((r0 + r1) + (r2 + r3));
+      }
+      __syncthreads();
+      uint32_t me = 0;
       if (liveA) {
         int yi = __float_as_int(x[1]);
         yi ^= (yi >> 31) & 0x7fffffff;
         const uint32_t yu = (uint32_t)yi ^ 0x80000000u;
-        me = robotA ? (int)(((yu >> 10) << 6) | (uint32_t)kA) : (int)(0x7fffffc0u | (uint32_t)kA);
+        me = robotA ? (((yu >> 10) << 6) | (uint32_t)kA) : (0x7fffffc0u | (uint32_t)kA);
         D4K_CHECK(rA >= 0 && rA < Rp);
-        sm.key[sA * Rp + rA] = me;
+        sm.key[sA * Rp + rA] = (int)me;
       }
       __syncthreads();
       if (robotA) {
-        const int4* kv = reinterpret_cast<const int4*>(sm.key + sA * Rp + (rA & ~(D4K_PL32_STRIP - 1)));
-        int r = rA & ~(D4K_PL32_STRIP - 1);
+        const uint4* kv = reinterpret_cast<const uint4*>(sm.key + sA * Rp + (rA & ~(D4K_PL32_STRIP - 1)));
+        uint32_t r0 = (uint32_t)(rA & ~(D4K_PL32_STRIP - 1)), r1 = 0, r2 = 0, r3 = 0;
 #pragma unroll
         for (int j = 0; j < D4K_PL32_STRIP / 4; ++j) {
-          const int4 v = kv[j];
-          r += (v.x < me) + (v.y < me) + (v.z < me) + (v.w < me);
+          const uint4 v = kv[j];
+          r0 += (v.x - me) >> 31;
+          r1 += (v.y - me) >> 31;
+          r2 += (v.z - me) >> 31;
+          r3 += (v.w - me) >> 31;
         }
-        rA = r;
+        rA = (int)((r0 + r1) + (r2 + r3));
       }
     }
     // ===== phase A: integrate the window's steps
@@ -303,6 +319,7 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
         px += KPF * kPl32RS;
         py += KPF * kPl32RS;
       }
+      D4K_CHECK(sA * Rp + rA < spc * Rp);
       sm.rbox[sA * Rp + rA] = bx;
       // state = position (velocity-input kinds): a NaN/inf state reaches the goal
       // distance, so the goal sum carries it (k23.cuh rollout_fused)
