@@ -86,7 +86,7 @@ __device__ __forceinline__ int top_bit(uint32_t v) {  // index of the highest se
 // Half h of one (sample, 32-step window) item: called by all 32 lanes of a warp,
 // lane = step.  Returns the conflict / obstacle bits (bit = column) this half finds.
 template <bool CULLC>  // CULLC: culling known on at compile time (production); else `cull_rt` decides
-__device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int h, int n_obs, float m2u, float cmh,
+__device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int h, int n_obs, float m2u, float cmh,
                                           bool cull_rt, uint64_t& conf, uint64_t& obsm) {
   const bool cull = CULLC || cull_rt;
   const unsigned full = 0xffffffffu;
@@ -98,8 +98,9 @@ __device__ __forceinline__ void item_pl32(const Pl32Smem& sm, int s, int w, int 
   const uint64_t nm2 = pack2(-m2u, -m2u);
   D4K_CHECK(s >= 0 && s < kPl32Spc && (h == 0 || h == 1) && n_obs >= 0);
   const float4 b0 = rb[2 * lane], b1 = rb[2 * lane + 1];
-  const float4 A = make_float4(fminf(b0.x, b1.x), fminf(b0.y, b1.y), fmaxf(b0.z, b1.z), fmaxf(b0.w, b1.w));
-  const float4 Ai = make_float4(A.x - cmh, A.y - cmh, A.z + cmh, A.w + cmh);
+  // the pair's union box grown by half the margin: what the partners' votes test against
+  const float4 Ai = make_float4(fminf(b0.x, b1.x) - cmh, fminf(b0.y, b1.y) - cmh, fmaxf(b0.z, b1.z) + cmh,
+                                fmaxf(b0.w, b1.w) + cmh);
   // the robots' own boxes grown by half the margin (the votes test them against
   // the partner pair's union box, not union against union: a pair whose union
   // meets only the gap between this pair's two robots is no candidate)
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(kPl32Threads, D4K_PL32_MINB) k_rollout_fitness
     // ===== phase B: this warp's half of the window's fitness
     uint64_t conf = 0, obsm = 0;
     if (mB < p.M) {
-      item_pl32<LEAN>(sm, sB, wB, hB, p.n_obs, p.margin_sq, 0.5f * p.cull_margin, p.cull != 0, conf, obsm);
+      item_pl32<LEAN>(sm, sB, hB, p.n_obs, p.margin_sq, 0.5f * p.cull_margin, p.cull != 0, conf, obsm);
       if (hB == 1) sm.msk[sB * 32 + lane] = make_uint4(lo32(conf), hi32(conf), lo32(obsm), hi32(obsm));
     }
     __syncthreads();
