@@ -48,6 +48,8 @@ def _cases():
                              (10, 4)),
         "diffdrive_R64_T48": (_square(64, 12.0, 6, kind=S.DIFFDRIVE, horizon=48, robot_radius=0.2, n_obs=7), 512, 10,
                               (10,)),
+        "R34_T5_tiny_horizon": (_square(34, 8.0, 9, horizon=5, robot_radius=0.2, n_obs=2), 300, 10, (10,)),
+        "R64_T1_single_step": (_square(64, 8.0, 10, horizon=1, robot_radius=0.2), 257, 10, (10,)),
         "holo2d_R36_T70": (_square(36, 8.0, 7, kind=S.HOLO2D, horizon=70, robot_radius=0.2, n_obs=3), 600, 10, (10, 5)),
     }
 

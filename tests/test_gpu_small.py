@@ -44,6 +44,7 @@ def _cases():
     out["holo3d_R7_T21_O3"] = (_square(7, 4.0, 3, S.HOLO3D, horizon=21, robot_radius=0.3, n_obs=3), 500, 10, (10, 2))
     out["holo3dvel_R12_T64_O9"] = (_square(12, 4.0, 4, S.HOLO3D_VEL, horizon=64, robot_radius=0.3, n_obs=9), 640, 10, (5,))
     out["unicycle_R5_T17"] = (_square(5, 3.0, 5, S.UNICYCLE, horizon=17, robot_radius=0.25, n_obs=1), 333, 10, (10, 1))
+    out["holo2dvel_R16_T3"] = (_square(16, 4.0, 7, S.HOLO2D_VEL, horizon=3, robot_radius=0.2, n_obs=1), 8192, 10, (10,))
     out["holo2dvel_R9_dense"] = (_square(9, 2.0, 6, S.HOLO2D_VEL, horizon=40, robot_radius=0.2, n_obs=4), 2048, 10, (10,))
     return out
 
