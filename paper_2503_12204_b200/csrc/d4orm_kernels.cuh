@@ -1064,7 +1064,10 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree_par(const S* __restrict
   extern __shared__ __align__(16) unsigned char tree_smem[];
   S* roots = reinterpret_cast<S*>(tree_smem);
   const int EB = kThreads / P;
-  const int el = threadIdx.x / P, j = threadIdx.x % P;
+  // element index fastest: a warp reads 32 consecutive elements of one partial row (one
+  // 128-byte line per load; with the block index fastest a warp touched 8 rows × 16 bytes),
+  // and roots are stored [block][element] so neither pass has bank conflicts
+  const int el = threadIdx.x % EB, j = threadIdx.x / EB;
   const int64_t e = (int64_t)blockIdx.x * EB + el;
   const int64_t nblk = nchunks / 8;
   if (e < elems) {
@@ -1072,7 +1075,7 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree_par(const S* __restrict
       S v8[8];  // eight loads in flight
 #pragma unroll
       for (int q = 0; q < 8; ++q) v8[q] = partial[(8 * b + q) * elems + e];
-      roots[(size_t)el * nblk + b] =
+      roots[(size_t)b * EB + el] =
           xadd(xadd(xadd(v8[0], v8[1]), xadd(v8[2], v8[3])), xadd(xadd(v8[4], v8[5]), xadd(v8[6], v8[7])));
     }
   }
@@ -1081,7 +1084,7 @@ __global__ void __launch_bounds__(kThreads) k_wmean_tree_par(const S* __restrict
   S stack[40];
   int top = 0;
   for (int64_t b = 0; b < nblk; ++b) {
-    S v = roots[(size_t)el * nblk + b];
+    S v = roots[(size_t)b * EB + el];
     for (int64_t k = b; k & 1; k >>= 1) v = xadd(stack[--top], v);  // merge equal-size subtrees
     D4K_CHECK(top >= 0 && top < 40);
     stack[top++] = v;
