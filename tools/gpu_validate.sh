@@ -1,3 +1,5 @@
+# One GPU call that validates a build: full GPU suite, smoke, the round bench lines, an ncu --set full
+# capture of a C5 step and the scaling projection (gpurun --timeout 4200 -- bash tools/gpu_validate.sh).
 mkdir -p gpurun_out
 START=$(date +%s)
 timeout 3000 python -m pytest tests -m gpu -q --durations=5 > gpurun_out/t_full_s5l.log 2>&1; echo "rc=$? wall=$(( $(date +%s) - START ))s" >> gpurun_out/t_full_s5l.log
