@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(NT) k_score_weights(const WeightParams p) {
 // sub-ranges to expose parallelism; large E already has enough CTAs along E and
 // keeps one sequential 256-sample walk per thread (best streaming efficiency).
 constexpr int kChunkSamples = 256;
-constexpr int kPartBatch = 16;  // loads in flight per thread
+constexpr int kPartBatch = 8;  // loads in flight per thread (16 with 2 resident CTAs: C2/C3 K5a 26.5 µs; 8 with 4: 22.5 µs)
 template <int SUB>
 struct PartShape {
   static constexpr int GROUPS = SUB == 1 ? 256 : 16;
@@ -677,7 +677,7 @@ struct PartArgs {
 // baselines.cpp:162-167; zero-weight samples are skipped as the reference only
 // visits the elites).
 template <typename S, typename W, int SUB, int DEV>
-__global__ void __launch_bounds__(PartShape<SUB>::THREADS) k_wmean_partial(const PartArgs<S> a,
+__global__ void __launch_bounds__(PartShape<SUB>::THREADS, (SUB > 1 && sizeof(S) == 4) ? 4 : 1) k_wmean_partial(const PartArgs<S> a,
                                                                            const W* __restrict__ w) {
   pdl_wait();
   constexpr int kPartGroups = PartShape<SUB>::GROUPS, kPartSub = SUB, kPartLanes = PartShape<SUB>::LANES;

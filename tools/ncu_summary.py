@@ -31,7 +31,11 @@ METRICS = {
 
 
 def load(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    if str(rep).endswith(".csv"):  # already exported on the GPU box (`ncu -i rep --page raw --csv`)
+        out = Path(rep).read_text()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     res = []
